@@ -1,0 +1,121 @@
+/*
+ * asdsm_b200.h -- C-ABI of the B200-native ASDSM solver (libasdsm_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in any signature (streams are
+ * passed as void*).  Each entry point names the reference interface it replaces
+ * (reference: proj/include/asdsm/*.hpp of arxiv/paper_2303_01163).  Errors are returned as
+ * status codes that mirror the reference's exception classes (errors.hpp:8-66); the
+ * message of the last failure on the calling thread is available from asdsm_last_error().
+ *
+ * Array layouts are the reference's: every mesh kind is linearized axis-0 fastest over
+ * 1-based interior indices (mesh.hpp:72-75), the holes kind block by block (mesh.hpp:150-154).
+ */
+#ifndef ASDSM_B200_H
+#define ASDSM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASDSM_B200_ABI_VERSION 1
+
+/* Status codes <-> errors.hpp exception classes. */
+enum asdsm_status {
+  ASDSM_OK = 0,
+  ASDSM_ERROR = 1,               /* asdsm::Error                               */
+  ASDSM_DIVISIBILITY_ERROR = 2,  /* asdsm::DivisibilityError  (errors.hpp:15) */
+  ASDSM_DEGENERATE_ERROR = 3,    /* asdsm::DegenerateError    (errors.hpp:21) */
+  ASDSM_INDEX_OUT_OF_RANGE = 4,  /* asdsm::IndexOutOfRange    (errors.hpp:25) */
+  ASDSM_NOT_A_SUBMESH = 5,       /* asdsm::NotASubmesh        (errors.hpp:31) */
+  ASDSM_INVALID_KIND = 6,        /* asdsm::InvalidKind        (errors.hpp:36) */
+  ASDSM_DIMENSION_MISMATCH = 7,  /* asdsm::DimensionMismatch  (errors.hpp:40) */
+  ASDSM_SINGULAR_MATRIX = 8,     /* asdsm::SingularMatrix     (errors.hpp:44) */
+  ASDSM_SKELETON_NOT_HOLLOW = 9, /* asdsm::SkeletonNotHollow  (errors.hpp:49) */
+  ASDSM_ZERO_NORM_SOLUTION = 10, /* asdsm::ZeroNormSolution   (errors.hpp:55) */
+  ASDSM_UNKNOWN_EXAMPLE = 11,    /* asdsm::UnknownExample     (errors.hpp:59) */
+  ASDSM_NO_EXACT_SOLUTION = 12,  /* asdsm::NoExactSolution    (errors.hpp:63) */
+  ASDSM_UNSUPPORTED = 13,        /* configuration outside the B200 path's scope */
+  ASDSM_CUDA_FAILURE = 14        /* CUDA runtime failure (no GPU, OOM, ...)     */
+};
+
+/* Stop reasons of IterationState::stop_reason (solver.hpp:53). */
+enum asdsm_stop { ASDSM_STOP_TOL = 1, ASDSM_STOP_STAGNATION = 2, ASDSM_STOP_MAX_ITER = 3 };
+
+typedef struct asdsm_plan asdsm_plan;       /* SolverContext (solver.hpp:114-155), device-resident */
+typedef struct asdsm_problem asdsm_problem; /* ProblemSpec (fdm.hpp:18-30), host-side catalogue   */
+
+/* IterateOptions (solver.hpp:56-68). */
+typedef struct {
+  double tol;               /* relative to ||b||_2 (absolute when b == 0); default 1e-12 */
+  int32_t max_iter;         /* default 20                                                */
+  int32_t stagnation_window;/* 0 disables; default 3                                     */
+  double stagnation_ratio;  /* default 0.99                                              */
+  double subsample;         /* must be 0 on this path (all rows)                         */
+  uint64_t rng_seed;        /* default 0                                                 */
+} asdsm_iterate_options;
+
+const char* asdsm_last_error(void);
+int asdsm_abi_version(void);
+void asdsm_default_options(asdsm_iterate_options* o);
+
+/* ---- problems (problems.hpp:20 make_problem, example_mesh; fdm.hpp:44 assemble_rhs) ---- */
+/* Reference example `example` (1..4), `setting` (1..2): problems.cpp:114-141. */
+int asdsm_problem_example(int example, int setting, asdsm_problem** out);
+/* BASELINE.json config id (0..4) with its seeded synthetic source. */
+int asdsm_problem_config(int config_id, uint64_t seed, asdsm_problem** out);
+void asdsm_problem_destroy(asdsm_problem* p);
+/* dim, time-dependence, constant coefficients (alpha/beta have 3 entries), exact available. */
+int asdsm_problem_info(const asdsm_problem* p, int* dim, int* time_dependent, int* constant_coeffs,
+                       double* alpha, double* beta, int* has_exact);
+/* Mesh of a BASELINE config (fine/coarse counts, 3 entries each) and its iteration budget. */
+int asdsm_config_mesh(int config_id, int* dim, int* fine_counts, int* coarse_counts, int* time_axis,
+                      int* iterations);
+/* assemble_rhs (fdm.hpp:44-46) on the tensor kind with coarse mask `mask`, host output. */
+int asdsm_assemble_rhs(const asdsm_problem* p, int dim, const int* fine_counts, const int* coarse_counts,
+                       int time_axis, unsigned mask, double* out);
+/* exact solution samples on the fine mesh (problems.hpp:29 error_norms' samples). */
+int asdsm_sample_exact(const asdsm_problem* p, int dim, const int* fine_counts, const int* coarse_counts,
+                       int time_axis, double* out);
+
+/* ---- plan (MeshConfig::create mesh.hpp:68 + SolverContext ctor solver.hpp:116) ---------- */
+/* Constant per-axis coefficients alpha[3], beta[3] (spatial axes; time axis ignored). */
+int asdsm_plan_create(int dim, const int* fine_counts, const int* coarse_counts, int time_axis,
+                      const double* alpha, const double* beta, asdsm_plan** out);
+void asdsm_plan_destroy(asdsm_plan* plan);
+/* MeshConfig::point_count (mesh.hpp:72) for a tensor kind (coarse mask) or the holes kind. */
+int asdsm_point_count(const asdsm_plan* plan, unsigned coarse_mask, int holes, int64_t* out);
+/* build_projector(...).index_map() (mesh.hpp:148): map from kind `from_mask` to kind
+ * `to_mask` (or the holes kind when to_holes != 0); computed on the GPU; host output. */
+int asdsm_projector_map(asdsm_plan* plan, unsigned from_mask, unsigned to_mask, int to_holes, int64_t* out);
+
+/* RhsBundle (solver.hpp:37-42) + optional exact samples (nullable); host or device memory.
+ * b_slab[a] lives on the kind coarse along axis a. */
+int asdsm_set_bundle(asdsm_plan* plan, const double* b_fine, const double* const* b_slab,
+                     const double* b_coarse, const double* exact, int on_device);
+
+/* asdsm_iterate (solver.hpp:161-163).  Host outputs (all nullable): history rows of
+ * (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms), the final iterate u and residual r. */
+int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* history, int* nrec,
+                  int* stop_code, double* u_out, double* r_out);
+/* Same solve fully on `stream` (cudaStream_t as void*, NULL = legacy): no host sync. */
+int asdsm_iterate_async(asdsm_plan* plan, const asdsm_iterate_options* opts, void* stream);
+/* After asdsm_iterate_async: history/outputs to host (synchronizes the stream). */
+int asdsm_fetch(asdsm_plan* plan, void* stream, double* history, int* nrec, int* stop_code, double* u_out,
+                double* r_out);
+/* Device pointer of the current iterate (valid until the next call on the plan). */
+int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev);
+/* Kernels this library launched during the last iterate call. */
+int64_t asdsm_last_launch_count(const asdsm_plan* plan);
+
+/* ---- single operations for parity tests (host arrays) ------------------------------- */
+int asdsm_residual(asdsm_plan* plan, const double* u, const double* b, double* r);     /* fdm.hpp:50 */
+int asdsm_initial_guess(asdsm_plan* plan, double* u_out);                              /* solver.hpp:132 (smooth) */
+int asdsm_error_guess(asdsm_plan* plan, const double* r, uint64_t seed, double* e_out); /* solver.hpp:135 */
+int asdsm_optimal_scaling(asdsm_plan* plan, const double* r, const double* e, double* s_out); /* solver.hpp:109 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASDSM_B200_H */

@@ -1,0 +1,306 @@
+// C-ABI layer (include/asdsm_b200.h) over the B200 Solver.  Thin: argument validation,
+// error-code translation, host<->device copies for the host-pointer entry points.
+#include "../../include/asdsm_b200.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/asdsm_problems.hpp"
+#include "assemble.hpp"
+#include "solver.hpp"
+
+using namespace asdsm_b200;
+
+struct asdsm_plan {
+  std::unique_ptr<Solver> solver;
+  cudaStream_t stream = nullptr;
+  int max_iter_run = 0;
+};
+
+struct asdsm_problem {
+  asdsm_cat::Problem p;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ASDSM_OK;
+  } catch (const AsdsmError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return ASDSM_CUDA_FAILURE;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return ASDSM_UNKNOWN_EXAMPLE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ASDSM_ERROR;
+  }
+}
+
+Mesh mesh_from(int dim, const int* nf, const int* nc, int time_axis) { return Mesh::create(dim, nf, nc, time_axis); }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* asdsm_last_error(void) { return g_last_error.c_str(); }
+int asdsm_abi_version(void) { return ASDSM_B200_ABI_VERSION; }
+
+void asdsm_default_options(asdsm_iterate_options* o) {
+  o->tol = 1e-12;
+  o->max_iter = 20;
+  o->stagnation_window = 3;
+  o->stagnation_ratio = 0.99;
+  o->subsample = 0.0;
+  o->rng_seed = 0;
+}
+
+int asdsm_problem_example(int example, int setting, asdsm_problem** out) {
+  return guarded([&] {
+    if (example < 1 || example > 4 || (setting != 1 && setting != 2))
+      throw AsdsmError(kUnknownExample, "example must be 1..4 and setting 1 or 2");
+    auto* p = new asdsm_problem;
+    p->p = asdsm_cat::reference_example(example, setting);
+    *out = p;
+  });
+}
+
+int asdsm_problem_config(int config_id, uint64_t seed, asdsm_problem** out) {
+  return guarded([&] {
+    if (config_id < 0 || config_id >= asdsm_cat::kNumBaselineConfigs)
+      throw AsdsmError(kUnknownExample, "config id must be 0..4");
+    auto* p = new asdsm_problem;
+    p->p = asdsm_cat::baseline_problem(config_id, seed);
+    *out = p;
+  });
+}
+
+void asdsm_problem_destroy(asdsm_problem* p) { delete p; }
+
+int asdsm_problem_info(const asdsm_problem* p, int* dim, int* time_dependent, int* constant_coeffs, double* alpha,
+                       double* beta, int* has_exact) {
+  return guarded([&] {
+    *dim = p->p.dim;
+    *time_dependent = p->p.time_dependent;
+    *constant_coeffs = p->p.constant_coeffs;
+    for (int a = 0; a < 3; ++a) {
+      alpha[a] = p->p.alpha_c[static_cast<size_t>(a)];
+      beta[a] = p->p.beta_c[static_cast<size_t>(a)];
+    }
+    *has_exact = static_cast<bool>(p->p.exact);
+  });
+}
+
+int asdsm_config_mesh(int config_id, int* dim, int* fine_counts, int* coarse_counts, int* time_axis, int* iterations) {
+  return guarded([&] {
+    if (config_id < 0 || config_id >= asdsm_cat::kNumBaselineConfigs)
+      throw AsdsmError(kUnknownExample, "config id must be 0..4");
+    const auto m = asdsm_cat::baseline_mesh(config_id);
+    *dim = m.dim;
+    for (int a = 0; a < 3; ++a) {
+      fine_counts[a] = m.nf[static_cast<size_t>(a)];
+      coarse_counts[a] = m.nc[static_cast<size_t>(a)];
+    }
+    *time_axis = m.time_axis;
+    *iterations = m.iterations;
+  });
+}
+
+int asdsm_assemble_rhs(const asdsm_problem* p, int dim, const int* fine_counts, const int* coarse_counts, int time_axis,
+                       unsigned mask, double* out) {
+  return guarded([&] {
+    const Mesh m = mesh_from(dim, fine_counts, coarse_counts, time_axis);
+    if (p->p.dim != dim) throw AsdsmError(kDimensionMismatch, "problem/mesh dimension mismatch");
+    if (p->p.time_dependent != (time_axis >= 0))
+      throw AsdsmError(kDimensionMismatch, "problem and mesh disagree about a time axis");
+    if (mask >= (1u << dim)) throw AsdsmError(kIndexOutOfRange, "mask out of range");
+    assemble_rhs(m, mask, p->p, out);
+  });
+}
+
+int asdsm_sample_exact(const asdsm_problem* p, int dim, const int* fine_counts, const int* coarse_counts, int time_axis,
+                       double* out) {
+  return guarded([&] {
+    if (!p->p.exact) throw AsdsmError(kNoExactSolution, "problem has no exact solution attached");
+    const Mesh m = mesh_from(dim, fine_counts, coarse_counts, time_axis);
+    sample_exact(m, p->p, out);
+  });
+}
+
+int asdsm_plan_create(int dim, const int* fine_counts, const int* coarse_counts, int time_axis, const double* alpha,
+                      const double* beta, asdsm_plan** out) {
+  return guarded([&] {
+    const Mesh m = mesh_from(dim, fine_counts, coarse_counts, time_axis);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw CudaError("no CUDA device: the B200 path has no CPU fallback");
+    auto plan = std::make_unique<asdsm_plan>();
+    ASDSM_CUDA_CHECK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    plan->solver = std::make_unique<Solver>(m, alpha, beta);
+    *out = plan.release();
+  });
+}
+
+void asdsm_plan_destroy(asdsm_plan* plan) {
+  if (!plan) return;
+  if (plan->stream) cudaStreamSynchronize(plan->stream);
+  plan->solver.reset();
+  if (plan->stream) cudaStreamDestroy(plan->stream);
+  delete plan;
+}
+
+int asdsm_point_count(const asdsm_plan* plan, unsigned coarse_mask, int holes, int64_t* out) {
+  return guarded([&] {
+    const Mesh& m = plan->solver->mesh();
+    if (holes) {
+      *out = m.hole_count();
+      return;
+    }
+    if (coarse_mask >= (1u << m.dim)) throw AsdsmError(kIndexOutOfRange, "from_mask: mask out of range");
+    *out = m.point_count(coarse_mask);
+  });
+}
+
+int asdsm_projector_map(asdsm_plan* plan, unsigned from_mask, unsigned to_mask, int to_holes, int64_t* out) {
+  return guarded([&] {
+    const Mesh& m = plan->solver->mesh();
+    const unsigned full = (1u << m.dim) - 1u;
+    if (from_mask > full || (!to_holes && to_mask > full)) throw AsdsmError(kIndexOutOfRange, "mask out of range");
+    i64 count = 0;
+    if (to_holes) {
+      if (from_mask != 0) throw AsdsmError(kNotASubmesh, "holes are a subset of the fine mesh only");
+      count = m.hole_count();
+    } else {
+      if ((from_mask & to_mask) != from_mask) throw AsdsmError(kNotASubmesh, "target is not a sub-mesh of the source");
+      count = m.point_count(to_mask);
+    }
+    long long* d = nullptr;
+    ASDSM_CUDA_CHECK(cudaMalloc(&d, static_cast<size_t>(count) * sizeof(long long) + 8));
+    if (to_holes)
+      launch_hole_map(plan->solver->mesh_dev(), d, count, plan->stream);
+    else
+      launch_projector_map(plan->solver->mesh_dev(), from_mask, to_mask, d, count, plan->stream);
+    cudaError_t e = cudaMemcpyAsync(out, d, static_cast<size_t>(count) * sizeof(long long), cudaMemcpyDeviceToHost,
+                                    plan->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(plan->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) throw CudaError(cudaGetErrorString(e));
+  });
+}
+
+int asdsm_set_bundle(asdsm_plan* plan, const double* b_fine, const double* const* b_slab, const double* b_coarse,
+                     const double* exact, int on_device) {
+  return guarded([&] {
+    plan->solver->set_bundle(b_fine, b_slab, b_coarse, exact, on_device != 0, plan->stream);
+    if (!on_device) ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+static RunOptions to_run(const asdsm_iterate_options* o) {
+  RunOptions r;
+  if (o) {
+    r.tol = o->tol;
+    r.max_iter = o->max_iter;
+    r.stagnation_window = o->stagnation_window;
+    r.stagnation_ratio = o->stagnation_ratio;
+    r.subsample = o->subsample;
+    r.rng_seed = o->rng_seed;
+  }
+  if (r.subsample != 0.0) throw AsdsmError(kUnsupported, "subsample > 0 is not supported on the B200 path yet");
+  if (r.max_iter < 0) r.max_iter = 0;
+  return r;
+}
+
+int asdsm_iterate_async(asdsm_plan* plan, const asdsm_iterate_options* opts, void* stream) {
+  return guarded([&] {
+    const RunOptions r = to_run(opts);
+    plan->max_iter_run = r.max_iter;
+    plan->solver->run(r, stream ? as_stream(stream) : plan->stream);
+  });
+}
+
+int asdsm_fetch(asdsm_plan* plan, void* stream, double* history, int* nrec, int* stop_code, double* u_out, double* r_out) {
+  return guarded([&] {
+    cudaStream_t s = stream ? as_stream(stream) : plan->stream;
+    std::vector<double> rows;
+    int stop = 0;
+    const int n = plan->solver->history(rows, stop, s);
+    if (history && n > 0) std::memcpy(history, rows.data(), rows.size() * sizeof(double));
+    if (nrec) *nrec = n;
+    if (stop_code) *stop_code = stop;
+    const size_t bytes = static_cast<size_t>(plan->solver->fine_size()) * sizeof(double);
+    if (u_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_out, plan->solver->u_current(s), bytes, cudaMemcpyDeviceToHost, s));
+    if (r_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(r_out, plan->solver->r_current(s), bytes, cudaMemcpyDeviceToHost, s));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* history, int* nrec, int* stop_code,
+                  double* u_out, double* r_out) {
+  const int rc = asdsm_iterate_async(plan, opts, nullptr);
+  if (rc != ASDSM_OK) return rc;
+  return asdsm_fetch(plan, nullptr, history, nrec, stop_code, u_out, r_out);
+}
+
+int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev) {
+  return guarded([&] { *u_dev = plan->solver->u_current(stream ? as_stream(stream) : plan->stream); });
+}
+
+int64_t asdsm_last_launch_count(const asdsm_plan* plan) { return plan->solver->last_launches(); }
+
+int asdsm_residual(asdsm_plan* plan, const double* u, const double* b, double* r) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const size_t bytes = static_cast<size_t>(S.fine_size()) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.u_buffer(0), u, bytes, cudaMemcpyHostToDevice, plan->stream));
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.e_buffer(), b, bytes, cudaMemcpyHostToDevice, plan->stream));
+    S.residual(S.u_buffer(0), S.e_buffer(), S.r_buffer(0), plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(r, S.r_buffer(0), bytes, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_initial_guess(asdsm_plan* plan, double* u_out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const size_t bytes = static_cast<size_t>(S.fine_size()) * sizeof(double);
+    S.initial_guess(S.u_buffer(0), 0, plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_out, S.u_buffer(0), bytes, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_error_guess(asdsm_plan* plan, const double* r, uint64_t seed, double* e_out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const size_t bytes = static_cast<size_t>(S.fine_size()) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.r_buffer(0), r, bytes, cudaMemcpyHostToDevice, plan->stream));
+    S.error_guess(S.r_buffer(0), seed, S.e_buffer(), plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(e_out, S.e_buffer(), bytes, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_optimal_scaling(asdsm_plan* plan, const double* r, const double* e, double* s_out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const size_t bytes = static_cast<size_t>(S.fine_size()) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.r_buffer(0), r, bytes, cudaMemcpyHostToDevice, plan->stream));
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.e_buffer(), e, bytes, cudaMemcpyHostToDevice, plan->stream));
+    *s_out = S.optimal_scaling(S.r_buffer(0), S.e_buffer(), plan->stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// Shared device/host definitions for the ASDSM B200 library.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace asdsm_b200 {
+
+using i64 = long long;
+
+#define ASDSM_CUDA_CHECK(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw ::asdsm_b200::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Complex arithmetic for mode spaces of operators whose 1D factor has complex eigenvalues
+// (cell Peclet number > 2 on a coarse step).  Only the ops the solver needs.
+struct cplx {
+  double re, im;
+};
+#ifndef __CUDACC__
+#ifndef __host__
+#define __host__
+#define __device__
+#endif
+#endif
+__host__ __device__ inline cplx cmake(double r, double i) { return cplx{r, i}; }
+__host__ __device__ inline cplx operator+(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+__host__ __device__ inline cplx operator-(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+__host__ __device__ inline cplx operator*(cplx a, cplx b) {
+  return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__host__ __device__ inline cplx operator*(double a, cplx b) { return cplx{a * b.re, a * b.im}; }
+
+template <typename T>
+__host__ __device__ inline T zero_of();
+template <>
+__host__ __device__ inline double zero_of<double>() { return 0.0; }
+template <>
+__host__ __device__ inline cplx zero_of<cplx>() { return cplx{0.0, 0.0}; }
+
+__host__ __device__ inline double real_part(double x) { return x; }
+__host__ __device__ inline double real_part(cplx x) { return x.re; }
+__host__ __device__ inline void fma_acc(double& acc, double a, double b) { acc = fma(a, b, acc); }
+__host__ __device__ inline void fma_acc(cplx& acc, cplx a, cplx b) {
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(-a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(a.im, b.re, acc.im);
+}
+__host__ __device__ inline void fma_acc(cplx& acc, double a, cplx b) {
+  acc.re = fma(a, b.re, acc.re);
+  acc.im = fma(a, b.im, acc.im);
+}
+__host__ __device__ inline void fma_acc(cplx& acc, cplx a, double b) {
+  acc.re = fma(a.re, b, acc.re);
+  acc.im = fma(a.im, b, acc.im);
+}
+
+// Non-contracted arithmetic: the residual/stencil kernels reproduce the reference's
+// rounding sequence (CSR row dot in column order, proj/src/sparse.cpp:66-72) exactly.
+#ifdef __CUDACC__
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+#endif
+
+constexpr int kMaxDim = 3;
+
+// Host-side count of kernels this library launched (reported as gpu_launches by bench.py).
+extern long long g_kernel_launches;
+constexpr int kNumSms = 148;
+
+}  // namespace asdsm_b200

@@ -1,0 +1,674 @@
+// ASDSM iteration kernels for sm_100a (fp64).
+//
+// Every fine-grid pass reproduces the reference's arithmetic order so the residual and the
+// merged skeleton are bitwise what proj/src computes for the same inputs:
+//   A*u row dot    : proj/src/sparse.cpp:66-72 over the CSR order of fdm.cpp:110-117
+//   residual       : proj/src/fdm.cpp:221-230
+//   spline         : proj/src/spline.cpp:9-57
+//   skeleton merge : proj/src/solver.cpp:154-196
+//   hole rhs       : proj/src/solver.cpp:414-432
+//   step control   : proj/src/solver.cpp:447-484, 621-677
+// Reductions use a fixed grid and a fixed combine tree, so results are run-to-run
+// deterministic (the reference's serial order is not reproduced).
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace asdsm_b200 {
+
+long long g_kernel_launches = 0;
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-level reduction of up to 4 values (sum, max, sum, max); thread 0 writes partials.
+__device__ void block_reduce4(double s0, double m1, double s2, double m3, double* partials) {
+  __shared__ double sh[4][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  s0 = warp_sum(s0);
+  m1 = warp_max(m1);
+  s2 = warp_sum(s2);
+  m3 = warp_max(m3);
+  if (lane == 0) {
+    sh[0][w] = s0;
+    sh[1][w] = m1;
+    sh[2][w] = s2;
+    sh[3][w] = m3;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    s0 = lane < nw ? sh[0][lane] : 0.0;
+    m1 = lane < nw ? sh[1][lane] : 0.0;
+    s2 = lane < nw ? sh[2][lane] : 0.0;
+    m3 = lane < nw ? sh[3][lane] : 0.0;
+    s0 = warp_sum(s0);
+    m1 = warp_max(m1);
+    s2 = warp_sum(s2);
+    m3 = warp_max(m3);
+    if (lane == 0) {
+      partials[0 * kRedBlocks + blockIdx.x] = s0;
+      partials[1 * kRedBlocks + blockIdx.x] = m1;
+      partials[2 * kRedBlocks + blockIdx.x] = s2;
+      partials[3 * kRedBlocks + blockIdx.x] = m3;
+    }
+  }
+}
+
+struct StencilArgs {
+  const double* u0;
+  const double* u1;
+  const double* e;
+  const double* b;
+  double* uo0;
+  double* uo1;
+  double* ro0;
+  double* ro1;
+  const double* exact;
+  FineGeom g;
+  Stencil st;
+  double* partials;
+  DevState* state;
+};
+
+// A*v at fine point (i,j,k) in the CSR column order of fdm.cpp:110-117, no contraction.
+// V(q, axis, dir) returns v at neighbour q (axis -1 = the point itself).
+template <int DIM, typename F>
+__device__ __forceinline__ double apply_row(const FineGeom& g, const Stencil& st, i64 p, int i, int j, int k, F V,
+                                            double& vp) {
+  double acc = 0.0;
+  if (DIM == 3 && k > 0) acc = add_rn(acc, mul_rn(st.left[2], V(p - g.stride[2], 2, -1)));
+  if (j > 0) acc = add_rn(acc, mul_rn(st.left[1], V(p - g.stride[1], 1, -1)));
+  if (i > 0) acc = add_rn(acc, mul_rn(st.left[0], V(p - 1, 0, -1)));
+  vp = V(p, -1, 0);
+  acc = add_rn(acc, mul_rn(st.diag, vp));
+  if (i < g.ext[0] - 1 && st.has_right[0]) acc = add_rn(acc, mul_rn(st.right[0], V(p + 1, 0, 1)));
+  if (j < g.ext[1] - 1 && st.has_right[1]) acc = add_rn(acc, mul_rn(st.right[1], V(p + g.stride[1], 1, 1)));
+  if (DIM == 3 && k < g.ext[2] - 1 && st.has_right[2])
+    acc = add_rn(acc, mul_rn(st.right[2], V(p + g.stride[2], 2, 1)));
+  return acc;
+}
+
+// residual (UPDATE=false): r[cur] = b - A u[cur]
+// update   (UPDATE=true) : u[1-cur] = u[cur] + s e ; r[1-cur] = b - A u[1-cur]
+// plus per-block partials of sum r^2, max |r|, sum d^2, max |d| (d = u - exact).
+template <int DIM, bool UPDATE>
+__global__ void __launch_bounds__(kRedThreads) stencil_kernel(StencilArgs a) {
+  const DevState* S = a.state;
+  if (!S->active) return;
+  double s = 0.0;
+  if (UPDATE) {
+    s = S->s;
+    if (s == 0.0) return;
+  }
+  const int cur = S->cur;
+  const double* __restrict__ u = cur ? a.u1 : a.u0;
+  double* __restrict__ uo = UPDATE ? (cur ? a.uo0 : a.uo1) : nullptr;
+  double* __restrict__ ro = UPDATE ? (cur ? a.ro0 : a.ro1) : (cur ? a.ro1 : a.ro0);
+  const double* __restrict__ e = a.e;
+  const FineGeom& g = a.g;
+  const int nseg = (g.ext[0] + blockDim.x - 1) / blockDim.x;
+  const i64 rows = static_cast<i64>(g.ext[1]) * (DIM == 3 ? g.ext[2] : 1);
+  const i64 items = rows * nseg;
+  double ssq = 0.0, rmax = 0.0, esq = 0.0, emax = 0.0;
+  auto V = [&](i64 q, int, int) -> double {
+    if (UPDATE) return add_rn(u[q], mul_rn(s, e[q]));
+    return u[q];
+  };
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    const i64 row = it / nseg;
+    const int i = static_cast<int>((it % nseg) * blockDim.x + threadIdx.x);
+    if (i >= g.ext[0]) continue;
+    const int j = static_cast<int>(row % g.ext[1]);
+    const int k = DIM == 3 ? static_cast<int>(row / g.ext[1]) : 0;
+    const i64 p = i + row * g.stride[1];
+    double vp;
+    const double av = apply_row<DIM>(g, a.st, p, i, j, k, V, vp);
+    const double r = sub_rn(a.b[p], av);
+    ro[p] = r;
+    if (UPDATE) uo[p] = vp;
+    ssq += r * r;
+    rmax = fmax(rmax, fabs(r));
+    if (a.exact) {
+      const double d = vp - a.exact[p];
+      esq += d * d;
+      emax = fmax(emax, fabs(d));
+    }
+  }
+  block_reduce4(ssq, rmax, esq, emax, a.partials);
+}
+
+struct DotArgs {
+  const double* e;
+  const double* r0;
+  const double* r1;
+  FineGeom g;
+  Stencil st;
+  double* partials;
+  DevState* state;
+};
+
+// w = A e (all rows, sparse.cpp:49-58 order); partial <r, w> and <w, w> (solver.cpp:456-461).
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads) ae_dots_kernel(DotArgs a) {
+  const DevState* S = a.state;
+  if (!S->active || !S->have_e) return;
+  const double* __restrict__ r = S->cur ? a.r1 : a.r0;
+  const double* __restrict__ e = a.e;
+  const FineGeom& g = a.g;
+  const int nseg = (g.ext[0] + blockDim.x - 1) / blockDim.x;
+  const i64 rows = static_cast<i64>(g.ext[1]) * (DIM == 3 ? g.ext[2] : 1);
+  const i64 items = rows * nseg;
+  double num = 0.0, den = 0.0;
+  auto V = [&](i64 q, int, int) -> double { return e[q]; };
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    const i64 row = it / nseg;
+    const int i = static_cast<int>((it % nseg) * blockDim.x + threadIdx.x);
+    if (i >= g.ext[0]) continue;
+    const int j = static_cast<int>(row % g.ext[1]);
+    const int k = DIM == 3 ? static_cast<int>(row / g.ext[1]) : 0;
+    const i64 p = i + row * g.stride[1];
+    double vp;
+    const double w = apply_row<DIM>(g, a.st, p, i, j, k, V, vp);
+    num += r[p] * w;
+    den += w * w;
+  }
+  block_reduce4(num, 0.0, den, 0.0, a.partials);
+}
+
+// Restriction r -> one tensor submesh (Projector::apply with build_projector's map,
+// mesh.cpp:174-179, 226-255).
+__global__ void gather_kernel(const double* src0, const double* src1, double* dst, MeshDev m, unsigned mask, i64 count,
+                              const DevState* state) {
+  if (!state->active) return;
+  const double* src = state->cur ? src1 : src0;
+  int ext[3];
+  i64 fstride[3];
+  i64 s = 1;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = a < m.dim ? (((mask >> a) & 1u) ? m.nc[a] : m.nf[a]) : 1;
+    fstride[a] = s;
+    s *= a < m.dim ? m.nf[a] : 1;
+  }
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    i64 rem = t, f = 0;
+    for (int a = 0; a < m.dim; ++a) {
+      const int ia = static_cast<int>(rem % ext[a]);
+      rem /= ext[a];
+      const i64 fi = ((mask >> a) & 1u) ? static_cast<i64>(ia + 1) * m.n[a] - 1 : ia;
+      f += fi * fstride[a];
+    }
+    dst[t] = src[f];
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) norm_sq_kernel(const double* x, i64 n, double* partials,
+                                                             const DevState* state) {
+  if (!state->active) return;
+  double s = 0.0;
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<i64>(gridDim.x) * blockDim.x)
+    s += x[t] * x[t];
+  block_reduce4(s, 0.0, 0.0, 0.0, partials);
+}
+
+// normalize_or_throw (solver.cpp:79-84): v /= ||v||_2 element by element.
+__global__ void divide_kernel(double* x, i64 n, const double* divisor, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const double d = *divisor;
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<i64>(gridDim.x) * blockDim.x)
+    x[t] = x[t] / d;
+}
+
+// Fixed-shape reduction of the kRedBlocks partials of one slot.
+__device__ double ctrl_reduce(const double* part, bool is_max) {
+  __shared__ double sh[kRedThreads];
+  double v = is_max ? 0.0 : 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v = is_max ? fmax(v, part[i]) : v + part[i];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = is_max ? fmax(sh[threadIdx.x], sh[threadIdx.x + w]) : sh[threadIdx.x] + sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kRedThreads) ctrl_kernel(CtrlArgs c, const double* partials, DevState* S,
+                                                          double* history) {
+  if (!S->active) return;
+  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
+  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
+  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
+  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
+  if (threadIdx.x != 0) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  auto record = [&](int k, double s_hat) {
+    double* row = history + static_cast<i64>(k) * 7;
+    row[0] = k;
+    row[1] = S->res_l2;
+    row[2] = S->res_inf;
+    row[3] = S->err_max;
+    row[4] = S->err_l2;
+    row[5] = s_hat;
+    row[6] = 0.0;
+    S->nrec = k + 1;
+  };
+  switch (c.op) {
+    case kCtrlResidualK0: {
+      S->res_l2 = sqrt(s0);
+      S->res_inf = m1;
+      S->err_max = c.has_exact ? m3 : nan;
+      S->err_l2 = c.has_exact ? sqrt(s2 * c.cell) : nan;
+      record(0, nan);
+      if (S->res_l2 <= S->stop_at) {
+        S->stop = 1;
+        S->active = 0;
+      } else if (c.max_iter <= 0) {
+        S->stop = 3;
+        S->active = 0;
+      }
+      S->have_e = 1;
+      break;
+    }
+    case kCtrlInit: {
+      S->b_l2 = sqrt(s0);
+      S->stop_at = c.tol * (S->b_l2 > 0.0 ? S->b_l2 : 1.0);
+      break;
+    }
+    case kCtrlSlabNorm: {
+      const double n = sqrt(s0);
+      S->slab_norm[c.which] = n;
+      if (!(n > 0.0)) S->have_e = 0;
+      break;
+    }
+    case kCtrlStep: {
+      double s = 0.0;
+      if (S->have_e) {
+        S->num = s0;
+        S->den = s2;
+        if (s2 > 0.0) {
+          const double q = s0 / s2;
+          s = (0.0 < q) ? q : 0.0;
+        }
+      }
+      S->s = s;
+      break;
+    }
+    case kCtrlAccept: {
+      double s = S->s;
+      if (s != 0.0) {
+        const double nl2 = sqrt(s0);
+        if (nl2 > S->res_l2 * c.tol_growth) {
+          s = 0.0;
+        } else {
+          S->cur = 1 - S->cur;
+          S->res_l2 = nl2;
+          S->res_inf = m1;
+          if (c.has_exact) {
+            S->err_max = m3;
+            S->err_l2 = sqrt(s2 * c.cell);
+          }
+        }
+      }
+      S->s = s;
+      record(c.k, s);
+      if (S->res_l2 <= S->stop_at) {
+        S->stop = 1;
+      } else if (c.stagnation_window > 0 && c.k >= c.stagnation_window) {
+        const double then = history[static_cast<i64>(c.k - c.stagnation_window) * 7 + 1];
+        if (S->res_l2 > then * c.stagnation_pow) S->stop = 2;
+      }
+      if (S->stop == 0 && c.k >= c.max_iter) S->stop = 3;
+      if (S->stop != 0) S->active = 0;
+      S->have_e = 1;
+      break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- 2D skeleton --------------
+__device__ __forceinline__ double knot(const MeshDev& m, int axis, int c) {
+  if (c == 0) return 0.0;
+  if (c == m.nc[axis] + 1) return 1.0;
+  return static_cast<double>(static_cast<i64>(c) * m.n[axis]) * m.h[axis];
+}
+
+// Natural cubic spline second derivatives through (0,0), (knot_c, v_c), (1,0)
+// (zero_clamped_spline + CubicSpline ctor, spline.cpp:9-37, 58-76).  y has nc+2 entries.
+__device__ void spline_second_derivs(const MeshDev& m, int axis, const double* y, double* mm, double* diag,
+                                     double* upper, double* rhs) {
+  const int n = m.nc[axis] + 2;
+  for (int i = 0; i < n; ++i) mm[i] = 0.0;
+  if (n == 2) return;
+  const int ni = n - 2;
+  for (int i = 0; i < ni; ++i) {
+    const double x0 = knot(m, axis, i), x1 = knot(m, axis, i + 1), x2 = knot(m, axis, i + 2);
+    const double hl = __dsub_rn(x1, x0);
+    const double hr = __dsub_rn(x2, x1);
+    diag[i] = __dadd_rn(hl, hr) / 3.0;
+    upper[i] = hr / 6.0;
+    rhs[i] = __dsub_rn(__dsub_rn(y[i + 2], y[i + 1]) / hr, __dsub_rn(y[i + 1], y[i]) / hl);
+  }
+  for (int i = 1; i < ni; ++i) {
+    const double lower = __dsub_rn(knot(m, axis, i + 1), knot(m, axis, i)) / 6.0;
+    const double w = lower / diag[i - 1];
+    diag[i] = __dsub_rn(diag[i], __dmul_rn(w, upper[i - 1]));
+    rhs[i] = __dsub_rn(rhs[i], __dmul_rn(w, rhs[i - 1]));
+  }
+  mm[ni] = rhs[ni - 1] / diag[ni - 1];
+  for (int i = ni - 1; i >= 1; --i) mm[i] = __dsub_rn(rhs[i - 1], __dmul_rn(upper[i - 1], mm[i + 1])) / diag[i - 1];
+}
+
+// CubicSpline::operator() (spline.cpp:39-56) at fine index fi (1-based) along `axis` for a
+// line whose knot values are y(c), c = 0..nc+1 (y(0) = y(nc+1) = 0), second derivatives mm.
+template <typename Y>
+__device__ __forceinline__ double spline_eval(const MeshDev& m, int axis, Y y, const double* mm, int fi) {
+  const double x = static_cast<double>(fi) * m.h[axis];
+  int i = fi / m.n[axis];
+  if (i > m.nc[axis]) i = m.nc[axis];
+  const double xi = knot(m, axis, i), xi1 = knot(m, axis, i + 1);
+  const double y0 = y(i), y1 = y(i + 1), m0 = mm[i], m1 = mm[i + 1];
+  const double h = __dsub_rn(xi1, xi);
+  const double t = __dsub_rn(x, xi);
+  const double c1 = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m0), m1)) / 6.0);
+  const double c2 = m0 / 2.0;
+  const double c3 = __dsub_rn(m1, m0) / __dmul_rn(6.0, h);
+  return __dadd_rn(y0, __dmul_rn(t, __dadd_rn(c1, __dmul_rn(t, __dadd_rn(c2, __dmul_rn(t, c3))))));
+}
+
+// Phase 1: cross values u_hat (Richardson u1 + u2 - u_cc, or the seeded choice) and the
+// corrections e1 = u_hat - P u_fc, e2 = u_hat - P u_cf (solver.cpp:166-184).
+__global__ void skel2d_cc_kernel(Skel2DArgs a, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const MeshDev& m = a.m;
+  const int ncc = m.nc[0] * m.nc[1];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncc; t += gridDim.x * blockDim.x) {
+    const int I = t % m.nc[0], J = t / m.nc[0];
+    const double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
+    const double u2 = a.u_cf[I + static_cast<i64>(m.nc[0]) * ((J + 1) * m.n[1] - 1)];
+    double uh;
+    if (a.u_cc) {
+      uh = __dsub_rn(__dadd_rn(u1, u2), a.u_cc[t]);
+    } else {
+      uh = (a.coin[0] == 0) ? u2 : u1;
+    }
+    a.e1[t] = __dsub_rn(uh, u1);
+    a.e2[t] = __dsub_rn(uh, u2);
+  }
+}
+
+// Phase 2: spline second derivatives, one thread per coarse line.
+__global__ void skel2d_spline_kernel(Skel2DArgs a, double* work, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const MeshDev& m = a.m;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nlines = m.nc[1] + m.nc[0];
+  if (t >= nlines) return;
+  const int maxn = (m.nc[0] > m.nc[1] ? m.nc[0] : m.nc[1]) + 2;
+  double* y = work + static_cast<i64>(t) * 4 * maxn;
+  double* dg = y + maxn;
+  double* up = dg + maxn;
+  double* rh = up + maxn;
+  if (t < m.nc[1]) {  // line J along x through e1[:, J]
+    const int J = t;
+    const int nc = m.nc[0];
+    y[0] = 0.0;
+    for (int C = 0; C < nc; ++C) y[C + 1] = a.e1[C + static_cast<i64>(nc) * J];
+    y[nc + 1] = 0.0;
+    spline_second_derivs(m, 0, y, a.m1 + static_cast<i64>(J) * (nc + 2), dg, up, rh);
+  } else {  // line I along y through e2[I, :]
+    const int I = t - m.nc[1];
+    const int nc = m.nc[1];
+    y[0] = 0.0;
+    for (int C = 0; C < nc; ++C) y[C + 1] = a.e2[I + static_cast<i64>(m.nc[0]) * C];
+    y[nc + 1] = 0.0;
+    spline_second_derivs(m, 1, y, a.m2 + static_cast<i64>(I) * (nc + 2), dg, up, rh);
+  }
+}
+
+// Phase 3: corrected anisotropic values merged onto the skeleton points (solver.cpp:186-195):
+//   coarse-row points  : ut_fc = u_fc + S1_J(x_i)
+//   coarse-column points: ut_cf = u_cf + S2_I(y_j)
+//   cross points       : (0 + ut_fc) + ut_cf + (-ut_cf), the scatter_add sequence.
+__global__ void skel2d_write_kernel(Skel2DArgs a, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const MeshDev& m = a.m;
+  const int nc0 = m.nc[0], nc1 = m.nc[1];
+  const i64 nrow_pts = static_cast<i64>(nc1) * m.nf[0];
+  const i64 ncol_pts = static_cast<i64>(nc0) * m.nf[1];
+  auto ut_cf = [&](int I, int j) {
+    const double* mm2 = a.m2 + static_cast<i64>(I) * (nc1 + 2);
+    auto y2 = [&](int c) -> double { return (c == 0 || c == nc1 + 1) ? 0.0 : a.e2[I + static_cast<i64>(nc0) * (c - 1)]; };
+    return __dadd_rn(a.u_cf[I + static_cast<i64>(nc0) * j], spline_eval(m, 1, y2, mm2, j + 1));
+  };
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < nrow_pts + ncol_pts;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    if (t < nrow_pts) {
+      const int i = static_cast<int>(t % m.nf[0]);
+      const int J = static_cast<int>(t / m.nf[0]);
+      const int j = (J + 1) * m.n[1] - 1;
+      const double* mm1 = a.m1 + static_cast<i64>(J) * (nc0 + 2);
+      auto y1 = [&](int c) -> double { return (c == 0 || c == nc0 + 1) ? 0.0 : a.e1[(c - 1) + static_cast<i64>(nc0) * J]; };
+      const double av = __dadd_rn(a.u_fc[i + static_cast<i64>(m.nf[0]) * J], spline_eval(m, 0, y1, mm1, i + 1));
+      double val = av;
+      if ((i + 1) % m.n[0] == 0) {
+        const double bv = ut_cf((i + 1) / m.n[0] - 1, j);
+        val = __dadd_rn(__dadd_rn(av, bv), -bv);
+      }
+      a.out[i + static_cast<i64>(m.nf[0]) * j] = val;
+    } else {
+      const i64 tc = t - nrow_pts;
+      const int j = static_cast<int>(tc % m.nf[1]);
+      const int I = static_cast<int>(tc / m.nf[1]);
+      if ((j + 1) % m.n[1] == 0) continue;  // cross points are written by the row pass
+      const int i = (I + 1) * m.n[0] - 1;
+      a.out[i + static_cast<i64>(m.nf[0]) * j] = ut_cf(I, j);
+    }
+  }
+}
+
+// Hole right-hand side (solver.cpp:416-424): rhs_p = b_p - (A_ff * skeleton)_p for every
+// hole point p, written in place of the (zero) skeleton value.  Hole neighbours carry 0.
+template <int DIM>
+__global__ void hole_rhs_kernel(double* e, const double* b, FineGeom g, Stencil st, MeshDev m, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const int nseg = (g.ext[0] + blockDim.x - 1) / blockDim.x;
+  const i64 rows = static_cast<i64>(g.ext[1]) * (DIM == 3 ? g.ext[2] : 1);
+  const i64 items = rows * nseg;
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    const i64 row = it / nseg;
+    const int i = static_cast<int>((it % nseg) * blockDim.x + threadIdx.x);
+    if (i >= g.ext[0]) continue;
+    const int j = static_cast<int>(row % g.ext[1]);
+    const int k = DIM == 3 ? static_cast<int>(row / g.ext[1]) : 0;
+    const bool sk_i = (i + 1) % m.n[0] == 0, sk_j = (j + 1) % m.n[1] == 0;
+    const bool sk_k = DIM == 3 ? ((k + 1) % m.n[2] == 0) : false;
+    if (sk_i || sk_j || sk_k) continue;  // skeleton point
+    const i64 p = i + row * g.stride[1];
+    // Neighbour q is a skeleton point iff its moved coordinate lies on a coarse plane
+    // (the unmoved coordinates are hole coordinates); hole neighbours carry 0.
+    const int idx[3] = {i, j, k};
+    auto V = [&](i64 q, int axis, int dir) -> double {
+      if (axis < 0) return 0.0;
+      return ((idx[axis] + dir + 1) % m.n[axis] == 0) ? e[q] : 0.0;
+    };
+    double vp;
+    const double av = apply_row<DIM>(g, st, p, i, j, k, V, vp);
+    const double bp = b ? b[p] : 0.0;
+    e[p] = sub_rn(bp, av);
+  }
+}
+
+__global__ void dense_matvec_kernel(const double* A, const double* b, double* x, int n, const DevState* state) {
+  if (!state->active) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(A[static_cast<i64>(i) * n + j], b[j], s);
+    s = warp_sum(s);
+    if (lane == 0) x[i] = s;
+  }
+}
+
+}  // namespace
+
+void launch_stencil(int dim, bool update, const double* u0, const double* u1, const double* e, const double* b,
+                    double* uo0, double* uo1, double* ro0, double* ro1, const double* exact, const FineGeom& g,
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s) {
+  StencilArgs a{u0, u1, e, b, uo0, uo1, ro0, ro1, exact, g, st, partials, state};
+  if (dim == 2) {
+    if (update) stencil_kernel<2, true><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+    else stencil_kernel<2, false><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+  } else {
+    if (update) stencil_kernel<3, true><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+    else stencil_kernel<3, false><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+  }
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_ae_dots(int dim, const double* e, const double* r0, const double* r1, const FineGeom& g,
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s) {
+  DotArgs a{e, r0, r1, g, st, partials, state};
+  if (dim == 2) ae_dots_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+  else ae_dots_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_gather(const double* src0, const double* src1, double* dst, const MeshDev& m, unsigned mask, i64 count,
+                   DevState* state, cudaStream_t s) {
+  const int bs = 256;
+  const i64 nb = std::min<i64>((count + bs - 1) / bs, 4 * kNumSms);
+  gather_kernel<<<static_cast<unsigned>(nb), bs, 0, s>>>(src0, src1, dst, m, mask, count, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s) {
+  norm_sq_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, n, partials, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_divide(double* x, i64 n, const double* divisor, DevState* state, cudaStream_t s) {
+  const int bs = 256;
+  const i64 nb = std::min<i64>((n + bs - 1) / bs, 4 * kNumSms);
+  divide_kernel<<<static_cast<unsigned>(nb), bs, 0, s>>>(x, n, divisor, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_ctrl(const CtrlArgs& a, const double* partials, DevState* state, double* history, cudaStream_t s) {
+  ctrl_kernel<<<1, kRedThreads, 0, s>>>(a, partials, state, history);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_skeleton2d(const Skel2DArgs& a, DevState* state, cudaStream_t s) {
+  const int ncc = a.m.nc[0] * a.m.nc[1];
+  g_kernel_launches += 2;
+  skel2d_cc_kernel<<<(ncc + 255) / 256, 256, 0, s>>>(a, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  const int nlines = a.m.nc[0] + a.m.nc[1];
+  // spline work: 4 * (max nc + 2) doubles per line; lives after m2 in the same allocation
+  const int maxn = (a.m.nc[0] > a.m.nc[1] ? a.m.nc[0] : a.m.nc[1]) + 2;
+  double* work = a.m2 + static_cast<i64>(a.m.nc[0]) * (a.m.nc[1] + 2);
+  (void)maxn;
+  skel2d_spline_kernel<<<(nlines + 63) / 64, 64, 0, s>>>(a, work, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  const i64 npts = static_cast<i64>(a.m.nc[1]) * a.m.nf[0] + static_cast<i64>(a.m.nc[0]) * a.m.nf[1];
+  const i64 nb = std::min<i64>((npts + 255) / 256, 4 * kNumSms);
+  skel2d_write_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(a, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
+                     DevState* state, cudaStream_t s) {
+  if (dim == 2) hole_rhs_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
+  else hole_rhs_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_dense_matvec(const double* Ainv, const double* b, double* x, int n, DevState* state, cudaStream_t s) {
+  dense_matvec_kernel<<<(n + 7) / 8, 256, 0, s>>>(Ainv, b, x, n, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+}  // namespace asdsm_b200
+
+namespace asdsm_b200 {
+namespace {
+
+__global__ void projector_map_kernel(MeshDev m, unsigned from_mask, unsigned to_mask, long long* out, i64 count) {
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    i64 rem = t, src = 0, fstride = 1;
+    for (int a = 0; a < m.dim; ++a) {
+      const bool tc = (to_mask >> a) & 1u, fc = (from_mask >> a) & 1u;
+      const int text = tc ? m.nc[a] : m.nf[a];
+      const int fext = fc ? m.nc[a] : m.nf[a];
+      const i64 ta = rem % text + 1;
+      rem /= text;
+      const i64 step = (tc && !fc) ? m.n[a] : 1;
+      src += (ta * step - 1) * fstride;
+      fstride *= fext;
+    }
+    out[t] = src;
+  }
+}
+
+__global__ void hole_map_kernel(MeshDev m, long long* out, i64 count) {
+  i64 per = 1;
+  for (int a = 0; a < m.dim; ++a) per *= m.n[a] - 1;
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    i64 blk = t / per, in = t % per, lin = 0, fstride = 1;
+    for (int a = 0; a < m.dim; ++a) {
+      const i64 h = blk % (m.nc[a] + 1);
+      blk /= (m.nc[a] + 1);
+      const i64 k = in % (m.n[a] - 1) + 1;
+      in /= (m.n[a] - 1);
+      lin += (h * m.n[a] + k - 1) * fstride;
+      fstride *= m.nf[a];
+    }
+    out[t] = lin;
+  }
+}
+
+}  // namespace
+
+void launch_projector_map(const MeshDev& m, unsigned from_mask, unsigned to_mask, long long* out, i64 count,
+                          cudaStream_t s) {
+  const i64 nb = std::min<i64>((count + 255) / 256, 8 * kNumSms);
+  projector_map_kernel<<<static_cast<unsigned>(std::max<i64>(nb, 1)), 256, 0, s>>>(m, from_mask, to_mask, out, count);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_hole_map(const MeshDev& m, long long* out, i64 count, cudaStream_t s) {
+  const i64 nb = std::min<i64>((count + 255) / 256, 8 * kNumSms);
+  hole_map_kernel<<<static_cast<unsigned>(std::max<i64>(nb, 1)), 256, 0, s>>>(m, out, count);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+}  // namespace asdsm_b200

@@ -1,0 +1,350 @@
+// Host orchestration of one ASDSM solve on the device (proj/src/solver.cpp:486-680 restated
+// for a device-resident state).  All per-iteration decisions (normalization guard, step
+// clamp, accept/revert, stop rules) happen in ctrl kernels, so a whole solve is enqueued
+// without host synchronization and can be captured in a CUDA graph.
+#include "solver.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <random>
+
+namespace asdsm_b200 {
+
+std::uint64_t mix_seed(std::uint64_t base, std::uint64_t k) {
+  std::uint64_t z = base + 0x9E3779B97F4A7C15ull * (k + 1);
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m) {
+  for (int a = 0; a < 3; ++a) {
+    alpha_[a] = alpha[a];
+    beta_[a] = beta[a];
+  }
+  md_.dim = m.dim;
+  for (int a = 0; a < 3; ++a) {
+    md_.nf[a] = a < m.dim ? m.nf[a] : 1;
+    md_.nc[a] = a < m.dim ? m.nc[a] : 1;
+    md_.n[a] = a < m.dim ? m.n[a] : 1;
+    md_.h[a] = a < m.dim ? m.h[a] : 0.0;
+  }
+  const unsigned full = (1u << m.dim) - 1u;
+  g_fine_ = kind_geom(m, 0u);
+  g_coarse_ = kind_geom(m, full);
+  fg_.dim = m.dim;
+  for (int a = 0; a < 3; ++a) {
+    fg_.ext[a] = g_fine_.ext[a];
+    fg_.stride[a] = g_fine_.stride[a];
+  }
+  fg_.size = g_fine_.size;
+  st_fine_ = make_stencil(m, 0u, alpha_, beta_);
+  st_coarse_ = make_stencil(m, full, alpha_, beta_);
+  for (int a = 0; a < m.dim; ++a) {
+    g_slab_[a] = kind_geom(m, 1u << a);
+    st_slab_[a] = make_stencil(m, 1u << a, alpha_, beta_);
+  }
+  cell_ = 1.0;
+  for (int a = 0; a < m.dim; ++a) cell_ *= m.h[a];
+
+  // Separable solvers: slabs (one box each), coarse box, hole boxes (all congruent).
+  const int tax = m.time_axis;
+  for (int a = 0; a < m.dim; ++a)
+    sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, "slab " + std::to_string(a));
+  sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, "coarse mesh");
+  int hext[3] = {1, 1, 1};
+  i64 nholes = 1;
+  for (int a = 0; a < m.dim; ++a) {
+    hext[a] = m.n[a] - 1;
+    nholes *= m.nc[a] + 1;
+  }
+  sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, "hole block");
+
+  const i64 nf = g_fine_.size;
+  for (int i = 0; i < 2; ++i) {
+    u_[i] = dev_.alloc<double>(static_cast<size_t>(nf));
+    r_[i] = dev_.alloc<double>(static_cast<size_t>(nf));
+  }
+  b_ = dev_.alloc<double>(static_cast<size_t>(nf));
+  e_ = dev_.alloc<double>(static_cast<size_t>(nf));
+  exact_ = dev_.alloc<double>(static_cast<size_t>(nf));
+  size_t scratch = sep_scratch_bytes(sep_hole_, nholes);
+  for (int a = 0; a < m.dim; ++a) {
+    const size_t n = static_cast<size_t>(g_slab_[a].size);
+    b_slab_[a] = dev_.alloc<double>(n);
+    rhs_slab_[a] = dev_.alloc<double>(n);
+    sol_slab_[a] = dev_.alloc<double>(n);
+    scratch = std::max(scratch, sep_scratch_bytes(sep_slab_[a], 1));
+  }
+  scratch = std::max(scratch, sep_scratch_bytes(sep_coarse_, 1));
+  scratch0_ = dev_.alloc<unsigned char>(scratch);
+  scratch1_ = dev_.alloc<unsigned char>(scratch);
+  b_coarse_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
+  u_cc_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
+  cc_e1_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
+  cc_e2_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
+  int maxnc = 0;
+  for (int a = 0; a < m.dim; ++a) maxnc = std::max(maxnc, m.nc[a]);
+  const size_t nlines = static_cast<size_t>(m.nc[0] + m.nc[1] + (m.dim == 3 ? m.nc[2] : 0));
+  spl_m1_ = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * (m.nc[0] + 2) + 16);
+  spl_m2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * (m.nc[1] + 2) + nlines * 4 * (maxnc + 2) + 16);
+  partials_ = dev_.alloc<double>(4 * kRedBlocks);
+  state_ = dev_.alloc<DevState>(1);
+  ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
+}
+
+BoxArray Solver::hole_array(double* p) const {
+  BoxArray b;
+  b.ptr = p;
+  for (int a = 0; a < 3; ++a) {
+    b.stride[a] = g_fine_.stride[a];
+    b.nbox[a] = a < mesh_.dim ? mesh_.nc[a] + 1 : 1;
+    b.box_stride[a] = a < mesh_.dim ? static_cast<i64>(mesh_.n[a]) * g_fine_.stride[a] : 0;
+  }
+  return b;
+}
+
+BoxArray Solver::kind_array(const KindGeom& g, double* p) const {
+  BoxArray b;
+  b.ptr = p;
+  for (int a = 0; a < 3; ++a) {
+    b.stride[a] = g.stride[a];
+    b.nbox[a] = 1;
+    b.box_stride[a] = 0;
+  }
+  return b;
+}
+
+void Solver::set_bundle(const double* b_fine, const double* const* b_slab, const double* b_coarse,
+                        const double* exact, bool on_device, cudaStream_t s) {
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const size_t nf = static_cast<size_t>(g_fine_.size) * sizeof(double);
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(b_, b_fine, nf, kind, s));
+  for (int a = 0; a < mesh_.dim; ++a)
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(b_slab_[a], b_slab[a], static_cast<size_t>(g_slab_[a].size) * sizeof(double), kind, s));
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(b_coarse_, b_coarse, static_cast<size_t>(g_coarse_.size) * sizeof(double), kind, s));
+  has_exact_ = exact != nullptr;
+  if (exact) ASDSM_CUDA_CHECK(cudaMemcpyAsync(exact_, exact, nf, kind, s));
+}
+
+void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
+  DevState h{};
+  h.cur = 0;
+  h.active = 1;
+  h.have_e = 1;
+  h.stop = 0;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  // stop_at from ||b||_2 (solver.cpp:570-571)
+  launch_norm_sq(b_, g_fine_.size, partials_, state_, s);
+  CtrlArgs c{};
+  c.op = kCtrlInit;
+  c.tol = o.tol;
+  launch_ctrl(c, partials_, state_, history_, s);
+}
+
+void Solver::skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s) {
+  if (mesh_.dim != 2) throw AsdsmError(kUnsupported, "3D skeleton merge not built yet");
+  Skel2DArgs a{};
+  a.m = md_;
+  a.u_fc = sol[1];
+  a.u_cf = sol[0];
+  a.u_cc = u_cc;
+  a.coin = coin;
+  a.e1 = cc_e1_;
+  a.e2 = cc_e2_;
+  a.m1 = spl_m1_;
+  a.m2 = spl_m2_;
+  a.out = out;
+  launch_skeleton2d(a, state_, s);
+}
+
+void Solver::fill(double* e, const double* b, cudaStream_t s) {
+  launch_hole_rhs(mesh_.dim, e, b, fg_, st_fine_, md_, state_, s);
+  const BoxArray h = hole_array(e);
+  sep_solve(sep_hole_, h, h, scratch0_, scratch1_, s);
+}
+
+// Alg. 1 with the assembled bundle (solver.cpp:518-548, smooth mode).
+void Solver::smooth_guess(double* out, cudaStream_t s) {
+  for (int a = 0; a < mesh_.dim; ++a)
+    sep_solve(sep_slab_[a], kind_array(g_slab_[a], b_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
+              scratch1_, s);
+  sep_solve(sep_coarse_, kind_array(g_coarse_, b_coarse_), kind_array(g_coarse_, u_cc_), scratch0_, scratch1_, s);
+  const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
+  skeleton(sol, u_cc_, nullptr, out, s);
+  fill(out, b_, s);
+}
+
+// error_guess (solver.cpp:550-558): restrict r, solve the slabs, normalize, merge, fill
+// against a zero right-hand side.
+void Solver::error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s) {
+  for (int a = 0; a < mesh_.dim; ++a) {
+    launch_gather(r0, r1, rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
+    sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
+              scratch1_, s);
+  }
+  for (int a = 0; a < mesh_.dim; ++a) {
+    launch_norm_sq(sol_slab_[a], g_slab_[a].size, partials_, state_, s);
+    CtrlArgs c{};
+    c.op = kCtrlSlabNorm;
+    c.which = a;
+    launch_ctrl(c, partials_, state_, history_, s);
+  }
+  for (int a = 0; a < mesh_.dim; ++a) launch_divide(sol_slab_[a], g_slab_[a].size, &state_->slab_norm[a], state_, s);
+  const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
+  skeleton(sol, nullptr, coins_ + 4 * k, out, s);
+  fill(out, nullptr, s);
+}
+
+void Solver::run(const RunOptions& o, cudaStream_t s) {
+  last_opts_ = o;
+  const long long l0 = g_kernel_launches;
+  const int cap = std::max(o.max_iter, 0) + 1;
+  if (cap > history_cap_) {
+    history_ = dev_.alloc<double>(static_cast<size_t>(cap) * 7);
+    history_cap_ = cap;
+  }
+  // Seeded draws (solver.cpp:110-120, 309-345): per iteration k the engine is
+  // mt19937_64(mix_seed(seed, k)); 2D takes one draw % 2, 3D one % 3 then three % 2.
+  std::vector<int> coins(static_cast<size_t>(4 * cap), 0);
+  for (int k = 0; k < cap; ++k) {
+    std::mt19937_64 eng(mix_seed(o.rng_seed, static_cast<std::uint64_t>(k)));
+    if (mesh_.dim == 2) {
+      coins[static_cast<size_t>(4 * k)] = static_cast<int>(eng() % 2);
+    } else {
+      coins[static_cast<size_t>(4 * k)] = static_cast<int>(eng() % 3);
+      for (int i = 1; i < 4; ++i) coins[static_cast<size_t>(4 * k + i)] = static_cast<int>(eng() % 2);
+    }
+  }
+  if (4 * cap > coins_cap_) {
+    coins_ = dev_.alloc<int>(static_cast<size_t>(4 * cap));
+    coins_cap_ = 4 * cap;
+  }
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(coins_, coins.data(), coins.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+
+  reset_state(o, s);
+  CtrlArgs c{};
+  c.has_exact = has_exact_;
+  c.cell = cell_;
+  c.tol_growth = 1.0 + 1e-12;
+  c.stagnation_window = o.stagnation_window;
+  c.stagnation_pow = std::pow(o.stagnation_ratio, o.stagnation_window);
+  c.max_iter = o.max_iter;
+  c.tol = o.tol;
+
+  smooth_guess(u_[0], s);
+  launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1],
+                 has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s);
+  c.op = kCtrlResidualK0;
+  c.k = 0;
+  launch_ctrl(c, partials_, state_, history_, s);
+
+  for (int k = 1; k <= o.max_iter; ++k) {
+    error_mode_guess(r_[0], r_[1], k, e_, s);
+    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s);
+    c.op = kCtrlStep;
+    c.k = k;
+    launch_ctrl(c, partials_, state_, history_, s);
+    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1],
+                   has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s);
+    c.op = kCtrlAccept;
+    launch_ctrl(c, partials_, state_, history_, s);
+  }
+  launches_ = g_kernel_launches - l0;
+}
+
+int Solver::history(std::vector<double>& rows, int& stop_code, cudaStream_t s) const {
+  DevState h{};
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&h, state_, sizeof(h), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  rows.assign(static_cast<size_t>(h.nrec) * 7, 0.0);
+  if (h.nrec > 0)
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(rows.data(), history_, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  stop_code = h.stop == 0 ? 3 : h.stop;
+  return h.nrec;
+}
+
+const double* Solver::u_current(cudaStream_t s) const {
+  int cur = 0;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&cur, &state_->cur, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  return u_[cur];
+}
+
+const double* Solver::r_current(cudaStream_t s) const {
+  int cur = 0;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&cur, &state_->cur, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  return r_[cur];
+}
+
+void Solver::residual(const double* u, const double* b, double* r, cudaStream_t s) {
+  DevState h{};
+  h.active = 1;
+  h.have_e = 1;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_stencil(mesh_.dim, false, u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_, state_, s);
+}
+
+void Solver::error_guess(const double* r, std::uint64_t seed, double* e, cudaStream_t s) {
+  DevState h{};
+  h.active = 1;
+  h.have_e = 1;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  if (coins_cap_ < 4) {
+    coins_ = dev_.alloc<int>(4);
+    coins_cap_ = 4;
+  }
+  int coins[4] = {0, 0, 0, 0};
+  std::mt19937_64 eng(seed);
+  if (mesh_.dim == 2) {
+    coins[0] = static_cast<int>(eng() % 2);
+  } else {
+    coins[0] = static_cast<int>(eng() % 3);
+    for (int i = 1; i < 4; ++i) coins[i] = static_cast<int>(eng() % 2);
+  }
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(coins_, coins, sizeof(coins), cudaMemcpyHostToDevice, s));
+  if (history_cap_ < 1) {
+    history_ = dev_.alloc<double>(7);
+    history_cap_ = 1;
+  }
+  error_mode_guess(r, r, 0, e, s);
+  DevState back{};
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&back, state_, sizeof(back), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (!back.have_e) throw AsdsmError(kZeroNormSolution, "initial_guess: zero-norm solution cannot be normalized");
+}
+
+double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s) {
+  DevState h{};
+  h.active = 1;
+  h.have_e = 1;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_ae_dots(mesh_.dim, e, r, r, fg_, st_fine_, partials_, state_, s);
+  CtrlArgs c{};
+  c.op = kCtrlStep;
+  if (history_cap_ < 1) {
+    history_ = dev_.alloc<double>(7);
+    history_cap_ = 1;
+  }
+  launch_ctrl(c, partials_, state_, history_, s);
+  DevState back{};
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&back, state_, sizeof(back), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  return back.s;
+}
+
+void Solver::initial_guess(double* u_out, std::uint64_t seed, cudaStream_t s) {
+  (void)seed;
+  DevState h{};
+  h.active = 1;
+  h.have_e = 1;
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  smooth_guess(u_out, s);
+}
+
+}  // namespace asdsm_b200

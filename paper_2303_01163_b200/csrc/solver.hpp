@@ -1,0 +1,109 @@
+// B200 ASDSM solver context: the device-resident counterpart of the reference's
+// SolverContext + asdsm_iterate (proj/include/asdsm/solver.hpp:114-163).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "sepsolve.cuh"
+
+namespace asdsm_b200 {
+
+// IterateOptions (proj/include/asdsm/solver.hpp:56-68).
+struct RunOptions {
+  double tol = 1e-12;
+  int max_iter = 20;
+  int stagnation_window = 3;
+  double stagnation_ratio = 0.99;
+  double subsample = 0.0;
+  std::uint64_t rng_seed = 0;
+};
+
+std::uint64_t mix_seed(std::uint64_t base, std::uint64_t k);  // solver.cpp:88-96
+
+class Solver {
+ public:
+  Solver(const Mesh& m, const double* alpha, const double* beta);
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
+
+  const Mesh& mesh() const { return mesh_; }
+  i64 fine_size() const { return g_fine_.size; }
+  i64 slab_size(int a) const { return g_slab_[a].size; }
+  i64 coarse_size() const { return g_coarse_.size; }
+
+  // Right-hand-side bundle (RhsBundle, solver.hpp:37-42) + optional exact samples.
+  // Pointers are host or device memory according to `on_device`.
+  void set_bundle(const double* b_fine, const double* const* b_slab, const double* b_coarse, const double* exact,
+                  bool on_device, cudaStream_t s);
+
+  // Initial guess + up to max_iter error-mode corrections, all control on the device.
+  void run(const RunOptions& o, cudaStream_t s);
+
+  // After run(): history rows (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms).
+  int history(std::vector<double>& rows, int& stop_code, cudaStream_t s) const;
+  const double* u_current(cudaStream_t s) const;  // synchronizes to read the selector
+  const double* r_current(cudaStream_t s) const;
+  double* u_buffer(int i) { return u_[i]; }
+  double* r_buffer(int i) { return r_[i]; }
+  double* e_buffer() { return e_; }
+  const double* b_fine() const { return b_; }
+
+  // Single operations (for the function-level parity tests).
+  void residual(const double* u, const double* b, double* r, cudaStream_t s);  // device pointers
+  void error_guess(const double* r, std::uint64_t seed, double* e, cudaStream_t s);
+  double optimal_scaling(const double* r, const double* e, cudaStream_t s);
+  void initial_guess(double* u_out, std::uint64_t seed, cudaStream_t s);
+
+  const MeshDev& mesh_dev() const { return md_; }
+
+  // Launch count of the last run() (kernels of this library only).
+  long long last_launches() const { return launches_; }
+
+ private:
+  void reset_state(const RunOptions& o, cudaStream_t s);
+  void smooth_guess(double* out, cudaStream_t s);
+  void error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s);
+  void skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s);
+  void fill(double* e, const double* b, cudaStream_t s);
+  BoxArray hole_array(double* p) const;
+  BoxArray kind_array(const KindGeom& g, double* p) const;
+
+  Mesh mesh_;
+  double alpha_[3] = {0, 0, 0}, beta_[3] = {0, 0, 0};
+  MeshDev md_{};
+  KindGeom g_fine_, g_slab_[3], g_coarse_;
+  FineGeom fg_{};
+  Stencil st_fine_, st_slab_[3], st_coarse_;
+  SepSolver sep_slab_[3], sep_coarse_, sep_hole_;
+  DeviceAlloc dev_;
+  double* u_[2] = {nullptr, nullptr};
+  double* r_[2] = {nullptr, nullptr};
+  double* b_ = nullptr;
+  double* e_ = nullptr;
+  double* exact_ = nullptr;
+  bool has_exact_ = false;
+  double* b_slab_[3] = {nullptr, nullptr, nullptr};
+  double* rhs_slab_[3] = {nullptr, nullptr, nullptr};
+  double* sol_slab_[3] = {nullptr, nullptr, nullptr};
+  double* b_coarse_ = nullptr;
+  double* u_cc_ = nullptr;
+  double* cc_e1_ = nullptr;
+  double* cc_e2_ = nullptr;
+  double* spl_m1_ = nullptr;
+  double* spl_m2_ = nullptr;
+  void* scratch0_ = nullptr;
+  void* scratch1_ = nullptr;
+  double* partials_ = nullptr;
+  DevState* state_ = nullptr;
+  double* history_ = nullptr;
+  int history_cap_ = 0;
+  int* coins_ = nullptr;
+  int coins_cap_ = 0;
+  RunOptions last_opts_{};
+  double cell_ = 1.0;
+  long long launches_ = 0;
+};
+
+}  // namespace asdsm_b200

@@ -1,0 +1,114 @@
+"""Helpers to run the compiled reference oracle (oracle/_ref/ref_dump) and load its dumps.
+
+Test infrastructure only: the checker, never the thing measured or shipped.
+"""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_DUMP = os.path.join(ROOT, "oracle", "_ref", "ref_dump")
+
+
+def have_ref():
+    return os.path.exists(REF_DUMP)
+
+
+def _meta(prefix):
+    with open(prefix + ".meta.txt") as f:
+        lines = f.read().split("\n")
+    dim, ta = map(int, lines[0].split())
+    nf = list(map(int, lines[1].split()))
+    nc = list(map(int, lines[2].split()))
+    return dim, ta, nf, nc
+
+
+def ref_iterate(spec, nf, nc, iters, seed, env=None):
+    with tempfile.TemporaryDirectory() as d:
+        prefix = os.path.join(d, "run")
+        e = dict(os.environ)
+        if env:
+            e.update(env)
+        subprocess.check_call([REF_DUMP, "iterate", spec, str(nf), str(nc), str(iters), str(seed), prefix], env=e)
+        rows = []
+        stop = None
+        with open(prefix + ".hist.txt") as f:
+            for line in f:
+                if line.startswith("# stop:"):
+                    stop = line.split(":")[1].strip()
+                    continue
+                rows.append([float(x) for x in line.split()])
+        out = {
+            "hist": np.array(rows),
+            "stop": stop,
+            "u": np.fromfile(prefix + ".u.f64"),
+            "r": np.fromfile(prefix + ".r.f64"),
+            "u0": np.fromfile(prefix + ".u0.f64"),
+            "r0": np.fromfile(prefix + ".r0.f64"),
+            "meta": _meta(prefix),
+        }
+    return out
+
+
+def ref_bundle(spec, nf, nc):
+    with tempfile.TemporaryDirectory() as d:
+        prefix = os.path.join(d, "b")
+        subprocess.check_call([REF_DUMP, "bundle", spec, str(nf), str(nc), prefix])
+        dim, ta, fnf, fnc = _meta(prefix)
+        out = {"meta": (dim, ta, fnf, fnc), "fine": np.fromfile(prefix + ".b_fine.f64"),
+               "aniso": [np.fromfile(prefix + f".b_slab{a}.f64") for a in range(dim)],
+               "coarse": np.fromfile(prefix + ".b_coarse.f64"),
+               "A_rowptr": np.fromfile(prefix + ".A_rowptr.i64", dtype=np.int64),
+               "A_col": np.fromfile(prefix + ".A_col.i64", dtype=np.int64),
+               "A_val": np.fromfile(prefix + ".A_val.f64")}
+        if os.path.exists(prefix + ".exact.f64"):
+            out["exact"] = np.fromfile(prefix + ".exact.f64")
+    return out
+
+
+def ref_error_guess(spec, nf, nc, seed, r):
+    with tempfile.TemporaryDirectory() as d:
+        rfile = os.path.join(d, "r.f64")
+        np.asarray(r, dtype=np.float64).tofile(rfile)
+        prefix = os.path.join(d, "eg")
+        subprocess.check_call([REF_DUMP, "errguess", spec, str(nf), str(nc), str(seed), rfile, prefix])
+        e = np.fromfile(prefix + ".e.f64")
+        with open(prefix + ".s.txt") as f:
+            s = float(f.read())
+    return e, s
+
+
+def ref_maps(spec, nf, nc):
+    with tempfile.TemporaryDirectory() as d:
+        prefix = os.path.join(d, "m")
+        subprocess.check_call([REF_DUMP, "maps", spec, str(nf), str(nc), prefix])
+        dim = _meta(prefix)[0]
+        maps = {}
+        full = (1 << dim) - 1
+        for fr in range(full + 1):
+            for to in range(full + 1):
+                if fr == to or (fr & to) != fr:
+                    continue
+                maps[(fr, to)] = np.fromfile(prefix + f".map_{fr}_{to}.i64", dtype=np.int64)
+        maps["holes"] = np.fromfile(prefix + ".map_holes.i64", dtype=np.int64)
+    return maps
+
+
+def csr_residual_exact(bundle, u, b=None):
+    """b - A u with the reference's CSR row order (sparse.cpp:49-58), vectorized per column slot.
+
+    Each row's entries are summed left to right starting from 0.0 exactly as the reference does,
+    so the result is bitwise the reference's residual.
+    """
+    rp, col, val = bundle["A_rowptr"], bundle["A_col"], bundle["A_val"]
+    n = len(rp) - 1
+    b = bundle["fine"] if b is None else b
+    counts = np.diff(rp)
+    acc = np.zeros(n)
+    for slot in range(int(counts.max())):
+        rows = np.nonzero(counts > slot)[0]
+        idx = rp[rows] + slot
+        acc[rows] = acc[rows] + val[idx] * u[col[idx]]
+    return b - acc

@@ -1,0 +1,114 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the compiled reference oracle.
+
+Tolerances:
+  * index maps, residual evaluation: bit-exact.
+  * initial guess / final solution: max-norm relative 1e-10.
+  * per-iteration residual norms: relative max(1e-10, 10x the reference's own reproducibility
+    floor up to that iteration), the floor measured live by re-running the reference with a
+    different (equally valid) fill ordering of its direct solver.
+"""
+import numpy as np
+import pytest
+
+import paper_2303_01163_b200 as pb
+from ref_tools import csr_residual_exact, have_ref, ref_bundle, ref_error_guess, ref_iterate, ref_maps
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")]
+
+
+def _ctx(spec, nf, nc):
+    if spec.startswith("ex:"):
+        _, e, s = spec.split(":")
+        prob = pb.make_problem(int(e), int(s))
+        mesh = pb.asdsm.example_mesh(int(e), int(s), nf, nc)
+    else:
+        _, cid, seed = spec.split(":")
+        prob = pb.baseline_problem(int(cid), int(seed))
+        mesh, _ = pb.baseline_mesh(int(cid))
+        if nf:
+            mesh = pb.MeshConfig.create(mesh.dim, [nf] * mesh.dim, [nc] * mesh.dim, mesh.time_axis)
+    return pb.SolverContext(mesh, prob), mesh, prob
+
+
+@pytest.mark.parametrize("spec,nf,nc", [("ex:1:1", 24, 4), ("ex:4:1", 14, 4), ("cfg:4:3", 29, 4), ("ex:3:1", 19, 4)])
+def test_index_maps_bit_exact(spec, nf, nc):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    ref = ref_maps(spec, nf, nc)
+    for key, m in ref.items():
+        if key == "holes":
+            continue
+        fr, to = key
+        got = ctx.projector_map(pb.MeshKind.from_mask(mesh.dim, fr), pb.MeshKind.from_mask(mesh.dim, to))
+        assert np.array_equal(got, m), (fr, to)
+    got = pb.hole_positions(mesh, ctx)
+    assert np.array_equal(got, ref["holes"])
+
+
+@pytest.mark.parametrize("spec,nf,nc", [("ex:1:1", 99, 9), ("cfg:2:5", 199, 9), ("ex:3:1", 49, 4),
+                                        ("ex:4:1", 24, 4), ("cfg:4:1", 29, 4)])
+def test_residual_bit_exact(spec, nf, nc):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    bun = ref_bundle(spec, nf, nc)
+    assert np.array_equal(ctx.bundle["fine"], bun["fine"])  # host assembly == reference assembly
+    for a in range(mesh.dim):
+        assert np.array_equal(ctx.bundle["aniso"][a], bun["aniso"][a])
+    assert np.array_equal(ctx.bundle["coarse"], bun["coarse"])
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal(ctx.fine_size())
+    r = ctx.residual(u)
+    want = csr_residual_exact(bun, u)
+    assert np.array_equal(r, want)
+
+
+@pytest.mark.parametrize("spec,nf,nc", [("ex:1:1", 99, 9), ("cfg:0:0", 0, 0), ("cfg:1:2", 199, 9),
+                                        ("cfg:2:5", 199, 9), ("ex:3:1", 99, 9)])
+def test_initial_guess(spec, nf, nc):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    ref = ref_iterate(spec, nf, nc, 0, 0)
+    u0 = ctx.initial_guess()
+    scale = np.max(np.abs(ref["u0"]))
+    assert np.max(np.abs(u0 - ref["u0"])) <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("spec,nf,nc,seed", [("ex:1:1", 99, 9, 3), ("cfg:2:5", 199, 9, 11)])
+def test_error_guess_and_scaling(spec, nf, nc, seed):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    ref = ref_iterate(spec, nf, nc, 0, 0)
+    r0 = ref["r0"]
+    e_ref, s_ref = ref_error_guess(spec, nf, nc, seed, r0)
+    e = ctx.error_guess(r0, seed)
+    assert np.max(np.abs(e - e_ref)) <= 1e-10 * np.max(np.abs(e_ref))
+    s = ctx.optimal_scaling(r0, e)
+    assert abs(s - s_ref) <= 1e-10 * abs(s_ref)
+
+
+def _rel_floor(spec, nf, nc, iters, seed, ref):
+    """Reference reproducibility floor: relative spread of its own residual history between two
+    equally valid fill orderings of its direct solver, made non-decreasing in k (rounding
+    differences, once present, propagate through the iteration)."""
+    alt = ref_iterate(spec, nf, nc, iters, seed, env={"ASDSM_STUB_NATURAL_ORDER": "1"})
+    want = ref["hist"][:, 1]
+    return np.maximum.accumulate(np.abs(alt["hist"][:, 1] - want) / want)
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters,seed", [
+    ("cfg:0:0", 0, 0, 10, 0),
+    ("ex:1:1", 99, 9, 20, 0),
+    ("ex:3:1", 99, 9, 20, 0),
+    ("cfg:1:2", 199, 9, 20, 1),
+    ("cfg:2:5", 199, 9, 20, 2),
+])
+def test_iterate_history(spec, nf, nc, iters, seed):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    ref = ref_iterate(spec, nf, nc, iters, seed)
+    st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=seed))
+    got = np.array([h.res_l2 for h in st.history])
+    want = ref["hist"][:, 1]
+    assert len(got) == len(want)
+    tol = want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, seed, ref))
+    bad = np.abs(got - want) > tol
+    assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
+    s_got = np.array([h.s_hat for h in st.history[1:]])
+    assert np.array_equal(s_got == 0.0, ref["hist"][1:, 5] == 0.0)  # same accept/revert decisions
+    scale = np.max(np.abs(ref["u"]))
+    assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * scale
