@@ -171,7 +171,7 @@ std::vector<double> to_interleaved(const std::vector<cld>& v) {
 }  // namespace
 
 SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Stencil& st,
-                           int time_axis_in_box, int prefer_line_axis, const std::string& what) {
+                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what) {
   SepSolver s;
   s.dim = dim;
   for (int a = 0; a < 3; ++a) s.ext[a] = a < dim ? ext[a] : 1;
@@ -245,7 +245,9 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
       sigma[static_cast<size_t>(c0 + cext[0] * c1)] = sg;
     }
 
-  s.use_pcr = (s.L == 0);
+  // PCR (one CTA per line) for lines along the contiguous axis or when there are few lines
+  // (a per-thread Thomas walk over a few long lines is latency bound); Thomas otherwise.
+  s.use_pcr = (s.L == 0) || (static_cast<i64>(s.ncombo) * nbatch < 8192 && m <= 6144);
   if (!s.use_pcr) {
     std::vector<cld> ipiv(static_cast<size_t>(m) * s.ncombo), cp(static_cast<size_t>(m) * s.ncombo);
     for (int c = 0; c < s.ncombo; ++c) {

@@ -123,6 +123,6 @@ struct DeviceAlloc {
 // Build a separable solver (host tables in long double, uploaded once).
 // `time_axis_in_box` marks an axis with the backward two-point stencil (not diagonalizable).
 SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Stencil& st,
-                           int time_axis_in_box, int prefer_line_axis, const std::string& what);
+                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what);
 
 }  // namespace asdsm_b200

@@ -53,15 +53,15 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   // Separable solvers: slabs (one box each), coarse box, hole boxes (all congruent).
   const int tax = m.time_axis;
   for (int a = 0; a < m.dim; ++a)
-    sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, "slab " + std::to_string(a));
-  sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, "coarse mesh");
+    sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
+  sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
   int hext[3] = {1, 1, 1};
   i64 nholes = 1;
   for (int a = 0; a < m.dim; ++a) {
     hext[a] = m.n[a] - 1;
     nholes *= m.nc[a] + 1;
   }
-  sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, "hole block");
+  sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block");
 
   const i64 nf = g_fine_.size;
   for (int i = 0; i < 2; ++i) {
@@ -91,6 +91,28 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   const size_t nlines = static_cast<size_t>(m.nc[0] + m.nc[1] + (m.dim == 3 ? m.nc[2] : 0));
   spl_m1_ = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * (m.nc[0] + 2) + 16);
   spl_m2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * (m.nc[1] + 2) + nlines * 4 * (maxnc + 2) + 16);
+  if (m.dim == 3) {
+    m3_.m = md_;
+    const size_t ntr = static_cast<size_t>(g_coarse_.size);
+    m3_.u_hat = dev_.alloc<double>(ntr);
+    int p = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = a + 1; b < 3; ++b, ++p) {
+        const int f = 3 - a - b;
+        m3_.corr[p] = dev_.alloc<double>(ntr);
+        m3_.mP[p] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nc[b] * (m.nc[f] + 2));
+        m3_.T[p] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nc[b] * m.nf[f]);
+      }
+    for (int a = 0; a < 3; ++a) {
+      const int f1 = (a == 0) ? 1 : 0, f2 = (a == 2) ? 1 : 2;
+      m3_.mF1[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f2] * (m.nc[f1] + 2));
+      m3_.mF2[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * (m.nc[f2] + 2));
+      m3_.mF3a[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nc[f2] * (m.nc[f1] + 2));
+      m3_.mF3b[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * (m.nc[f2] + 2));
+      m3_.g3[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * (m.nc[f2] + 2));
+      m3_.corrected[a] = dev_.alloc<double>(static_cast<size_t>(g_slab_[a].size));
+    }
+  }
   partials_ = dev_.alloc<double>(4 * kRedBlocks);
   state_ = dev_.alloc<DevState>(1);
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
@@ -146,7 +168,14 @@ void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
 }
 
 void Solver::skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s) {
-  if (mesh_.dim != 2) throw AsdsmError(kUnsupported, "3D skeleton merge not built yet");
+  if (mesh_.dim == 3) {
+    Merge3DArgs A = m3_;
+    for (int a = 0; a < 3; ++a) A.u[a] = sol[a];
+    A.u_ccc = u_cc;
+    A.coin = coin;
+    launch_merge3d(A, out, state_, s);
+    return;
+  }
   Skel2DArgs a{};
   a.m = md_;
   a.u_fc = sol[1];

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "merge3d.cuh"
 #include "plan.hpp"
 #include "sepsolve.cuh"
 
@@ -93,6 +94,7 @@ class Solver {
   double* cc_e2_ = nullptr;
   double* spl_m1_ = nullptr;
   double* spl_m2_ = nullptr;
+  Merge3DArgs m3_{};
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
   double* partials_ = nullptr;

@@ -112,3 +112,22 @@ def test_iterate_history(spec, nf, nc, iters, seed):
     assert np.array_equal(s_got == 0.0, ref["hist"][1:, 5] == 0.0)  # same accept/revert decisions
     scale = np.max(np.abs(ref["u"]))
     assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("spec,nf,nc", [("ex:4:1", 24, 4), ("cfg:3:0", 29, 4), ("cfg:4:3", 29, 4)])
+def test_initial_guess_3d(spec, nf, nc):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    ref = ref_iterate(spec, nf, nc, 0, 0)
+    u0 = ctx.initial_guess()
+    scale = np.max(np.abs(ref["u0"]))
+    assert np.max(np.abs(u0 - ref["u0"])) <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters,seed", [
+    ("ex:4:1", 24, 4, 10, 0),
+    ("cfg:3:0", 29, 4, 10, 1),
+    ("cfg:4:3", 29, 4, 10, 2),
+    ("cfg:3:0", 59, 9, 6, 0),
+])
+def test_iterate_history_3d(spec, nf, nc, iters, seed):
+    test_iterate_history(spec, nf, nc, iters, seed)
