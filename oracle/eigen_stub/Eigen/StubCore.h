@@ -140,7 +140,10 @@ class SparseLU {
         });
         level.insert(level.end(), nbs.begin(), nbs.end());
       }
-      perm_.insert(perm_.end(), level.rbegin(), level.rend());
+      if (const char* o = std::getenv("ASDSM_STUB_ORDER"); o && std::string(o) == "cm")
+        perm_.insert(perm_.end(), level.begin(), level.end());  // Cuthill-McKee, not reversed
+      else
+        perm_.insert(perm_.end(), level.rbegin(), level.rend());
     }
     if (std::getenv("ASDSM_STUB_NATURAL_ORDER")) {
       perm_.resize(static_cast<std::size_t>(n_));

@@ -1,0 +1,21 @@
+// fp64 tile GEMM on the DMMA pipe (mma.sync.m8n8k4.f64) for the eigenvector transforms:
+//   out(line p, q) = sum_k in(line p, k) * M[q][k]
+// over a batch of strided lines (same LineMap addressing as the scalar transform kernel).
+#pragma once
+#include "plan.hpp"
+
+namespace asdsm_b200 {
+
+struct GemmLines {
+  int o_ext[2];
+  i64 o_in[2], o_out[2];
+  int nbox[3];
+  i64 in_bs[3], out_bs[3];
+  i64 nlines;
+};
+
+// in_es / out_es: element stride along the transform axis for input / output.
+void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
+                           const GemmLines& L, cudaStream_t s);
+
+}  // namespace asdsm_b200

@@ -1,0 +1,106 @@
+// Error-mode hole fill for 2D boxes (Alg. 3 / fill_core, proj/src/solver.cpp:414-432),
+// specialised to the separable solver with line axis y and diagonalized axis x.
+//
+// In error mode the hole right-hand side is 0 - (A_ff * skeleton) on hole rows, which is
+// non-zero only on the ring of points adjacent to the skeleton.  Its forward eigenvector
+// transform along x is therefore analytic: for interior rows
+//     fhat(k, j) = W[k][0] f(0, j) + W[k][m-1] f(m-1, j)
+// and only the first/last rows need a full (O(m) per mode) transform.  One CTA per
+// (hole, block of modes) builds the ring rhs from the skeleton, forms fhat on the fly and
+// runs both Thomas sweeps in shared memory; the dense back transform is the DMMA GEMM.
+#include "holes2d.cuh"
+
+namespace asdsm_b200 {
+
+namespace {
+
+// 0 - row_dot(p, skeleton) for hole point (i, j) of the hole with fine origin (ox, oy);
+// neighbours outside the box are skeleton points (or the domain boundary: no column).
+__device__ __forceinline__ double ring_rhs(const double* __restrict__ e, const Hole2DArgs& A, int ox, int oy, int i,
+                                           int j) {
+  const Stencil& st = A.st;
+  double acc = 0.0;
+  const i64 Nx = A.nf0;
+  if (j == 0 && oy > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], e[static_cast<i64>(oy - 1) * Nx + ox + i]));
+  if (i == 0 && ox > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], e[static_cast<i64>(oy + j) * Nx + ox - 1]));
+  if (i == A.m0 - 1 && ox + A.m0 < A.nf0 && st.has_right[0])
+    acc = __dadd_rn(acc, __dmul_rn(st.right[0], e[static_cast<i64>(oy + j) * Nx + ox + A.m0]));
+  if (j == A.m1 - 1 && oy + A.m1 < A.nf1 && st.has_right[1])
+    acc = __dadd_rn(acc, __dmul_rn(st.right[1], e[static_cast<i64>(oy + A.m1) * Nx + ox + i]));
+  return __dsub_rn(0.0, acc);
+}
+
+__global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* __restrict__ modes, Hole2DArgs A,
+                                         const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  extern __shared__ double sm[];
+  const int m0 = A.m0, m1 = A.m1, KB = blockDim.x;
+  double* fL = sm;
+  double* fR = fL + m1;
+  double* fB = fR + m1;
+  double* fT = fB + m0;
+  const int hole = blockIdx.x;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  const int ox = hx * A.n0, oy = hy * A.n1;
+  for (int t = threadIdx.x; t < m1; t += KB) {
+    fL[t] = ring_rhs(e, A, ox, oy, 0, t);
+    fR[t] = ring_rhs(e, A, ox, oy, m0 - 1, t);
+  }
+  for (int t = threadIdx.x; t < m0; t += KB) {
+    fB[t] = ring_rhs(e, A, ox, oy, t, 0);
+    fT[t] = ring_rhs(e, A, ox, oy, t, m1 - 1);
+  }
+  __syncthreads();
+  const int k = blockIdx.y * KB + threadIdx.x;
+  if (k >= m0) return;
+  // full transforms of the first and last rows
+  double fb = 0.0, ft = 0.0;
+  for (int i = 0; i < m0; ++i) {
+    const double w = A.Wt[static_cast<i64>(i) * m0 + k];
+    fb = fma(w, fB[i], fb);
+    ft = fma(w, fT[i], ft);
+  }
+  const double w0 = A.Wt[k], wm = A.Wt[static_cast<i64>(m0 - 1) * m0 + k];
+  const double l = A.line_left;
+  // forward sweep; y is parked in the mode buffer and overwritten by the backward sweep
+  double* out = modes + static_cast<i64>(hole) * m0 * m1;
+  double y = 0.0;
+  for (int j = 0; j < m1; ++j) {
+    double f;
+    if (j == 0) f = fb;
+    else if (j == m1 - 1) f = ft;
+    else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
+    const double iv = A.ipiv[static_cast<i64>(j) * m0 + k];
+    y = (j == 0) ? f * iv : (f - l * y) * iv;
+    out[static_cast<i64>(j) * m0 + k] = y;
+  }
+  // backward sweep, mode layout [hole][j][k]
+  double x = y;
+  for (int j = m1 - 2; j >= 0; --j) {
+    x = out[static_cast<i64>(j) * m0 + k] - A.cp[static_cast<i64>(j) * m0 + k] * x;
+    out[static_cast<i64>(j) * m0 + k] = x;
+  }
+}
+
+}  // namespace
+
+size_t hole2d_smem_bytes(int m0, int m1, int kb) {
+  (void)kb;
+  return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0));
+}
+
+void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s) {
+  const int kb = A.kb;
+  const size_t smem = hole2d_smem_bytes(A.m0, A.m1, kb);
+  dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m0 + kb - 1) / kb));
+  hole2d_fwd_thomas_kernel<<<grid, kb, smem, s>>>(e, modes, A, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void hole2d_prepare(size_t smem) {
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+}
+
+}  // namespace asdsm_b200

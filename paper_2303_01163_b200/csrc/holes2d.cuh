@@ -1,0 +1,23 @@
+#pragma once
+#include "kernels.cuh"
+
+namespace asdsm_b200 {
+
+struct Hole2DArgs {
+  int m0, m1;        // hole extents (x modes, y rows)
+  int n0, n1;        // refinement factors
+  int nf0, nf1;      // fine extents
+  int nbox0, nbox1;  // holes per axis (nc + 1)
+  int kb;            // modes per CTA
+  Stencil st;        // fine stencil
+  const double* Wt;  // forward eigenvectors along x, transposed: Wt[i*m0 + k] = W[k][i]
+  const double* ipiv;  // Thomas pivots [j][k]
+  const double* cp;    // Thomas upper factors [j][k]
+  double line_left;
+};
+
+size_t hole2d_smem_bytes(int m0, int m1, int kb);
+void hole2d_prepare(size_t smem);
+void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);
+
+}  // namespace asdsm_b200

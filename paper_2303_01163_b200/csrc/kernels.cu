@@ -479,6 +479,20 @@ __global__ void dense_matvec_kernel(const double* A, const double* b, double* x,
 
 }  // namespace
 
+__global__ void state_init_kernel(DevState* S, int active, int have_e) {
+  DevState h{};
+  h.cur = 0;
+  h.active = active;
+  h.have_e = have_e;
+  *S = h;
+}
+
+void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s) {
+  state_init_kernel<<<1, 1, 0, s>>>(state, active, have_e);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void launch_stencil(int dim, bool update, const double* u0, const double* u1, const double* e, const double* b,
                     double* uo0, double* uo1, double* ro0, double* ro1, const double* exact, const FineGeom& g,
                     const Stencil& st, double* partials, DevState* state, cudaStream_t s) {

@@ -49,6 +49,9 @@ void launch_gather(const double* src0, const double* src1, double* dst, const Me
 void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s);
 void launch_divide(double* x, i64 n, const double* divisor, DevState* state, cudaStream_t s);
 
+// Device-side state initialization (capturable in a CUDA graph; no host memcpy).
+void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s);
+
 // Final reductions + control (single CTA).
 enum CtrlOp {
   kCtrlResidualK0 = 0,   // res norms of r0 (+ err) -> state, record row 0

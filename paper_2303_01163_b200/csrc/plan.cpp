@@ -176,25 +176,30 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
   s.dim = dim;
   for (int a = 0; a < 3; ++a) s.ext[a] = a < dim ? ext[a] : 1;
 
-  // Line axis: the time axis if present (its backward stencil is defective), else the axis
-  // whose eigenvector scaling is worst conditioned; ties go to the slowest axis, whose lines
-  // coalesce across threads.
+  // Line axis L: the time axis if present (its backward stencil is defective).  Otherwise the
+  // longest axis (a dense eigenvector transform costs O(extent) per point, so the long axis
+  // is the one solved by line recurrences); ties go to the slowest axis, whose lines coalesce
+  // across threads.  If another axis' eigenvector scaling is too ill-conditioned it becomes L.
+  auto cond_of = [&](int a) -> ld {
+    const ld l = st.left[a], r = st.right[a];
+    if (r == 0 || l == 0) return 1e300L;
+    return std::exp(std::fabs(0.5L * std::log(std::fabs(l / r))) * static_cast<ld>(s.ext[a] - 1));
+  };
   if (time_axis_in_box >= 0) {
     s.L = time_axis_in_box;
   } else if (prefer_line_axis >= 0) {
     s.L = prefer_line_axis;
   } else {
-    ld best = -1;
-    for (int a = 0; a < dim; ++a) {
-      const ld l = st.left[a], r = st.right[a];
-      ld score = 0;
-      if (r != 0 && l != 0) score = std::fabs(0.5L * std::log(std::fabs(l / r))) * static_cast<ld>(s.ext[a] + 1);
-      score += 1e-9L * static_cast<ld>(s.ext[a]);
-      if (score >= best) {
-        best = score;
-        s.L = a;
+    s.L = dim - 1;
+    for (int a = dim - 1; a >= 0; --a)
+      if (s.ext[a] > s.ext[s.L]) s.L = a;
+    int bad = -1, nbad = 0;
+    for (int a = 0; a < dim; ++a)
+      if (a != s.L && cond_of(a) > 1e4L) {
+        bad = a;
+        ++nbad;
       }
-    }
+    if (nbad == 1 && cond_of(s.L) <= 1e4L) s.L = bad;
   }
   std::vector<AxisEigen> eig(3);
   for (int a = 0; a < dim; ++a) {
@@ -220,6 +225,11 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
     } else {
       s.W[a] = upload(dev, to_real(e.W));
       s.V[a] = upload(dev, to_real(e.V));
+      const int m = s.ext[a];
+      std::vector<double> wt(static_cast<size_t>(m) * m);
+      for (int k = 0; k < m; ++k)
+        for (int j = 0; j < m; ++j) wt[static_cast<size_t>(j) * m + k] = static_cast<double>(e.W[static_cast<size_t>(k) * m + j].real());
+      s.Wt[a] = upload(dev, wt);
     }
   }
 

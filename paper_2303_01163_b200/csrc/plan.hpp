@@ -99,6 +99,7 @@ struct SepSolver {
   // device tables
   double* W[3] = {nullptr, nullptr, nullptr};  // forward V^{-1}: [k][j]
   double* V[3] = {nullptr, nullptr, nullptr};  // backward V: [j][k]
+  double* Wt[3] = {nullptr, nullptr, nullptr}; // forward, transposed: [j][k] = W[k][j] (real only)
   double* th_ipiv = nullptr;  // [pos][combo]
   double* th_cp = nullptr;    // [pos][combo]
   int pcr_levels = 0;

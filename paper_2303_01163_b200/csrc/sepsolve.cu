@@ -6,12 +6,17 @@
 //   pcr_kernel       : parallel cyclic reduction for few long lines, one CTA per line,
 //                      precomputed elimination factors, line held in shared memory
 #include "sepsolve.cuh"
+#include "dmma_gemm.cuh"
+
+#include <cstdlib>
+#include <type_traits>
 
 namespace asdsm_b200 {
 
 namespace {
 
 constexpr int TP = 64, TQ = 64, TK = 16, NT = 256;
+constexpr int kPcrMaxSmem = 200 * 1024;
 
 template <typename T>
 struct Acc {
@@ -274,6 +279,26 @@ void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const Bo
   dim3 grid(static_cast<unsigned>((M.nlines + TP - 1) / TP), static_cast<unsigned>((m + TQ - 1) / TQ));
   const TIn* ip = reinterpret_cast<const TIn*>(in.ptr);
   TOut* op = reinterpret_cast<TOut*>(out.ptr);
+  if constexpr (std::is_same<TIn, double>::value && std::is_same<TMat, double>::value &&
+                std::is_same<TOut, double>::value) {
+    static const bool scalar = std::getenv("ASDSM_SCALAR_GEMM") != nullptr;
+    if (!scalar) {
+      GemmLines G{};
+      for (int i = 0; i < 2; ++i) {
+        G.o_ext[i] = M.o_ext[i];
+        G.o_in[i] = M.o_in[i];
+        G.o_out[i] = M.o_out[i];
+      }
+      for (int a = 0; a < 3; ++a) {
+        G.nbox[a] = M.nbox[a];
+        G.in_bs[a] = M.in_bs[a];
+        G.out_bs[a] = M.out_bs[a];
+      }
+      G.nlines = M.nlines;
+      launch_dmma_transform(ip, op, mat, m, in.stride[axis], out.stride[axis], G, st);
+      return;
+    }
+  }
   if (axis == 0)
     transform_kernel<TIn, TMat, TOut, true><<<grid, NT, 0, st>>>(ip, op, mat, m, in.stride[axis], out.stride[axis], M);
   else
@@ -325,8 +350,7 @@ void launch_line_solve(const SepSolver& S, const BoxArray& buf, cudaStream_t st)
     A.k2 = reinterpret_cast<const T*>(S.pcr_k2);
     A.invb = reinterpret_cast<const T*>(S.pcr_invb);
     const size_t smem = 2 * static_cast<size_t>(A.m) * sizeof(T);
-    ASDSM_CUDA_CHECK(cudaFuncSetAttribute(pcr_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
+    if (smem > kPcrMaxSmem) throw AsdsmError(kUnsupported, "PCR line longer than shared memory allows");
     pcr_kernel<T><<<static_cast<unsigned>(nb * S.ncombo), 1024, smem, st>>>(A);
   }
   ASDSM_CUDA_CHECK(cudaGetLastError());
@@ -334,6 +358,14 @@ void launch_line_solve(const SepSolver& S, const BoxArray& buf, cudaStream_t st)
 }
 
 }  // namespace
+
+void sep_prepare() {
+  static bool done = false;
+  if (done) return;
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(pcr_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(pcr_kernel<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  done = true;
+}
 
 size_t sep_scratch_bytes(const SepSolver& S, i64 nboxes) {
   return static_cast<size_t>(S.mode_size()) * nboxes * (S.complex_modes ? sizeof(cplx) : sizeof(double));

@@ -10,6 +10,10 @@ namespace asdsm_b200 {
 void sep_solve(const SepSolver& S, const BoxArray& in, const BoxArray& out, void* scratch0,
                void* scratch1, cudaStream_t stream);
 
+// One-time kernel attribute setup (large dynamic shared memory for PCR); call before any
+// stream capture.
+void sep_prepare();
+
 // Mode-space bytes one batch of `nboxes` needs per scratch buffer.
 size_t sep_scratch_bytes(const SepSolver& S, i64 nboxes);
 

@@ -4,7 +4,11 @@
 // without host synchronization and can be captured in a CUDA graph.
 #include "solver.hpp"
 
+#include "dmma_gemm.cuh"
+#include "holes2d.cuh"
+
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 
@@ -115,6 +119,7 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   }
   partials_ = dev_.alloc<double>(4 * kRedBlocks);
   state_ = dev_.alloc<DevState>(1);
+  sep_prepare();
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
 }
 
@@ -152,13 +157,12 @@ void Solver::set_bundle(const double* b_fine, const double* const* b_slab, const
   if (exact) ASDSM_CUDA_CHECK(cudaMemcpyAsync(exact_, exact, nf, kind, s));
 }
 
+Solver::~Solver() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+}
+
 void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
-  DevState h{};
-  h.cur = 0;
-  h.active = 1;
-  h.have_e = 1;
-  h.stop = 0;
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_state_init(state_, 1, 1, s);
   // stop_at from ||b||_2 (solver.cpp:570-571)
   launch_norm_sq(b_, g_fine_.size, partials_, state_, s);
   CtrlArgs c{};
@@ -191,6 +195,44 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
 }
 
 void Solver::fill(double* e, const double* b, cudaStream_t s) {
+  static const bool generic = std::getenv("ASDSM_GENERIC_FILL") != nullptr;
+  const SepSolver& H = sep_hole_;
+  if (!generic && mesh_.dim == 2 && b == nullptr && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
+    // Error mode: ring rhs + analytic forward transform + Thomas (one kernel), then the DMMA
+    // back transform straight into the hole positions of the fine array.
+    Hole2DArgs A{};
+    A.m0 = H.ext[0];
+    A.m1 = H.ext[1];
+    A.n0 = mesh_.n[0];
+    A.n1 = mesh_.n[1];
+    A.nf0 = mesh_.nf[0];
+    A.nf1 = mesh_.nf[1];
+    A.nbox0 = mesh_.nc[0] + 1;
+    A.nbox1 = mesh_.nc[1] + 1;
+    A.kb = 128;
+    A.st = st_fine_;
+    A.Wt = H.Wt[0];
+    A.ipiv = H.th_ipiv;
+    A.cp = H.th_cp;
+    A.line_left = H.line_left;
+    double* modes = static_cast<double*>(scratch0_);
+    launch_hole2d_fwd_thomas(e, modes, A, state_, s);
+    GemmLines G{};
+    G.o_ext[0] = A.m1;
+    G.o_ext[1] = 1;
+    G.o_in[0] = A.m0;
+    G.o_out[0] = g_fine_.stride[1];
+    G.nbox[0] = A.nbox0;
+    G.nbox[1] = A.nbox1;
+    G.nbox[2] = 1;
+    G.in_bs[0] = static_cast<i64>(A.m0) * A.m1;
+    G.in_bs[1] = static_cast<i64>(A.m0) * A.m1 * A.nbox0;
+    G.out_bs[0] = A.n0;
+    G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
+    G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
+    launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
+    return;
+  }
   launch_hole_rhs(mesh_.dim, e, b, fg_, st_fine_, md_, state_, s);
   const BoxArray h = hole_array(e);
   sep_solve(sep_hole_, h, h, scratch0_, scratch1_, s);
@@ -230,11 +272,14 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
 
 void Solver::run(const RunOptions& o, cudaStream_t s) {
   last_opts_ = o;
-  const long long l0 = g_kernel_launches;
   const int cap = std::max(o.max_iter, 0) + 1;
   if (cap > history_cap_) {
     history_ = dev_.alloc<double>(static_cast<size_t>(cap) * 7);
     history_cap_ = cap;
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
   }
   // Seeded draws (solver.cpp:110-120, 309-345): per iteration k the engine is
   // mt19937_64(mix_seed(seed, k)); 2D takes one draw % 2, 3D one % 3 then three % 2.
@@ -251,9 +296,50 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
   if (4 * cap > coins_cap_) {
     coins_ = dev_.alloc<int>(static_cast<size_t>(4 * cap));
     coins_cap_ = 4 * cap;
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
   }
   ASDSM_CUDA_CHECK(cudaMemcpyAsync(coins_, coins.data(), coins.size() * sizeof(int), cudaMemcpyHostToDevice, s));
 
+  static const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
+  if (no_graph || s == nullptr) {
+    const long long l0 = g_kernel_launches;
+    enqueue_run(o, s);
+    launches_ = g_kernel_launches - l0;
+    return;
+  }
+  const bool same = graph_exec_ && graph_opts_.tol == o.tol && graph_opts_.max_iter == o.max_iter &&
+                    graph_opts_.stagnation_window == o.stagnation_window &&
+                    graph_opts_.stagnation_ratio == o.stagnation_ratio;
+  if (!same) {
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    const long long l0 = g_kernel_launches;
+    ASDSM_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_run(o, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ASDSM_CUDA_CHECK(cudaStreamEndCapture(s, &g));
+    graph_launches_ = g_kernel_launches - l0;
+    const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+    cudaGraphDestroy(g);
+    ASDSM_CUDA_CHECK(e);
+    graph_opts_ = o;
+  }
+  ASDSM_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
+  launches_ = graph_launches_;
+}
+
+void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   reset_state(o, s);
   CtrlArgs c{};
   c.has_exact = has_exact_;
@@ -282,7 +368,6 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
     c.op = kCtrlAccept;
     launch_ctrl(c, partials_, state_, history_, s);
   }
-  launches_ = g_kernel_launches - l0;
 }
 
 int Solver::history(std::vector<double>& rows, int& stop_code, cudaStream_t s) const {
@@ -312,18 +397,12 @@ const double* Solver::r_current(cudaStream_t s) const {
 }
 
 void Solver::residual(const double* u, const double* b, double* r, cudaStream_t s) {
-  DevState h{};
-  h.active = 1;
-  h.have_e = 1;
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_state_init(state_, 1, 1, s);
   launch_stencil(mesh_.dim, false, u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_, state_, s);
 }
 
 void Solver::error_guess(const double* r, std::uint64_t seed, double* e, cudaStream_t s) {
-  DevState h{};
-  h.active = 1;
-  h.have_e = 1;
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_state_init(state_, 1, 1, s);
   if (coins_cap_ < 4) {
     coins_ = dev_.alloc<int>(4);
     coins_cap_ = 4;
@@ -349,10 +428,7 @@ void Solver::error_guess(const double* r, std::uint64_t seed, double* e, cudaStr
 }
 
 double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s) {
-  DevState h{};
-  h.active = 1;
-  h.have_e = 1;
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_state_init(state_, 1, 1, s);
   launch_ae_dots(mesh_.dim, e, r, r, fg_, st_fine_, partials_, state_, s);
   CtrlArgs c{};
   c.op = kCtrlStep;
@@ -369,10 +445,7 @@ double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s)
 
 void Solver::initial_guess(double* u_out, std::uint64_t seed, cudaStream_t s) {
   (void)seed;
-  DevState h{};
-  h.active = 1;
-  h.have_e = 1;
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(state_, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  launch_state_init(state_, 1, 1, s);
   smooth_guess(u_out, s);
 }
 

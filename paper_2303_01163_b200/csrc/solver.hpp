@@ -61,9 +61,11 @@ class Solver {
 
   // Launch count of the last run() (kernels of this library only).
   long long last_launches() const { return launches_; }
+  ~Solver();
 
  private:
   void reset_state(const RunOptions& o, cudaStream_t s);
+  void enqueue_run(const RunOptions& o, cudaStream_t s);
   void smooth_guess(double* out, cudaStream_t s);
   void error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s);
   void skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s);
@@ -106,6 +108,9 @@ class Solver {
   RunOptions last_opts_{};
   double cell_ = 1.0;
   long long launches_ = 0;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  RunOptions graph_opts_{};
+  long long graph_launches_ = 0;
 };
 
 }  // namespace asdsm_b200
