@@ -112,3 +112,13 @@ def csr_residual_exact(bundle, u, b=None):
         idx = rp[rows] + slot
         acc[rows] = acc[rows] + val[idx] * u[col[idx]]
     return b - acc
+
+
+def eval_floor(bundle, u):
+    """fp64 evaluation floor of the residual: eps * || |A| |u| ||_2 (A from the reference CSR)."""
+    rp, col, val = bundle["A_rowptr"], bundle["A_col"], bundle["A_val"]
+    n = len(rp) - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    absau = np.zeros(n)
+    np.add.at(absau, rows, np.abs(val) * np.abs(u[col]))
+    return np.finfo(np.float64).eps * float(np.linalg.norm(absau))

@@ -3,16 +3,19 @@
 Tolerances:
   * index maps, residual evaluation: bit-exact.
   * initial guess / final solution: max-norm relative 1e-10.
-  * per-iteration residual norms: relative max(1e-10, 10x the reference's own reproducibility
-    floor up to that iteration), the floor measured live by re-running the reference with a
-    different (equally valid) fill ordering of its direct solver (Cuthill-McKee instead of
-    reverse Cuthill-McKee in the Eigen stand-in).
+  * per-iteration residual norms: |d res_k| <= max(1e-10 * res_k, 10 * spread_k * res_k,
+    eps * || |A| |u| ||_2), where spread_k is the reference's own reproducibility floor up to
+    iteration k (relative spread of its history when re-run with a different, equally valid
+    fill ordering of its direct solver: Cuthill-McKee instead of reverse Cuthill-McKee), and
+    the last term is the fp64 evaluation floor of b - A u itself (no two implementations
+    whose iterates differ in the last bit can agree on the residual more closely).
 """
 import numpy as np
 import pytest
 
 import paper_2303_01163_b200 as pb
-from ref_tools import csr_residual_exact, have_ref, ref_bundle, ref_error_guess, ref_iterate, ref_maps
+from ref_tools import (csr_residual_exact, eval_floor, have_ref, ref_bundle, ref_error_guess, ref_iterate,
+                       ref_maps)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")]
 
@@ -106,7 +109,8 @@ def test_iterate_history(spec, nf, nc, iters, seed):
     got = np.array([h.res_l2 for h in st.history])
     want = ref["hist"][:, 1]
     assert len(got) == len(want)
-    tol = want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, seed, ref))
+    tol = np.maximum(want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, seed, ref)),
+                     eval_floor(ref_bundle(spec, nf, nc), ref["u"]))
     bad = np.abs(got - want) > tol
     assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
     s_got = np.array([h.s_hat for h in st.history[1:]])
