@@ -109,6 +109,14 @@ int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev);
 /* Kernels this library launched during the last iterate call. */
 int64_t asdsm_last_launch_count(const asdsm_plan* plan);
 
+/* The plan's own stream (cudaStream_t as void*). */
+void* asdsm_plan_stream(asdsm_plan* plan);
+/* Component timing after an iterate call: each component of one ASDSM iteration launched
+ * `reps` times between CUDA events on `stream`; per launch: ms, algorithmic bytes and
+ * flops, and launches per solve.  names: 64 chars per component. */
+int asdsm_profile_components(asdsm_plan* plan, void* stream, int reps, int max_components, char* names, double* ms,
+                             double* bytes, double* flops, int* per_solve, int* count);
+
 /* ---- single operations for parity tests (host arrays) ------------------------------- */
 int asdsm_residual(asdsm_plan* plan, const double* u, const double* b, double* r);     /* fdm.hpp:50 */
 int asdsm_initial_guess(asdsm_plan* plan, double* u_out);                              /* solver.hpp:132 (smooth) */

@@ -260,6 +260,25 @@ int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev) 
 
 int64_t asdsm_last_launch_count(const asdsm_plan* plan) { return plan->solver->last_launches(); }
 
+void* asdsm_plan_stream(asdsm_plan* plan) { return plan->stream; }
+
+int asdsm_profile_components(asdsm_plan* plan, void* stream, int reps, int max_components, char* names, double* ms,
+                             double* bytes, double* flops, int* per_solve, int* count) {
+  return guarded([&] {
+    const auto comps = plan->solver->profile(stream ? as_stream(stream) : plan->stream, reps);
+    const int n = std::min<int>(max_components, static_cast<int>(comps.size()));
+    for (int i = 0; i < n; ++i) {
+      std::strncpy(names + 64 * i, comps[static_cast<size_t>(i)].name.c_str(), 63);
+      names[64 * i + 63] = 0;
+      ms[i] = comps[static_cast<size_t>(i)].ms;
+      bytes[i] = comps[static_cast<size_t>(i)].bytes;
+      flops[i] = comps[static_cast<size_t>(i)].flops;
+      per_solve[i] = comps[static_cast<size_t>(i)].per_solve;
+    }
+    *count = n;
+  });
+}
+
 int asdsm_residual(asdsm_plan* plan, const double* u, const double* b, double* r) {
   return guarded([&] {
     Solver& S = *plan->solver;

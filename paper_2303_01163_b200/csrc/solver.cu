@@ -450,3 +450,92 @@ void Solver::initial_guess(double* u_out, std::uint64_t seed, cudaStream_t s) {
 }
 
 }  // namespace asdsm_b200
+
+namespace asdsm_b200 {
+
+std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
+  std::vector<Component> out;
+  cudaEvent_t e0, e1;
+  ASDSM_CUDA_CHECK(cudaEventCreate(&e0));
+  ASDSM_CUDA_CHECK(cudaEventCreate(&e1));
+  const i64 N = g_fine_.size;
+  const i64 NH = mesh_.hole_count();
+  const int iters = std::max(last_opts_.max_iter, 1);
+  auto timed = [&](const char* name, double bytes, double flops, int per_solve, auto&& body) {
+    launch_state_init(state_, 1, 1, s);
+    body();  // warm
+    ASDSM_CUDA_CHECK(cudaEventRecord(e0, s));
+    for (int i = 0; i < reps; ++i) body();
+    ASDSM_CUDA_CHECK(cudaEventRecord(e1, s));
+    ASDSM_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    ASDSM_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    Component c;
+    c.name = name;
+    c.ms = ms / reps;
+    c.bytes = bytes;
+    c.flops = flops;
+    c.per_solve = per_solve;
+    out.push_back(c);
+  };
+  // a non-zero step so the update kernel does its work
+  auto set_step = [&]() {
+    CtrlArgs c{};
+    c.op = kCtrlStep;
+    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s);
+    launch_ctrl(c, partials_, state_, history_, s);
+  };
+  const double ex = has_exact_ ? 1.0 : 0.0;
+  timed("update_residual", 8.0 * N * (5.0 + ex), 0.0, iters, [&] {
+    launch_state_init(state_, 1, 1, s);
+    set_step();
+    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr, fg_,
+                   st_fine_, partials_, state_, s);
+  });
+  // the stencil-only time is what we want: subtract the set_step part measured alone
+  timed("step_dots", 8.0 * N * 2.0, 0.0, iters, [&] { set_step(); });
+  out[0].ms -= out[1].ms;
+  const SepSolver& H = sep_hole_;
+  double hflops = 0;
+  for (int i = 0; i < H.nd; ++i) hflops += 2.0 * 2.0 * H.ext[H.dax[i]] * static_cast<double>(NH);
+  timed("hole_fill", 8.0 * NH * 3.0, hflops, iters, [&] { fill(e_, nullptr, s); });
+  if (mesh_.dim == 2 && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
+    GemmLines G{};
+    G.o_ext[0] = H.ext[1];
+    G.o_ext[1] = 1;
+    G.o_in[0] = H.ext[0];
+    G.o_out[0] = g_fine_.stride[1];
+    G.nbox[0] = mesh_.nc[0] + 1;
+    G.nbox[1] = mesh_.nc[1] + 1;
+    G.nbox[2] = 1;
+    G.in_bs[0] = static_cast<i64>(H.ext[0]) * H.ext[1];
+    G.in_bs[1] = G.in_bs[0] * G.nbox[0];
+    G.out_bs[0] = mesh_.n[0];
+    G.out_bs[1] = static_cast<i64>(mesh_.n[1]) * g_fine_.stride[1];
+    G.nlines = static_cast<i64>(H.ext[1]) * G.nbox[0] * G.nbox[1];
+    timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
+          [&] { launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s); });
+  }
+  i64 slab_pts = 0;
+  for (int a = 0; a < mesh_.dim; ++a) slab_pts += g_slab_[a].size;
+  timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
+    for (int a = 0; a < mesh_.dim; ++a) {
+      launch_gather(r_[0], r_[1], rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
+      sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
+                scratch1_, s);
+    }
+  });
+  timed("skeleton_merge", 8.0 * slab_pts * 2.0, 0.0, iters, [&] {
+    const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
+    skeleton(sol, nullptr, coins_, e_, s);
+  });
+  timed("residual", 8.0 * N * 3.0, 0.0, 1, [&] {
+    launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
+                   partials_, state_, s);
+  });
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return out;
+}
+
+}  // namespace asdsm_b200

@@ -2,6 +2,7 @@
 // SolverContext + asdsm_iterate (proj/include/asdsm/solver.hpp:114-163).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "kernels.cuh"
@@ -58,6 +59,15 @@ class Solver {
   void initial_guess(double* u_out, std::uint64_t seed, cudaStream_t s);
 
   const MeshDev& mesh_dev() const { return md_; }
+
+  // Component timing for the roofline (CUDA events on `s`, `reps` launches each, after a
+  // run()).  Names/ms/bytes/flops per launch and launches per solve.
+  struct Component {
+    std::string name;
+    double ms = 0, bytes = 0, flops = 0;
+    int per_solve = 0;
+  };
+  std::vector<Component> profile(cudaStream_t s, int reps);
 
   // Launch count of the last run() (kernels of this library only).
   long long last_launches() const { return launches_; }
