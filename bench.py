@@ -104,6 +104,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def max_over_ranks(value, device):
+    """Max of a per-rank scalar over all ranks (timings: the slowest rank defines the step)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def reference_solve(cid, seed, iters):
     """One solve of the compiled reference (oracle/_ref: the reference's own sources); returns
     (solve seconds excluding context setup, history rows)."""
@@ -213,11 +224,7 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = ctx.launch_count()
-    ms = float(np.mean(times))
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(float(np.mean(times)), "cuda")
     value = world * ndof * iters / (ms / 1e3)
 
     hist = np.empty((iters + 1) * 7)
@@ -303,11 +310,7 @@ def main():
         bb.record(pstream)
         bb.synchronize()
         etimes.append(a.elapsed_time(bb))
-    ems = float(np.mean(etimes))
-    if world > 1:
-        t = torch.tensor([ems], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ems = float(t.item())
+    ems = max_over_ranks(float(np.mean(etimes)), "cuda")
     h2d = 8 * (b["fine"].size + sum(x.size for x in b["aniso"]) + b["coarse"].size + (ndof if h_exact is not None else 0))
     d2h = 8 * (2 * ndof + (iters + 1) * 7)
     e2e = {"value": world * ndof * iters / (ems / 1e3), "unit": "DOF-iter/s", "h2d_bytes_per_step": int(h2d),
