@@ -1,0 +1,163 @@
+// Device-side control logic and the last-block reduction fold (header-only so every
+// translation unit's reduction kernels can finish with the control op, no separate launch).
+#pragma once
+#include "kernels.cuh"
+
+namespace asdsm_b200 {
+
+__device__ __forceinline__ double ctrl_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-shape reduction of the kRedBlocks partials of one slot.
+__device__ inline double ctrl_reduce(const double* part, bool is_max) {
+  __shared__ double sh[kRedThreads];
+  double v = is_max ? 0.0 : 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v = is_max ? fmax(v, __ldcg(part + i)) : v + __ldcg(part + i);
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = is_max ? fmax(sh[threadIdx.x], sh[threadIdx.x + w]) : sh[threadIdx.x] + sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Control logic of one reduction (thread 0 of the reducing block).
+__device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, double s2, double m3, DevState* S,
+                           double* history) {
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  auto record = [&](int k, double s_hat) {
+    double* row = history + static_cast<i64>(k) * 7;
+    row[0] = k;
+    row[1] = S->res_l2;
+    row[2] = S->res_inf;
+    row[3] = S->err_max;
+    row[4] = S->err_l2;
+    row[5] = s_hat;
+    row[6] = 0.0;
+    S->nrec = k + 1;
+  };
+  switch (c.op) {
+    case kCtrlResidualK0: {
+      S->res_l2 = sqrt(s0);
+      S->res_inf = m1;
+      S->err_max = c.has_exact ? m3 : nan;
+      S->err_l2 = c.has_exact ? sqrt(s2 * c.cell) : nan;
+      record(0, nan);
+      if (S->res_l2 <= S->stop_at) {
+        S->stop = 1;
+        S->active = 0;
+      } else if (c.max_iter <= 0) {
+        S->stop = 3;
+        S->active = 0;
+      }
+      S->have_e = 1;
+      break;
+    }
+    case kCtrlInit: {
+      S->b_l2 = sqrt(s0);
+      S->stop_at = c.tol * (S->b_l2 > 0.0 ? S->b_l2 : 1.0);
+      break;
+    }
+    case kCtrlSlabNorms2: {
+      const double n0 = sqrt(s0), n1 = sqrt(s2);
+      S->slab_norm[0] = n0;
+      S->slab_norm[1] = n1;
+      if (!(n0 > 0.0) || !(n1 > 0.0)) S->have_e = 0;
+      break;
+    }
+    case kCtrlSlabNorm: {
+      const double n = sqrt(s0);
+      S->slab_norm[c.which] = n;
+      if (!(n > 0.0)) S->have_e = 0;
+      break;
+    }
+    case kCtrlStep: {
+      double s = 0.0;
+      if (S->have_e) {
+        S->num = s0;
+        S->den = s2;
+        if (s2 > 0.0) {
+          const double q = s0 / s2;
+          s = (0.0 < q) ? q : 0.0;
+        }
+      }
+      S->s = s;
+      break;
+    }
+    case kCtrlAccept: {
+      double s = S->s;
+      if (s != 0.0) {
+        const double nl2 = sqrt(s0);
+        if (nl2 > S->res_l2 * c.tol_growth) {
+          s = 0.0;
+        } else {
+          S->cur = 1 - S->cur;
+          S->res_l2 = nl2;
+          S->res_inf = m1;
+          if (c.has_exact) {
+            S->err_max = m3;
+            S->err_l2 = sqrt(s2 * c.cell);
+          }
+        }
+      }
+      S->s = s;
+      record(c.k, s);
+      if (S->res_l2 <= S->stop_at) {
+        S->stop = 1;
+      } else if (c.stagnation_window > 0 && c.k >= c.stagnation_window) {
+        const double then = history[static_cast<i64>(c.k - c.stagnation_window) * 7 + 1];
+        if (S->res_l2 > then * c.stagnation_pow) S->stop = 2;
+      }
+      if (S->stop == 0 && c.k >= c.max_iter) S->stop = 3;
+      if (S->stop != 0) S->active = 0;
+      S->have_e = 1;
+      break;
+    }
+  }
+}
+
+static __global__ void __launch_bounds__(kRedThreads) ctrl_kernel(CtrlArgs c, const double* partials, DevState* S,
+                                                          double* history) {
+  if (!S->active) return;
+  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
+  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
+  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
+  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
+  if (threadIdx.x != 0) return;
+  ctrl_apply(c, s0, m1, s2, m3, S, history);
+}
+
+// Last-block fold: after every block has written its partials, the last block to finish
+// reduces them in a fixed order and applies the control op -- no separate ctrl launch.
+
+__device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history) {
+  if (c.op < 0) return;
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(&S->red_counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
+  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
+  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
+  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
+  if (threadIdx.x == 0) {
+    ctrl_apply(c, s0, m1, s2, m3, S, history);
+    S->red_counter = 0;
+    __threadfence();
+  }
+}
+
+
+}  // namespace asdsm_b200

@@ -37,8 +37,8 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
   __shared__ double Bs[BQ][BK + PAD];
   __shared__ i64 s_ib[BP], s_ob[BP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const i64 p0 = static_cast<i64>(blockIdx.x) * BP;
-  const int q0 = blockIdx.y * BQ;
+  const i64 p0 = static_cast<i64>(blockIdx.y) * BP;  // grid = (q tiles, line blocks)
+  const int q0 = blockIdx.x * BQ;
   if (tid < BP) {
     i64 ib = 0, ob = 0;
     if (p0 + tid < L.nlines) line_base(L, p0 + tid, ib, ob);
@@ -128,7 +128,11 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
 
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((L.nlines + BP - 1) / BP), static_cast<unsigned>((m + BQ - 1) / BQ));
+  // q tiles fastest: the CTAs re-reading the same A rows are co-scheduled (L2 hits)
+  const i64 pb = (L.nlines + BP - 1) / BP;
+  const unsigned qb = static_cast<unsigned>((m + BQ - 1) / BQ);
+  if (pb > 65535) throw AsdsmError(kUnsupported, "transform batch too large for the grid");
+  dim3 grid(qb, static_cast<unsigned>(pb));
   const bool ci = in_es == 1, co = out_es == 1;
   if (ci && co) dmma_transform_kernel<true, true><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
   else if (ci) dmma_transform_kernel<true, false><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);

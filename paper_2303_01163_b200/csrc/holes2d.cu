@@ -32,6 +32,8 @@ __device__ __forceinline__ double ring_rhs(const double* __restrict__ e, const H
 
 __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* __restrict__ modes, Hole2DArgs A,
                                          const DevState* state) {
+  const double* __restrict__ ipiv = A.ipiv;
+  const double* __restrict__ cpv = A.cp;
   if (!state->active || !state->have_e) return;
   extern __shared__ double sm[];
   const int m0 = A.m0, m1 = A.m1, KB = blockDim.x;
@@ -39,6 +41,7 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
   double* fR = fL + m1;
   double* fB = fR + m1;
   double* fT = fB + m0;
+  double* ys = fT + m0;  // [m1][KB] when A.y_in_smem
   const int hole = blockIdx.x;
   const int hx = hole % A.nbox0, hy = hole / A.nbox0;
   const int ox = hx * A.n0, oy = hy * A.n1;
@@ -70,28 +73,31 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
     if (j == 0) f = fb;
     else if (j == m1 - 1) f = ft;
     else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
-    const double iv = A.ipiv[static_cast<i64>(j) * m0 + k];
+    const double iv = __ldg(ipiv + static_cast<i64>(j) * m0 + k);
     y = (j == 0) ? f * iv : (f - l * y) * iv;
-    out[static_cast<i64>(j) * m0 + k] = y;
+    if (A.y_in_smem) ys[j * KB + threadIdx.x] = y;
+    else out[static_cast<i64>(j) * m0 + k] = y;
   }
   // backward sweep, mode layout [hole][j][k]
   double x = y;
+  out[static_cast<i64>(m1 - 1) * m0 + k] = x;
   for (int j = m1 - 2; j >= 0; --j) {
-    x = out[static_cast<i64>(j) * m0 + k] - A.cp[static_cast<i64>(j) * m0 + k] * x;
+    const double yj = A.y_in_smem ? ys[j * KB + threadIdx.x] : out[static_cast<i64>(j) * m0 + k];
+    x = yj - __ldg(cpv + static_cast<i64>(j) * m0 + k) * x;
     out[static_cast<i64>(j) * m0 + k] = x;
   }
 }
 
 }  // namespace
 
-size_t hole2d_smem_bytes(int m0, int m1, int kb) {
-  (void)kb;
-  return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0));
+size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem) {
+  return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0) +
+                           (y_in_smem ? static_cast<size_t>(m1) * kb : 0));
 }
 
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s) {
   const int kb = A.kb;
-  const size_t smem = hole2d_smem_bytes(A.m0, A.m1, kb);
+  const size_t smem = hole2d_smem_bytes(A.m0, A.m1, kb, A.y_in_smem);
   dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m0 + kb - 1) / kb));
   hole2d_fwd_thomas_kernel<<<grid, kb, smem, s>>>(e, modes, A, state);
   ASDSM_CUDA_CHECK(cudaGetLastError());

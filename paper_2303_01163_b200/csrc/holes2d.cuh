@@ -14,9 +14,10 @@ struct Hole2DArgs {
   const double* ipiv;  // Thomas pivots [j][k]
   const double* cp;    // Thomas upper factors [j][k]
   double line_left;
+  int y_in_smem;     // park the forward sweep in shared memory (else in the mode buffer)
 };
 
-size_t hole2d_smem_bytes(int m0, int m1, int kb);
+size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem);
 void hole2d_prepare(size_t smem);
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);
 

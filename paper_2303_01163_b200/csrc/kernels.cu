@@ -14,6 +14,7 @@
 
 #include "kernels.cuh"
 #include "spline.cuh"
+#include "ctrl.cuh"
 
 namespace asdsm_b200 {
 
@@ -66,6 +67,7 @@ __device__ void block_reduce4(double s0, double m1, double s2, double m3, double
   }
 }
 
+
 struct StencilArgs {
   const double* u0;
   const double* u1;
@@ -80,6 +82,8 @@ struct StencilArgs {
   Stencil st;
   double* partials;
   DevState* state;
+  CtrlArgs ctrl;
+  double* history;
 };
 
 // A*v at fine point (i,j,k) in the CSR column order of fdm.cpp:110-117, no contraction.
@@ -105,13 +109,11 @@ __device__ __forceinline__ double apply_row(const FineGeom& g, const Stencil& st
 // plus per-block partials of sum r^2, max |r|, sum d^2, max |d| (d = u - exact).
 template <int DIM, bool UPDATE>
 __global__ void __launch_bounds__(kRedThreads) stencil_kernel(StencilArgs a) {
-  const DevState* S = a.state;
+  DevState* S = a.state;
   if (!S->active) return;
   double s = 0.0;
-  if (UPDATE) {
-    s = S->s;
-    if (s == 0.0) return;
-  }
+  if (UPDATE) s = S->s;
+  const bool work = !UPDATE || s != 0.0;
   const int cur = S->cur;
   const double* __restrict__ u = cur ? a.u1 : a.u0;
   double* __restrict__ uo = UPDATE ? (cur ? a.uo0 : a.uo1) : nullptr;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kRedThreads) stencil_kernel(StencilArgs a) {
     if (UPDATE) return add_rn(u[q], mul_rn(s, e[q]));
     return u[q];
   };
-  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+  for (i64 it = work ? blockIdx.x : items; it < items; it += gridDim.x) {
     const i64 row = it / nseg;
     const int i = static_cast<int>((it % nseg) * blockDim.x + threadIdx.x);
     if (i >= g.ext[0]) continue;
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(kRedThreads) stencil_kernel(StencilArgs a) {
     }
   }
   block_reduce4(ssq, rmax, esq, emax, a.partials);
+  fold_ctrl(a.ctrl, a.partials, S, a.history);
 }
 
 struct DotArgs {
@@ -157,13 +160,16 @@ struct DotArgs {
   Stencil st;
   double* partials;
   DevState* state;
+  CtrlArgs ctrl;
+  double* history;
 };
 
 // w = A e (all rows, sparse.cpp:49-58 order); partial <r, w> and <w, w> (solver.cpp:456-461).
 template <int DIM>
 __global__ void __launch_bounds__(kRedThreads) ae_dots_kernel(DotArgs a) {
-  const DevState* S = a.state;
-  if (!S->active || !S->have_e) return;
+  DevState* S = a.state;
+  if (!S->active) return;
+  const bool work = S->have_e;
   const double* __restrict__ r = S->cur ? a.r1 : a.r0;
   const double* __restrict__ e = a.e;
   const FineGeom& g = a.g;
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(kRedThreads) ae_dots_kernel(DotArgs a) {
   const i64 items = rows * nseg;
   double num = 0.0, den = 0.0;
   auto V = [&](i64 q, int, int) -> double { return e[q]; };
-  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+  for (i64 it = work ? blockIdx.x : items; it < items; it += gridDim.x) {
     const i64 row = it / nseg;
     const int i = static_cast<int>((it % nseg) * blockDim.x + threadIdx.x);
     if (i >= g.ext[0]) continue;
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(kRedThreads) ae_dots_kernel(DotArgs a) {
     den += w * w;
   }
   block_reduce4(num, 0.0, den, 0.0, a.partials);
+  fold_ctrl(a.ctrl, a.partials, S, a.history);
 }
 
 // Restriction r -> one tensor submesh (Projector::apply with build_projector's map,
@@ -215,13 +222,14 @@ __global__ void gather_kernel(const double* src0, const double* src1, double* ds
 }
 
 __global__ void __launch_bounds__(kRedThreads) norm_sq_kernel(const double* x, i64 n, double* partials,
-                                                             const DevState* state) {
+                                                             DevState* state, CtrlArgs c, double* history) {
   if (!state->active) return;
   double s = 0.0;
   for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
        t += static_cast<i64>(gridDim.x) * blockDim.x)
     s += x[t] * x[t];
   block_reduce4(s, 0.0, 0.0, 0.0, partials);
+  fold_ctrl(c, partials, state, history);
 }
 
 // normalize_or_throw (solver.cpp:79-84): v /= ||v||_2 element by element.
@@ -233,115 +241,6 @@ __global__ void divide_kernel(double* x, i64 n, const double* divisor, const Dev
     x[t] = x[t] / d;
 }
 
-// Fixed-shape reduction of the kRedBlocks partials of one slot.
-__device__ double ctrl_reduce(const double* part, bool is_max) {
-  __shared__ double sh[kRedThreads];
-  double v = is_max ? 0.0 : 0.0;
-  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v = is_max ? fmax(v, part[i]) : v + part[i];
-  sh[threadIdx.x] = v;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] = is_max ? fmax(sh[threadIdx.x], sh[threadIdx.x + w]) : sh[threadIdx.x] + sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  const double r = sh[0];
-  __syncthreads();
-  return r;
-}
-
-__global__ void __launch_bounds__(kRedThreads) ctrl_kernel(CtrlArgs c, const double* partials, DevState* S,
-                                                          double* history) {
-  if (!S->active) return;
-  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
-  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
-  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
-  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
-  if (threadIdx.x != 0) return;
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  auto record = [&](int k, double s_hat) {
-    double* row = history + static_cast<i64>(k) * 7;
-    row[0] = k;
-    row[1] = S->res_l2;
-    row[2] = S->res_inf;
-    row[3] = S->err_max;
-    row[4] = S->err_l2;
-    row[5] = s_hat;
-    row[6] = 0.0;
-    S->nrec = k + 1;
-  };
-  switch (c.op) {
-    case kCtrlResidualK0: {
-      S->res_l2 = sqrt(s0);
-      S->res_inf = m1;
-      S->err_max = c.has_exact ? m3 : nan;
-      S->err_l2 = c.has_exact ? sqrt(s2 * c.cell) : nan;
-      record(0, nan);
-      if (S->res_l2 <= S->stop_at) {
-        S->stop = 1;
-        S->active = 0;
-      } else if (c.max_iter <= 0) {
-        S->stop = 3;
-        S->active = 0;
-      }
-      S->have_e = 1;
-      break;
-    }
-    case kCtrlInit: {
-      S->b_l2 = sqrt(s0);
-      S->stop_at = c.tol * (S->b_l2 > 0.0 ? S->b_l2 : 1.0);
-      break;
-    }
-    case kCtrlSlabNorm: {
-      const double n = sqrt(s0);
-      S->slab_norm[c.which] = n;
-      if (!(n > 0.0)) S->have_e = 0;
-      break;
-    }
-    case kCtrlStep: {
-      double s = 0.0;
-      if (S->have_e) {
-        S->num = s0;
-        S->den = s2;
-        if (s2 > 0.0) {
-          const double q = s0 / s2;
-          s = (0.0 < q) ? q : 0.0;
-        }
-      }
-      S->s = s;
-      break;
-    }
-    case kCtrlAccept: {
-      double s = S->s;
-      if (s != 0.0) {
-        const double nl2 = sqrt(s0);
-        if (nl2 > S->res_l2 * c.tol_growth) {
-          s = 0.0;
-        } else {
-          S->cur = 1 - S->cur;
-          S->res_l2 = nl2;
-          S->res_inf = m1;
-          if (c.has_exact) {
-            S->err_max = m3;
-            S->err_l2 = sqrt(s2 * c.cell);
-          }
-        }
-      }
-      S->s = s;
-      record(c.k, s);
-      if (S->res_l2 <= S->stop_at) {
-        S->stop = 1;
-      } else if (c.stagnation_window > 0 && c.k >= c.stagnation_window) {
-        const double then = history[static_cast<i64>(c.k - c.stagnation_window) * 7 + 1];
-        if (S->res_l2 > then * c.stagnation_pow) S->stop = 2;
-      }
-      if (S->stop == 0 && c.k >= c.max_iter) S->stop = 3;
-      if (S->stop != 0) S->active = 0;
-      S->have_e = 1;
-      break;
-    }
-  }
-}
-
 // ---------------------------------------------------------------- 2D skeleton --------------
 // Phase 1: cross values u_hat (Richardson u1 + u2 - u_cc, or the seeded choice) and the
 // corrections e1 = u_hat - P u_fc, e2 = u_hat - P u_cf (solver.cpp:166-184).
@@ -351,8 +250,12 @@ __global__ void skel2d_cc_kernel(Skel2DArgs a, const DevState* state) {
   const int ncc = m.nc[0] * m.nc[1];
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncc; t += gridDim.x * blockDim.x) {
     const int I = t % m.nc[0], J = t / m.nc[0];
-    const double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
-    const double u2 = a.u_cf[I + static_cast<i64>(m.nc[0]) * ((J + 1) * m.n[1] - 1)];
+    double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
+    double u2 = a.u_cf[I + static_cast<i64>(m.nc[0]) * ((J + 1) * m.n[1] - 1)];
+    if (a.norm_fc) {
+      u1 = u1 / *a.norm_fc;
+      u2 = u2 / *a.norm_cf;
+    }
     double uh;
     if (a.u_cc) {
       uh = __dsub_rn(__dadd_rn(u1, u2), a.u_cc[t]);
@@ -393,6 +296,46 @@ __global__ void skel2d_spline_kernel(Skel2DArgs a, double* work, const DevState*
   }
 }
 
+// Phases 1+2 in one CTA (coarse counts <= 62): cross values, corrections, spline second
+// derivatives with per-thread local arrays.
+__global__ void skel2d_ccspline_kernel(Skel2DArgs a, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const MeshDev& m = a.m;
+  const int nc0 = m.nc[0], nc1 = m.nc[1];
+  for (int t = threadIdx.x; t < nc0 * nc1; t += blockDim.x) {
+    const int I = t % nc0, J = t / nc0;
+    double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
+    double u2 = a.u_cf[I + static_cast<i64>(nc0) * ((J + 1) * m.n[1] - 1)];
+    if (a.norm_fc) {
+      u1 = u1 / *a.norm_fc;
+      u2 = u2 / *a.norm_cf;
+    }
+    double uh;
+    if (a.u_cc) uh = __dsub_rn(__dadd_rn(u1, u2), a.u_cc[t]);
+    else uh = (a.coin[0] == 0) ? u2 : u1;
+    a.e1[t] = __dsub_rn(uh, u1);
+    a.e2[t] = __dsub_rn(uh, u2);
+  }
+  __syncthreads();
+  constexpr int KM = 64;
+  for (int t = threadIdx.x; t < nc0 + nc1; t += blockDim.x) {
+    double y[KM], dg[KM], up[KM], rh[KM];
+    if (t < nc1) {
+      const int J = t;
+      y[0] = 0.0;
+      for (int C = 0; C < nc0; ++C) y[C + 1] = a.e1[C + static_cast<i64>(nc0) * J];
+      y[nc0 + 1] = 0.0;
+      spline_second_derivs(m, 0, y, a.m1 + static_cast<i64>(J) * (nc0 + 2), dg, up, rh);
+    } else {
+      const int I = t - nc1;
+      y[0] = 0.0;
+      for (int C = 0; C < nc1; ++C) y[C + 1] = a.e2[I + static_cast<i64>(nc0) * C];
+      y[nc1 + 1] = 0.0;
+      spline_second_derivs(m, 1, y, a.m2 + static_cast<i64>(I) * (nc1 + 2), dg, up, rh);
+    }
+  }
+}
+
 // Phase 3: corrected anisotropic values merged onto the skeleton points (solver.cpp:186-195):
 //   coarse-row points  : ut_fc = u_fc + S1_J(x_i)
 //   coarse-column points: ut_cf = u_cf + S2_I(y_j)
@@ -406,7 +349,9 @@ __global__ void skel2d_write_kernel(Skel2DArgs a, const DevState* state) {
   auto ut_cf = [&](int I, int j) {
     const double* mm2 = a.m2 + static_cast<i64>(I) * (nc1 + 2);
     auto y2 = [&](int c) -> double { return (c == 0 || c == nc1 + 1) ? 0.0 : a.e2[I + static_cast<i64>(nc0) * (c - 1)]; };
-    return __dadd_rn(a.u_cf[I + static_cast<i64>(nc0) * j], spline_eval(m, 1, y2, mm2, j + 1));
+    double u = a.u_cf[I + static_cast<i64>(nc0) * j];
+    if (a.norm_cf) u = u / *a.norm_cf;
+    return __dadd_rn(u, spline_eval(m, 1, y2, mm2, j + 1));
   };
   for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < nrow_pts + ncol_pts;
        t += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -416,7 +361,9 @@ __global__ void skel2d_write_kernel(Skel2DArgs a, const DevState* state) {
       const int j = (J + 1) * m.n[1] - 1;
       const double* mm1 = a.m1 + static_cast<i64>(J) * (nc0 + 2);
       auto y1 = [&](int c) -> double { return (c == 0 || c == nc0 + 1) ? 0.0 : a.e1[(c - 1) + static_cast<i64>(nc0) * J]; };
-      const double av = __dadd_rn(a.u_fc[i + static_cast<i64>(m.nf[0]) * J], spline_eval(m, 0, y1, mm1, i + 1));
+      double ufc = a.u_fc[i + static_cast<i64>(m.nf[0]) * J];
+      if (a.norm_fc) ufc = ufc / *a.norm_fc;
+      const double av = __dadd_rn(ufc, spline_eval(m, 0, y1, mm1, i + 1));
       double val = av;
       if ((i + 1) % m.n[0] == 0) {
         const double bv = ut_cf((i + 1) / m.n[0] - 1, j);
@@ -495,8 +442,12 @@ void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s) 
 
 void launch_stencil(int dim, bool update, const double* u0, const double* u1, const double* e, const double* b,
                     double* uo0, double* uo1, double* ro0, double* ro1, const double* exact, const FineGeom& g,
-                    const Stencil& st, double* partials, DevState* state, cudaStream_t s) {
-  StencilArgs a{u0, u1, e, b, uo0, uo1, ro0, ro1, exact, g, st, partials, state};
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s, const CtrlArgs* ctrl,
+                    double* history) {
+  CtrlArgs c{};
+  c.op = -1;
+  if (ctrl) c = *ctrl;
+  StencilArgs a{u0, u1, e, b, uo0, uo1, ro0, ro1, exact, g, st, partials, state, c, history};
   if (dim == 2) {
     if (update) stencil_kernel<2, true><<<kRedBlocks, kRedThreads, 0, s>>>(a);
     else stencil_kernel<2, false><<<kRedBlocks, kRedThreads, 0, s>>>(a);
@@ -509,8 +460,12 @@ void launch_stencil(int dim, bool update, const double* u0, const double* u1, co
 }
 
 void launch_ae_dots(int dim, const double* e, const double* r0, const double* r1, const FineGeom& g,
-                    const Stencil& st, double* partials, DevState* state, cudaStream_t s) {
-  DotArgs a{e, r0, r1, g, st, partials, state};
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s, const CtrlArgs* ctrl,
+                    double* history) {
+  CtrlArgs c{};
+  c.op = -1;
+  if (ctrl) c = *ctrl;
+  DotArgs a{e, r0, r1, g, st, partials, state, c, history};
   if (dim == 2) ae_dots_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(a);
   else ae_dots_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(a);
   ASDSM_CUDA_CHECK(cudaGetLastError());
@@ -526,8 +481,12 @@ void launch_gather(const double* src0, const double* src1, double* dst, const Me
   ++g_kernel_launches;
 }
 
-void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s) {
-  norm_sq_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, n, partials, state);
+void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s, const CtrlArgs* ctrl,
+                    double* history) {
+  CtrlArgs c{};
+  c.op = -1;
+  if (ctrl) c = *ctrl;
+  norm_sq_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, n, partials, state, c, history);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }
@@ -547,6 +506,16 @@ void launch_ctrl(const CtrlArgs& a, const double* partials, DevState* state, dou
 }
 
 void launch_skeleton2d(const Skel2DArgs& a, DevState* state, cudaStream_t s) {
+  if (a.m.nc[0] <= 62 && a.m.nc[1] <= 62) {
+    skel2d_ccspline_kernel<<<1, 256, 0, s>>>(a, state);
+    ASDSM_CUDA_CHECK(cudaGetLastError());
+    const i64 npts = static_cast<i64>(a.m.nc[1]) * a.m.nf[0] + static_cast<i64>(a.m.nc[0]) * a.m.nf[1];
+    const i64 nb = std::min<i64>((npts + 255) / 256, 4 * kNumSms);
+    skel2d_write_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(a, state);
+    ASDSM_CUDA_CHECK(cudaGetLastError());
+    g_kernel_launches += 2;
+    return;
+  }
   const int ncc = a.m.nc[0] * a.m.nc[1];
   g_kernel_launches += 2;
   skel2d_cc_kernel<<<(ncc + 255) / 256, 256, 0, s>>>(a, state);

@@ -15,7 +15,7 @@ struct DevState {
   int have_e;    // error guess exists (no ZeroNormSolution)
   int stop;      // 0 running, 1 tol, 2 stagnation, 3 max_iter
   int nrec;      // history rows written
-  int pad_;
+  unsigned red_counter;  // blocks finished in the current folded reduction
   double res_l2, res_inf, err_max, err_l2;
   double s;                      // step of the current iteration
   double num, den;               // <r, Ae>, <Ae, Ae>
@@ -38,15 +38,21 @@ struct MeshDev {  // mesh scalars the skeleton kernels need
   double h[3];
 };
 
-// Reductions: partials[slot * kRedBlocks + block]; slots: 0 sum, 1 max, 2 sum, 3 max.
+struct CtrlArgs;
+
+// Reductions: partials[slot * kRedBlocks + block]; slots: 0 sum, 1 max, 2 sum, 3 max.  With a
+// non-null `ctrl`, the last block to finish reduces the partials and applies the control op.
 void launch_stencil(int dim, bool update, const double* u0, const double* u1, const double* e, const double* b,
                     double* uo0, double* uo1, double* ro0, double* ro1, const double* exact, const FineGeom& g,
-                    const Stencil& st, double* partials, DevState* state, cudaStream_t s);
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s,
+                    const CtrlArgs* ctrl = nullptr, double* history = nullptr);
 void launch_ae_dots(int dim, const double* e, const double* r0, const double* r1, const FineGeom& g,
-                    const Stencil& st, double* partials, DevState* state, cudaStream_t s);
+                    const Stencil& st, double* partials, DevState* state, cudaStream_t s,
+                    const CtrlArgs* ctrl = nullptr, double* history = nullptr);
 void launch_gather(const double* src0, const double* src1, double* dst, const MeshDev& m, unsigned mask,
                    i64 count, DevState* state, cudaStream_t s);
-void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s);
+void launch_norm_sq(const double* x, i64 n, double* partials, DevState* state, cudaStream_t s,
+                    const CtrlArgs* ctrl = nullptr, double* history = nullptr);
 void launch_divide(double* x, i64 n, const double* divisor, DevState* state, cudaStream_t s);
 
 // Device-side state initialization (capturable in a CUDA graph; no host memcpy).
@@ -59,6 +65,7 @@ enum CtrlOp {
   kCtrlStep = 2,         // num/den -> s
   kCtrlAccept = 3,       // next norms; accept/revert; record row k; stop rules
   kCtrlInit = 4,         // ||b||_2 -> stop_at = tol * (||b|| > 0 ? ||b|| : 1)
+  kCtrlSlabNorms2 = 5,   // slot 0 / slot 2 sums -> slab_norm[0], slab_norm[1]; have_e
 };
 struct CtrlArgs {
   int op;
@@ -86,6 +93,8 @@ struct Skel2DArgs {
   double* m1;           // spline second derivatives, nc1 lines x (nc0+2)
   double* m2;           // nc0 lines x (nc1+2)
   double* out;          // fine array: skeleton points written
+  const double* norm_fc;  // error mode: ||u_fc||_2 (values are divided by it, solver.cpp:79-84), else null
+  const double* norm_cf;
 };
 void launch_skeleton2d(const Skel2DArgs& a, DevState* state, cudaStream_t s);
 

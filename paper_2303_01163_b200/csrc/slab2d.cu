@@ -1,0 +1,153 @@
+// 2D slab solves (the anisotropic systems A_fc, A_cf of Alg. 1, solved by the reference with
+// Eigen SparseLU, linsolve.cpp:58-66) as the paper's dimension-reduced line solves:
+//   launch 1, one CTA per (coarse mode k, slab): restriction of r onto the slab fused with the
+//            coarse-axis eigenvector transform, then PCR along the fine line in shared memory;
+//   launch 2: back transform to the slab layout + squared norms for normalize_or_throw
+//            (solver.cpp:79-84), the last block finalizing both norms.
+#include "slab2d.cuh"
+#include "ctrl.cuh"
+
+namespace asdsm_b200 {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kMaxSmem = 200 * 1024;
+
+template <typename T>
+__device__ __forceinline__ T ld(const double* p, i64 i);
+template <>
+__device__ __forceinline__ double ld<double>(const double* p, i64 i) { return __ldg(p + i); }
+template <>
+__device__ __forceinline__ cplx ld<cplx>(const double* p, i64 i) { return cplx{__ldg(p + 2 * i), __ldg(p + 2 * i + 1)}; }
+
+__device__ __forceinline__ void st_out(double* p, i64 i, double v) { p[i] = v; }
+__device__ __forceinline__ void st_out(double* p, i64 i, cplx v) { reinterpret_cast<cplx*>(p)[i] = v; }
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, const DevState* S) {
+  if (!S->active) return;
+  extern __shared__ unsigned char smem[];
+  const int a = blockIdx.y, f = 1 - a;
+  const MeshDev& m = A.m;
+  const int nc = m.nc[a], nf = m.nf[f], k = blockIdx.x;
+  if (k >= nc) return;
+  T* x0 = reinterpret_cast<T*>(smem);
+  T* x1 = x0 + nf;
+  const double* rf = A.in_fine0 ? (S->cur ? A.in_fine1 : A.in_fine0) : nullptr;
+  const i64 Nx = m.nf[0];
+  for (int x = threadIdx.x; x < nf; x += blockDim.x) {
+    T acc = zero_of<T>();
+    for (int j = 0; j < nc; ++j) {
+      double v;
+      const int fj = (j + 1) * m.n[a] - 1;  // station on the coarse axis
+      if (rf) v = (a == 0) ? rf[fj + Nx * x] : rf[x + Nx * fj];
+      else v = (a == 0) ? A.in_slab[a][j + static_cast<i64>(nc) * x] : A.in_slab[a][x + static_cast<i64>(nf) * j];
+      fma_acc(acc, ld<T>(A.W[a], static_cast<i64>(k) * nc + j), v);
+    }
+    x0[x] = acc;
+  }
+  __syncthreads();
+  const int L = A.levels[a];
+  const double* K1 = A.k1[a];
+  const double* K2 = A.k2[a];
+  int s = 1;
+  for (int lev = 0; lev < L; ++lev, s <<= 1) {
+    const i64 base = (static_cast<i64>(k) * L + lev) * nf;
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+      T v = x0[i];
+      if (i - s >= 0) v = v - ld<T>(K1, base + i) * x0[i - s];
+      if (i + s < nf) v = v - ld<T>(K2, base + i) * x0[i + s];
+      x1[i] = v;
+    }
+    __syncthreads();
+    T* t = x0;
+    x0 = x1;
+    x1 = t;
+  }
+  for (int i = threadIdx.x; i < nf; i += blockDim.x)
+    st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
+}
+
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, double* partials, DevState* S,
+                                                                   double* history, CtrlArgs c) {
+  if (!S->active) return;
+  const MeshDev& m = A.m;
+  double ss[2] = {0.0, 0.0};
+  for (int a = 0; a < 2; ++a) {
+    const int f = 1 - a, nc = m.nc[a], nf = m.nf[f];
+    const i64 n = static_cast<i64>(nc) * nf;
+    for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += static_cast<i64>(gridDim.x) * blockDim.x) {
+      int j, x;
+      if (a == 0) {
+        j = static_cast<int>(t % nc);
+        x = static_cast<int>(t / nc);
+      } else {
+        x = static_cast<int>(t % nf);
+        j = static_cast<int>(t / nf);
+      }
+      T acc = zero_of<T>();
+      for (int k = 0; k < nc; ++k) fma_acc(acc, ld<T>(A.V[a], static_cast<i64>(j) * nc + k), ld<T>(A.modes[a], static_cast<i64>(k) * nf + x));
+      const double v = real_part(acc);
+      A.sol[a][t] = v;
+      ss[a] += v * v;
+    }
+  }
+  // partial sums: slot 0 = slab 0, slot 2 = slab 1
+  __shared__ double sh[2][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int q = 0; q < 2; ++q) {
+    double v = ss[q];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[q][w] = v;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int q = 0; q < 2; ++q) {
+      double v = lane < nw ? sh[q][lane] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        partials[(2 * q) * kRedBlocks + blockIdx.x] = v;
+        partials[(2 * q + 1) * kRedBlocks + blockIdx.x] = 0.0;
+      }
+    }
+  }
+  fold_ctrl(c, partials, S, history);
+}
+
+}  // namespace
+
+void slab2d_prepare() {
+  static bool done = false;
+  if (done) return;
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(slab2d_fwd_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(slab2d_fwd_kernel<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+  done = true;
+}
+
+void launch_slab2d_fwd(const Slab2DArgs& A, DevState* st, cudaStream_t s) {
+  const int ncmax = std::max(A.m.nc[0], A.m.nc[1]);
+  const int nfmax = std::max(A.m.nf[0], A.m.nf[1]);
+  const size_t smem = 2 * static_cast<size_t>(nfmax) * (A.cplx ? sizeof(cplx) : sizeof(double));
+  if (smem > kMaxSmem) throw AsdsmError(kUnsupported, "2D slab line longer than shared memory allows");
+  dim3 grid(static_cast<unsigned>(ncmax), 2);
+  if (A.cplx) slab2d_fwd_kernel<cplx><<<grid, kThreads, smem, s>>>(A, st);
+  else slab2d_fwd_kernel<double><<<grid, kThreads, smem, s>>>(A, st);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_slab2d_back(const Slab2DArgs& A, double* partials, DevState* st, double* history, bool with_norms,
+                        cudaStream_t s) {
+  CtrlArgs c{};
+  c.op = with_norms ? kCtrlSlabNorms2 : -1;
+  if (A.cplx) slab2d_back_kernel<cplx><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c);
+  else slab2d_back_kernel<double><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+}  // namespace asdsm_b200

@@ -6,6 +6,7 @@
 
 #include "dmma_gemm.cuh"
 #include "holes2d.cuh"
+#include "slab2d.cuh"
 
 #include <cmath>
 #include <cstdlib>
@@ -120,6 +121,19 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   partials_ = dev_.alloc<double>(4 * kRedBlocks);
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
+  if (m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
+    fast2d_ = true;
+    for (int a = 0; a < 2; ++a) {
+      const SepSolver& S = sep_slab_[a];
+      fast2d_ = fast2d_ && S.use_pcr && S.nd == 1 && S.dax[0] == a && S.L == 1 - a &&
+                S.complex_modes == sep_slab_[0].complex_modes;
+    }
+    if (fast2d_) {
+      slab2d_prepare();
+      for (int a = 0; a < 2; ++a)
+        slab_modes_[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[1 - a] * 2);
+    }
+  }
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
 }
 
@@ -164,11 +178,10 @@ Solver::~Solver() {
 void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
   launch_state_init(state_, 1, 1, s);
   // stop_at from ||b||_2 (solver.cpp:570-571)
-  launch_norm_sq(b_, g_fine_.size, partials_, state_, s);
   CtrlArgs c{};
   c.op = kCtrlInit;
   c.tol = o.tol;
-  launch_ctrl(c, partials_, state_, history_, s);
+  launch_norm_sq(b_, g_fine_.size, partials_, state_, s, &c, history_);
 }
 
 void Solver::skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s) {
@@ -191,6 +204,10 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
   a.m1 = spl_m1_;
   a.m2 = spl_m2_;
   a.out = out;
+  if (fast2d_ && coin != nullptr) {  // normalized on the fly (values / norm, as normalize_or_throw)
+    a.norm_fc = &state_->slab_norm[1];
+    a.norm_cf = &state_->slab_norm[0];
+  }
   launch_skeleton2d(a, state_, s);
 }
 
@@ -209,7 +226,8 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nf1 = mesh_.nf[1];
     A.nbox0 = mesh_.nc[0] + 1;
     A.nbox1 = mesh_.nc[1] + 1;
-    A.kb = 128;
+    A.kb = 32;
+    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
     A.st = st_fine_;
     A.Wt = H.Wt[0];
     A.ipiv = H.th_ipiv;
@@ -238,8 +256,37 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
   sep_solve(sep_hole_, h, h, scratch0_, scratch1_, s);
 }
 
+static Slab2DArgs slab2d_args(const MeshDev& md, const SepSolver* S, double* const* modes, double* const* sol) {
+  Slab2DArgs A{};
+  A.m = md;
+  A.cplx = S[0].complex_modes ? 1 : 0;
+  for (int a = 0; a < 2; ++a) {
+    A.W[a] = S[a].W[a];
+    A.V[a] = S[a].V[a];
+    A.k1[a] = S[a].pcr_k1;
+    A.k2[a] = S[a].pcr_k2;
+    A.invb[a] = S[a].pcr_invb;
+    A.levels[a] = S[a].pcr_levels;
+    A.modes[a] = modes[a];
+    A.sol[a] = sol[a];
+  }
+  return A;
+}
+
 // Alg. 1 with the assembled bundle (solver.cpp:518-548, smooth mode).
 void Solver::smooth_guess(double* out, cudaStream_t s) {
+  if (fast2d_) {
+    Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
+    A.in_slab[0] = b_slab_[0];
+    A.in_slab[1] = b_slab_[1];
+    launch_slab2d_fwd(A, state_, s);
+    launch_slab2d_back(A, partials_, state_, history_, false, s);
+    sep_solve(sep_coarse_, kind_array(g_coarse_, b_coarse_), kind_array(g_coarse_, u_cc_), scratch0_, scratch1_, s);
+    const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
+    skeleton(sol, u_cc_, nullptr, out, s);
+    fill(out, b_, s);
+    return;
+  }
   for (int a = 0; a < mesh_.dim; ++a)
     sep_solve(sep_slab_[a], kind_array(g_slab_[a], b_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
               scratch1_, s);
@@ -252,17 +299,27 @@ void Solver::smooth_guess(double* out, cudaStream_t s) {
 // error_guess (solver.cpp:550-558): restrict r, solve the slabs, normalize, merge, fill
 // against a zero right-hand side.
 void Solver::error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s) {
+  if (fast2d_) {
+    Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
+    A.in_fine0 = r0;
+    A.in_fine1 = r1;
+    launch_slab2d_fwd(A, state_, s);
+    launch_slab2d_back(A, partials_, state_, history_, true, s);
+    const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
+    skeleton(sol, nullptr, coins_ + 4 * k, out, s);
+    fill(out, nullptr, s);
+    return;
+  }
   for (int a = 0; a < mesh_.dim; ++a) {
     launch_gather(r0, r1, rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
     sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
               scratch1_, s);
   }
   for (int a = 0; a < mesh_.dim; ++a) {
-    launch_norm_sq(sol_slab_[a], g_slab_[a].size, partials_, state_, s);
     CtrlArgs c{};
     c.op = kCtrlSlabNorm;
     c.which = a;
-    launch_ctrl(c, partials_, state_, history_, s);
+    launch_norm_sq(sol_slab_[a], g_slab_[a].size, partials_, state_, s, &c, history_);
   }
   for (int a = 0; a < mesh_.dim; ++a) launch_divide(sol_slab_[a], g_slab_[a].size, &state_->slab_norm[a], state_, s);
   const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
@@ -351,22 +408,19 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   c.tol = o.tol;
 
   smooth_guess(u_[0], s);
-  launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1],
-                 has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s);
   c.op = kCtrlResidualK0;
   c.k = 0;
-  launch_ctrl(c, partials_, state_, history_, s);
+  launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1],
+                 has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s, &c, history_);
 
   for (int k = 1; k <= o.max_iter; ++k) {
     error_mode_guess(r_[0], r_[1], k, e_, s);
-    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s);
     c.op = kCtrlStep;
     c.k = k;
-    launch_ctrl(c, partials_, state_, history_, s);
-    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1],
-                   has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s);
+    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s, &c, history_);
     c.op = kCtrlAccept;
-    launch_ctrl(c, partials_, state_, history_, s);
+    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1],
+                   has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s, &c, history_);
   }
 }
 
@@ -429,14 +483,13 @@ void Solver::error_guess(const double* r, std::uint64_t seed, double* e, cudaStr
 
 double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s) {
   launch_state_init(state_, 1, 1, s);
-  launch_ae_dots(mesh_.dim, e, r, r, fg_, st_fine_, partials_, state_, s);
-  CtrlArgs c{};
-  c.op = kCtrlStep;
   if (history_cap_ < 1) {
     history_ = dev_.alloc<double>(7);
     history_cap_ = 1;
   }
-  launch_ctrl(c, partials_, state_, history_, s);
+  CtrlArgs c{};
+  c.op = kCtrlStep;
+  launch_ae_dots(mesh_.dim, e, r, r, fg_, st_fine_, partials_, state_, s, &c, history_);
   DevState back{};
   ASDSM_CUDA_CHECK(cudaMemcpyAsync(&back, state_, sizeof(back), cudaMemcpyDeviceToHost, s));
   ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -482,8 +535,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   auto set_step = [&]() {
     CtrlArgs c{};
     c.op = kCtrlStep;
-    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s);
-    launch_ctrl(c, partials_, state_, history_, s);
+    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s, &c, history_);
   };
   const double ex = has_exact_ ? 1.0 : 0.0;
   timed("update_residual", 8.0 * N * (5.0 + ex), 0.0, iters, [&] {
@@ -519,6 +571,14 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   i64 slab_pts = 0;
   for (int a = 0; a < mesh_.dim; ++a) slab_pts += g_slab_[a].size;
   timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
+    if (fast2d_) {
+      Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
+      A.in_fine0 = r_[0];
+      A.in_fine1 = r_[1];
+      launch_slab2d_fwd(A, state_, s);
+      launch_slab2d_back(A, partials_, state_, history_, true, s);
+      return;
+    }
     for (int a = 0; a < mesh_.dim; ++a) {
       launch_gather(r_[0], r_[1], rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
       sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,

@@ -107,6 +107,8 @@ class Solver {
   double* spl_m1_ = nullptr;
   double* spl_m2_ = nullptr;
   Merge3DArgs m3_{};
+  bool fast2d_ = false;          // fused 2D slab/skeleton/hole path
+  double* slab_modes_[2] = {nullptr, nullptr};
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
   double* partials_ = nullptr;
