@@ -14,7 +14,7 @@ __device__ __forceinline__ double ctrl_warp_sum(double v) {
 // Fixed-shape reduction of the kRedBlocks partials of one slot.
 __device__ inline double ctrl_reduce(const double* part, bool is_max) {
   __shared__ double sh[kRedThreads];
-  double v = is_max ? 0.0 : 0.0;
+  double v = 0.0;
   for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v = is_max ? fmax(v, __ldcg(part + i)) : v + __ldcg(part + i);
   sh[threadIdx.x] = v;
   __syncthreads();
@@ -25,6 +25,51 @@ __device__ inline double ctrl_reduce(const double* part, bool is_max) {
   const double r = sh[0];
   __syncthreads();
   return r;
+}
+
+// All four slots (sum, max, sum, max) in one pass: fixed per-thread order, then a fixed
+// warp-shuffle tree and one shared-memory round.
+__device__ inline void ctrl_reduce4(const double* part, double& s0, double& m1, double& s2, double& m3) {
+  __shared__ double sh[4][32];
+  double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+    a += __ldcg(part + i);
+    b = fmax(b, __ldcg(part + kRedBlocks + i));
+    c += __ldcg(part + 2 * kRedBlocks + i);
+    d = fmax(d, __ldcg(part + 3 * kRedBlocks + i));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b = fmax(b, __shfl_down_sync(0xffffffffu, b, o));
+    c += __shfl_down_sync(0xffffffffu, c, o);
+    d = fmax(d, __shfl_down_sync(0xffffffffu, d, o));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    sh[0][w] = a;
+    sh[1][w] = b;
+    sh[2][w] = c;
+    sh[3][w] = d;
+  }
+  __syncthreads();
+  if (w == 0) {
+    a = lane < nw ? sh[0][lane] : 0.0;
+    b = lane < nw ? sh[1][lane] : 0.0;
+    c = lane < nw ? sh[2][lane] : 0.0;
+    d = lane < nw ? sh[3][lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b = fmax(b, __shfl_down_sync(0xffffffffu, b, o));
+      c += __shfl_down_sync(0xffffffffu, c, o);
+      d = fmax(d, __shfl_down_sync(0xffffffffu, d, o));
+    }
+  }
+  s0 = a;
+  m1 = b;
+  s2 = c;
+  m3 = d;
 }
 
 // Control logic of one reduction (thread 0 of the reducing block).
@@ -148,10 +193,8 @@ __device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
-  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
-  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
-  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
+  double s0, m1, s2, m3;
+  ctrl_reduce4(partials, s0, m1, s2, m3);
   if (threadIdx.x == 0) {
     ctrl_apply(c, s0, m1, s2, m3, S, history);
     S->red_counter = 0;

@@ -56,35 +56,82 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
   __syncthreads();
   const int k = blockIdx.y * KB + threadIdx.x;
   if (k >= m0) return;
-  // full transforms of the first and last rows
+  // full transforms of the first and last rows (8 independent loads in flight per step)
   double fb = 0.0, ft = 0.0;
-  for (int i = 0; i < m0; ++i) {
-    const double w = A.Wt[static_cast<i64>(i) * m0 + k];
-    fb = fma(w, fB[i], fb);
-    ft = fma(w, fT[i], ft);
+  {
+    int i = 0;
+    for (; i + 8 <= m0; i += 8) {
+      double w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = __ldg(A.Wt + static_cast<i64>(i + q) * m0 + k);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        fb = fma(w[q], fB[i + q], fb);
+        ft = fma(w[q], fT[i + q], ft);
+      }
+    }
+    for (; i < m0; ++i) {
+      const double w = __ldg(A.Wt + static_cast<i64>(i) * m0 + k);
+      fb = fma(w, fB[i], fb);
+      ft = fma(w, fT[i], ft);
+    }
   }
-  const double w0 = A.Wt[k], wm = A.Wt[static_cast<i64>(m0 - 1) * m0 + k];
+  const double w0 = __ldg(A.Wt + k), wm = __ldg(A.Wt + static_cast<i64>(m0 - 1) * m0 + k);
   const double l = A.line_left;
-  // forward sweep; y is parked in the mode buffer and overwritten by the backward sweep
   double* out = modes + static_cast<i64>(hole) * m0 * m1;
+  // forward sweep, pivots prefetched 8 rows ahead; y parked in smem or the mode buffer
   double y = 0.0;
-  for (int j = 0; j < m1; ++j) {
-    double f;
-    if (j == 0) f = fb;
-    else if (j == m1 - 1) f = ft;
-    else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
-    const double iv = __ldg(ipiv + static_cast<i64>(j) * m0 + k);
-    y = (j == 0) ? f * iv : (f - l * y) * iv;
-    if (A.y_in_smem) ys[j * KB + threadIdx.x] = y;
-    else out[static_cast<i64>(j) * m0 + k] = y;
+  constexpr int U = 8;
+  double ivn[U];
+#pragma unroll
+  for (int q = 0; q < U; ++q) ivn[q] = q < m1 ? __ldg(ipiv + static_cast<i64>(q) * m0 + k) : 0.0;
+  for (int j0 = 0; j0 < m1; j0 += U) {
+    double iv[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      iv[q] = ivn[q];
+      const int jn = j0 + U + q;
+      ivn[q] = jn < m1 ? __ldg(ipiv + static_cast<i64>(jn) * m0 + k) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int j = j0 + q;
+      if (j >= m1) break;
+      double f;
+      if (j == 0) f = fb;
+      else if (j == m1 - 1) f = ft;
+      else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
+      y = (j == 0) ? f * iv[q] : (f - l * y) * iv[q];
+      if (A.y_in_smem) ys[j * KB + threadIdx.x] = y;
+      else out[static_cast<i64>(j) * m0 + k] = y;
+    }
   }
   // backward sweep, mode layout [hole][j][k]
   double x = y;
   out[static_cast<i64>(m1 - 1) * m0 + k] = x;
-  for (int j = m1 - 2; j >= 0; --j) {
-    const double yj = A.y_in_smem ? ys[j * KB + threadIdx.x] : out[static_cast<i64>(j) * m0 + k];
-    x = yj - __ldg(cpv + static_cast<i64>(j) * m0 + k) * x;
-    out[static_cast<i64>(j) * m0 + k] = x;
+  double cpn[U];
+#pragma unroll
+  for (int q = 0; q < U; ++q) {
+    const int j = m1 - 2 - q;
+    cpn[q] = j >= 0 ? __ldg(cpv + static_cast<i64>(j) * m0 + k) : 0.0;
+  }
+  for (int j0 = m1 - 2; j0 >= 0; j0 -= U) {
+    double cpj[U], yv[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      cpj[q] = cpn[q];
+      const int jn = j0 - U - q;
+      cpn[q] = jn >= 0 ? __ldg(cpv + static_cast<i64>(jn) * m0 + k) : 0.0;
+      const int j = j0 - q;
+      yv[q] = j >= 0 ? (A.y_in_smem ? ys[j * KB + threadIdx.x] : out[static_cast<i64>(j) * m0 + k]) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int j = j0 - q;
+      if (j < 0) break;
+      x = yv[q] - cpj[q] * x;
+      out[static_cast<i64>(j) * m0 + k] = x;
+    }
   }
 }
 

@@ -7,6 +7,8 @@
 #include "slab2d.cuh"
 #include "ctrl.cuh"
 
+#include <type_traits>
+
 namespace asdsm_b200 {
 
 namespace {
@@ -51,24 +53,66 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
   const int L = A.levels[a];
   const double* K1 = A.k1[a];
   const double* K2 = A.k2[a];
+  if constexpr (std::is_same<T, cplx>::value) {  // complex: coefficients straight from L2
+    int s = 1;
+    for (int lev = 0; lev < L; ++lev, s <<= 1) {
+      const i64 base = (static_cast<i64>(k) * L + lev) * nf;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        T v = x0[i];
+        if (i - s >= 0) v = v - ld<T>(K1, base + i) * x0[i - s];
+        if (i + s < nf) v = v - ld<T>(K2, base + i) * x0[i + s];
+        x1[i] = v;
+      }
+      __syncthreads();
+      T* t = x0;
+      x0 = x1;
+      x1 = t;
+    }
+    for (int i = threadIdx.x; i < nf; i += blockDim.x)
+      st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
+    return;
+  }
+  constexpr int E = 6;  // elements per thread (line length <= 6144)
+  T c1[E], c2[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = threadIdx.x + e * kThreads;
+    const i64 base = static_cast<i64>(k) * L * nf;
+    c1[e] = (i < nf && L > 0) ? ld<T>(K1, base + i) : zero_of<T>();
+    c2[e] = (i < nf && L > 0) ? ld<T>(K2, base + i) : zero_of<T>();
+  }
   int s = 1;
   for (int lev = 0; lev < L; ++lev, s <<= 1) {
-    const i64 base = (static_cast<i64>(k) * L + lev) * nf;
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+    T n1[E], n2[E];
+    const i64 nbase = (static_cast<i64>(k) * L + lev + 1) * nf;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {  // prefetch the next level while this one computes
+      const int i = threadIdx.x + e * kThreads;
+      n1[e] = (i < nf && lev + 1 < L) ? ld<T>(K1, nbase + i) : zero_of<T>();
+      n2[e] = (i < nf && lev + 1 < L) ? ld<T>(K2, nbase + i) : zero_of<T>();
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = threadIdx.x + e * kThreads;
+      if (i >= nf) break;
       T v = x0[i];
-      if (i - s >= 0) v = v - ld<T>(K1, base + i) * x0[i - s];
-      if (i + s < nf) v = v - ld<T>(K2, base + i) * x0[i + s];
+      if (i - s >= 0) v = v - c1[e] * x0[i - s];
+      if (i + s < nf) v = v - c2[e] * x0[i + s];
       x1[i] = v;
     }
     __syncthreads();
     T* t = x0;
     x0 = x1;
     x1 = t;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      c1[e] = n1[e];
+      c2[e] = n2[e];
+    }
   }
   for (int i = threadIdx.x; i < nf; i += blockDim.x)
     st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
 }
-
 
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, double* partials, DevState* S,
@@ -132,6 +176,7 @@ void launch_slab2d_fwd(const Slab2DArgs& A, DevState* st, cudaStream_t s) {
   const int ncmax = std::max(A.m.nc[0], A.m.nc[1]);
   const int nfmax = std::max(A.m.nf[0], A.m.nf[1]);
   const size_t smem = 2 * static_cast<size_t>(nfmax) * (A.cplx ? sizeof(cplx) : sizeof(double));
+  if (!A.cplx && nfmax > 6 * kThreads) throw AsdsmError(kUnsupported, "2D slab line longer than 6144");
   if (smem > kMaxSmem) throw AsdsmError(kUnsupported, "2D slab line longer than shared memory allows");
   dim3 grid(static_cast<unsigned>(ncmax), 2);
   if (A.cplx) slab2d_fwd_kernel<cplx><<<grid, kThreads, smem, s>>>(A, st);
