@@ -12,10 +12,10 @@ __device__ __forceinline__ double ctrl_warp_sum(double v) {
 }
 
 // Fixed-shape reduction of the kRedBlocks partials of one slot.
-__device__ inline double ctrl_reduce(const double* part, bool is_max) {
+__device__ inline double ctrl_reduce(const double* part, bool is_max, int nblocks = kRedBlocks) {
   __shared__ double sh[kRedThreads];
   double v = 0.0;
-  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) v = is_max ? fmax(v, __ldcg(part + i)) : v + __ldcg(part + i);
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) v = is_max ? fmax(v, __ldcg(part + i)) : v + __ldcg(part + i);
   sh[threadIdx.x] = v;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -29,14 +29,14 @@ __device__ inline double ctrl_reduce(const double* part, bool is_max) {
 
 // All four slots (sum, max, sum, max) in one pass: fixed per-thread order, then a fixed
 // warp-shuffle tree and one shared-memory round.
-__device__ inline void ctrl_reduce4(const double* part, double& s0, double& m1, double& s2, double& m3) {
+__device__ inline void ctrl_reduce4(const double* part, int nblocks, double& s0, double& m1, double& s2, double& m3) {
   __shared__ double sh[4][32];
   double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
-  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
     a += __ldcg(part + i);
-    b = fmax(b, __ldcg(part + kRedBlocks + i));
-    c += __ldcg(part + 2 * kRedBlocks + i);
-    d = fmax(d, __ldcg(part + 3 * kRedBlocks + i));
+    b = fmax(b, __ldcg(part + kRedStride + i));
+    c += __ldcg(part + 2 * kRedStride + i);
+    d = fmax(d, __ldcg(part + 3 * kRedStride + i));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -170,12 +170,52 @@ __device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, doubl
 static __global__ void __launch_bounds__(kRedThreads) ctrl_kernel(CtrlArgs c, const double* partials, DevState* S,
                                                           double* history) {
   if (!S->active) return;
-  const double s0 = ctrl_reduce(partials + 0 * kRedBlocks, false);
-  const double m1 = ctrl_reduce(partials + 1 * kRedBlocks, true);
-  const double s2 = ctrl_reduce(partials + 2 * kRedBlocks, false);
-  const double m3 = ctrl_reduce(partials + 3 * kRedBlocks, true);
+  const double s0 = ctrl_reduce(partials + 0 * kRedStride, false);
+  const double m1 = ctrl_reduce(partials + 1 * kRedStride, true);
+  const double s2 = ctrl_reduce(partials + 2 * kRedStride, false);
+  const double m3 = ctrl_reduce(partials + 3 * kRedStride, true);
   if (threadIdx.x != 0) return;
   ctrl_apply(c, s0, m1, s2, m3, S, history);
+}
+
+// Block partials of (sum, max, sum, max) for any 1D grid: partials[slot*kRedStride + block].
+__device__ inline void block_reduce4_march(double s0, double m1, double s2, double m3, double* partials) {
+  __shared__ double sh[4][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, o);
+    m1 = fmax(m1, __shfl_down_sync(0xffffffffu, m1, o));
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    m3 = fmax(m3, __shfl_down_sync(0xffffffffu, m3, o));
+  }
+  if (lane == 0) {
+    sh[0][w] = s0;
+    sh[1][w] = m1;
+    sh[2][w] = s2;
+    sh[3][w] = m3;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    s0 = lane < nw ? sh[0][lane] : 0.0;
+    m1 = lane < nw ? sh[1][lane] : 0.0;
+    s2 = lane < nw ? sh[2][lane] : 0.0;
+    m3 = lane < nw ? sh[3][lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_down_sync(0xffffffffu, s0, o);
+      m1 = fmax(m1, __shfl_down_sync(0xffffffffu, m1, o));
+      s2 += __shfl_down_sync(0xffffffffu, s2, o);
+      m3 = fmax(m3, __shfl_down_sync(0xffffffffu, m3, o));
+    }
+    if (lane == 0) {
+      partials[0 * kRedStride + blockIdx.x] = s0;
+      partials[1 * kRedStride + blockIdx.x] = m1;
+      partials[2 * kRedStride + blockIdx.x] = s2;
+      partials[3 * kRedStride + blockIdx.x] = m3;
+    }
+  }
 }
 
 // Last-block fold: after every block has written its partials, the last block to finish
@@ -184,18 +224,19 @@ static __global__ void __launch_bounds__(kRedThreads) ctrl_kernel(CtrlArgs c, co
 __device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history) {
   if (c.op < 0) return;
   __shared__ int last;
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
     __threadfence();
     const unsigned t = atomicAdd(&S->red_counter, 1u);
-    last = (t == gridDim.x - 1);
+    last = (t == nblocks - 1);
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   double s0, m1, s2, m3;
-  ctrl_reduce4(partials, s0, m1, s2, m3);
-  if (threadIdx.x == 0) {
+  ctrl_reduce4(partials, static_cast<int>(nblocks), s0, m1, s2, m3);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
     ctrl_apply(c, s0, m1, s2, m3, S, history);
     S->red_counter = 0;
     __threadfence();

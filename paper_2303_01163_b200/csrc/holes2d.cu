@@ -152,6 +152,9 @@ void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& 
 }
 
 void hole2d_prepare(size_t smem) {
+  static bool done = false;
+  if (done) return;
+  done = true;
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
 }

@@ -59,10 +59,10 @@ __device__ void block_reduce4(double s0, double m1, double s2, double m3, double
     s2 = warp_sum(s2);
     m3 = warp_max(m3);
     if (lane == 0) {
-      partials[0 * kRedBlocks + blockIdx.x] = s0;
-      partials[1 * kRedBlocks + blockIdx.x] = m1;
-      partials[2 * kRedBlocks + blockIdx.x] = s2;
-      partials[3 * kRedBlocks + blockIdx.x] = m3;
+      partials[0 * kRedStride + blockIdx.x] = s0;
+      partials[1 * kRedStride + blockIdx.x] = m1;
+      partials[2 * kRedStride + blockIdx.x] = s2;
+      partials[3 * kRedStride + blockIdx.x] = m3;
     }
   }
 }

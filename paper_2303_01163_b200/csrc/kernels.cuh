@@ -5,6 +5,7 @@
 namespace asdsm_b200 {
 
 constexpr int kRedBlocks = 4 * kNumSms;  // fixed grid => deterministic reduction order
+constexpr int kRedStride = 65536;         // partials[slot * kRedStride + block], blocks <= kRedStride
 constexpr int kRedThreads = 256;
 
 // Device-resident iteration state (the reference's IterationState scalars,

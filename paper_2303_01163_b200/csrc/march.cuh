@@ -1,0 +1,31 @@
+#pragma once
+#include "kernels.cuh"
+
+namespace asdsm_b200 {
+
+enum { kMarchResidual = 0, kMarchUpdate = 1, kMarchDots = 2 };
+
+struct MarchArgs {
+  const double* u0;  // current iterate buffers (state->cur selects); DOTS: unused
+  const double* u1;
+  const double* e;   // correction (UPDATE, DOTS)
+  const double* b;
+  double* uo0;       // UPDATE outputs go to the non-current buffers
+  double* uo1;
+  double* ro0;       // residual buffers (RESIDUAL writes the current one; DOTS reads it)
+  double* ro1;
+  const double* r0;
+  const double* r1;
+  const double* exact;
+  FineGeom g;
+  Stencil st;
+  double* partials;
+  DevState* state;
+  CtrlArgs ctrl;
+  double* history;
+};
+
+unsigned march_blocks(const FineGeom& g);
+void launch_march(int mode, const MarchArgs& A, cudaStream_t s);
+
+}  // namespace asdsm_b200

@@ -154,8 +154,8 @@ __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, 
       double v = lane < nw ? sh[q][lane] : 0.0;
       for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
       if (lane == 0) {
-        partials[(2 * q) * kRedBlocks + blockIdx.x] = v;
-        partials[(2 * q + 1) * kRedBlocks + blockIdx.x] = 0.0;
+        partials[(2 * q) * kRedStride + blockIdx.x] = v;
+        partials[(2 * q + 1) * kRedStride + blockIdx.x] = 0.0;
       }
     }
   }

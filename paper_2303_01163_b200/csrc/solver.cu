@@ -7,6 +7,7 @@
 #include "dmma_gemm.cuh"
 #include "holes2d.cuh"
 #include "slab2d.cuh"
+#include "march.cuh"
 
 #include <cmath>
 #include <cstdlib>
@@ -118,7 +119,7 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
       m3_.corrected[a] = dev_.alloc<double>(static_cast<size_t>(g_slab_[a].size));
     }
   }
-  partials_ = dev_.alloc<double>(4 * kRedBlocks);
+  partials_ = dev_.alloc<double>(4 * static_cast<size_t>(kRedStride));
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
   if (m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
@@ -226,8 +227,9 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nf1 = mesh_.nf[1];
     A.nbox0 = mesh_.nc[0] + 1;
     A.nbox1 = mesh_.nc[1] + 1;
-    A.kb = 32;
-    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
+    A.kb = 64;
+    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 100 * 1024 ? 1 : 0;
+    hole2d_prepare(100 * 1024);
     A.st = st_fine_;
     A.Wt = H.Wt[0];
     A.ipiv = H.th_ipiv;
@@ -254,6 +256,31 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
   launch_hole_rhs(mesh_.dim, e, b, fg_, st_fine_, md_, state_, s);
   const BoxArray h = hole_array(e);
   sep_solve(sep_hole_, h, h, scratch0_, scratch1_, s);
+}
+
+static MarchArgs march_args(const double* u0, const double* u1, const double* e, const double* b, double* uo0,
+                            double* uo1, double* ro0, double* ro1, const double* exact, const FineGeom& g,
+                            const Stencil& st, double* partials, DevState* state, const CtrlArgs& c,
+                            double* history) {
+  MarchArgs A{};
+  A.u0 = u0;
+  A.u1 = u1;
+  A.e = e;
+  A.b = b;
+  A.uo0 = uo0;
+  A.uo1 = uo1;
+  A.ro0 = ro0;
+  A.ro1 = ro1;
+  A.r0 = ro0;
+  A.r1 = ro1;
+  A.exact = exact;
+  A.g = g;
+  A.st = st;
+  A.partials = partials;
+  A.state = state;
+  A.ctrl = c;
+  A.history = history;
+  return A;
 }
 
 static Slab2DArgs slab2d_args(const MeshDev& md, const SepSolver* S, double* const* modes, double* const* sol) {
@@ -410,17 +437,19 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   smooth_guess(u_[0], s);
   c.op = kCtrlResidualK0;
   c.k = 0;
-  launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1],
-                 has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s, &c, history_);
+  const double* ex = has_exact_ ? exact_ : nullptr;
+  launch_march(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], ex, fg_, st_fine_,
+                                          partials_, state_, c, history_), s);
 
   for (int k = 1; k <= o.max_iter; ++k) {
     error_mode_guess(r_[0], r_[1], k, e_, s);
     c.op = kCtrlStep;
     c.k = k;
-    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s, &c, history_);
+    launch_march(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+                                        st_fine_, partials_, state_, c, history_), s);
     c.op = kCtrlAccept;
-    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1],
-                   has_exact_ ? exact_ : nullptr, fg_, st_fine_, partials_, state_, s, &c, history_);
+    launch_march(kMarchUpdate, march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_,
+                                          partials_, state_, c, history_), s);
   }
 }
 
@@ -452,7 +481,10 @@ const double* Solver::r_current(cudaStream_t s) const {
 
 void Solver::residual(const double* u, const double* b, double* r, cudaStream_t s) {
   launch_state_init(state_, 1, 1, s);
-  launch_stencil(mesh_.dim, false, u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_, state_, s);
+  CtrlArgs c{};
+  c.op = -1;
+  launch_march(kMarchResidual, march_args(u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_,
+                                          state_, c, nullptr), s);
 }
 
 void Solver::error_guess(const double* r, std::uint64_t seed, double* e, cudaStream_t s) {
@@ -489,7 +521,8 @@ double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s)
   }
   CtrlArgs c{};
   c.op = kCtrlStep;
-  launch_ae_dots(mesh_.dim, e, r, r, fg_, st_fine_, partials_, state_, s, &c, history_);
+  launch_march(kMarchDots, march_args(nullptr, nullptr, e, nullptr, nullptr, nullptr, const_cast<double*>(r),
+                                      const_cast<double*>(r), nullptr, fg_, st_fine_, partials_, state_, c, history_), s);
   DevState back{};
   ASDSM_CUDA_CHECK(cudaMemcpyAsync(&back, state_, sizeof(back), cudaMemcpyDeviceToHost, s));
   ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -535,14 +568,17 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   auto set_step = [&]() {
     CtrlArgs c{};
     c.op = kCtrlStep;
-    launch_ae_dots(mesh_.dim, e_, r_[0], r_[1], fg_, st_fine_, partials_, state_, s, &c, history_);
+    launch_march(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+                                        st_fine_, partials_, state_, c, history_), s);
   };
   const double ex = has_exact_ ? 1.0 : 0.0;
   timed("update_residual", 8.0 * N * (5.0 + ex), 0.0, iters, [&] {
     launch_state_init(state_, 1, 1, s);
     set_step();
-    launch_stencil(mesh_.dim, true, u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr, fg_,
-                   st_fine_, partials_, state_, s);
+    CtrlArgs c{};
+    c.op = -1;
+    launch_march(kMarchUpdate, march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr,
+                                          fg_, st_fine_, partials_, state_, c, history_), s);
   });
   // the stencil-only time is what we want: subtract the set_step part measured alone
   timed("step_dots", 8.0 * N * 2.0, 0.0, iters, [&] { set_step(); });
@@ -590,8 +626,10 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     skeleton(sol, nullptr, coins_, e_, s);
   });
   timed("residual", 8.0 * N * 3.0, 0.0, 1, [&] {
-    launch_stencil(mesh_.dim, false, u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
-                   partials_, state_, s);
+    CtrlArgs c{};
+    c.op = -1;
+    launch_march(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+                                            st_fine_, partials_, state_, c, history_), s);
   });
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
