@@ -15,8 +15,8 @@ namespace asdsm_b200 {
 
 namespace {
 
-constexpr int TX2 = 128, SY2 = 32;            // 2D: threads per x-tile, rows per strip
-constexpr int TX3 = 32, TY3 = 16, SZ3 = 16;   // 3D: x-by-y tile, z chunk
+constexpr int TX2 = 128;                      // 2D: threads per x-tile (rows per strip: MarchArgs::strip)
+constexpr int TX3 = 32, TY3 = 16;             // 3D: x-by-y tile (z chunk: MarchArgs::strip)
 
 template <int MODE>
 struct Src {
@@ -45,29 +45,54 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
   const int Nx = A.g.ext[0], Ny = A.g.ext[1];
   const i64 sy = A.g.stride[1];
   const Stencil& st = A.st;
-  Src<MODE> V{cur ? A.u1 : A.u0, A.e, s};
+  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  const double* __restrict__ ee = A.e;
+  Src<MODE> V{uu, ee, s};
   const double* __restrict__ rcur = cur ? A.r1 : A.r0;
   double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
   double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
   __shared__ double row[2][TX2 + 2];
+  const int SY = A.strip;
   const int ntx = (Nx + TX2 - 1) / TX2;
   const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-  const int x0 = tx * TX2, y0 = ty * SY2;
-  const int y1 = min(y0 + SY2, Ny);
+  const int x0 = tx * TX2, y0 = ty * SY;
+  const int y1 = min(y0 + SY, Ny);
   const int t = threadIdx.x;
   const int x = x0 + t;
   const bool in = x < Nx;
+  const bool hl = t == 0 && x0 > 0;                        // loads the left halo
+  const bool hr = (t == TX2 - 1 || x == Nx - 1) && x + 1 < Nx;  // loads the right halo
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // ssq/num, max, esq/den, emax
   if (work) {
+    // register pipeline: vd (y-1), vc (y), vu (y+1); raw loads of row y+2 and of the next
+    // halos / b / r are issued one row ahead so their latency overlaps the current row
     double vd = (in && y0 > 0) ? V(x + (y0 - 1) * sy) : 0.0;
     double vc = in ? V(x + y0 * sy) : 0.0;
+    double vu = (in && y0 + 1 < Ny) ? V(x + (y0 + 1) * sy) : 0.0;
+    double hL = hl ? V(x0 - 1 + y0 * sy) : 0.0;
+    double hR = hr ? V(x + 1 + y0 * sy) : 0.0;
+    double bq = (in && MODE != kMarchDots) ? __ldg(A.b + x + y0 * sy) : 0.0;
+    double rq = (in && MODE == kMarchDots) ? __ldg(rcur + x + y0 * sy) : 0.0;
+    double xq = (in && A.exact && MODE != kMarchDots) ? __ldg(A.exact + x + y0 * sy) : 0.0;
     int buf = 0;
     for (int y = y0; y < y1; ++y) {
       const i64 p = x + y * sy;
-      const double vu = (in && y + 1 < Ny) ? V(p + sy) : 0.0;
+      // prefetch row y+2 (raw), next halos, next b / r / exact
+      double pu = 0.0, pe = 0.0, nL = 0.0, nR = 0.0, nb = 0.0, nr = 0.0, nx = 0.0;
+      if (in && y + 2 < Ny) {
+        pu = (MODE == kMarchDots) ? 0.0 : __ldg(uu + p + 2 * sy);
+        if (MODE != kMarchResidual) pe = __ldg(ee + p + 2 * sy);
+      }
+      if (y + 1 < y1) {
+        if (hl) nL = V(x0 - 1 + (y + 1) * sy);
+        if (hr) nR = V(x + 1 + (y + 1) * sy);
+        if (in && MODE != kMarchDots) nb = __ldg(A.b + p + sy);
+        if (in && MODE == kMarchDots) nr = __ldg(rcur + p + sy);
+        if (in && A.exact && MODE != kMarchDots) nx = __ldg(A.exact + p + sy);
+      }
       row[buf][t + 1] = vc;
-      if (t == 0) row[buf][0] = x0 > 0 ? V(x0 - 1 + y * sy) : 0.0;
-      if (t == TX2 - 1 || x == Nx - 1) row[buf][t + 2] = x + 1 < Nx ? V(p + 1) : 0.0;
+      if (t == 0) row[buf][0] = hL;
+      if (t == TX2 - 1 || x == Nx - 1) row[buf][t + 2] = hR;
       __syncthreads();
       if (in) {
         double acc = 0.0;
@@ -77,17 +102,16 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
         if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], row[buf][t + 2]));
         if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], vu));
         if (MODE == kMarchDots) {
-          const double rp = __ldg(rcur + p);
-          a0 += rp * acc;
+          a0 += rq * acc;
           a2 += acc * acc;
         } else {
-          const double r = __dsub_rn(__ldg(A.b + p), acc);
+          const double r = __dsub_rn(bq, acc);
           ro[p] = r;
           if (MODE == kMarchUpdate) uo[p] = vc;
           a0 += r * r;
           a1 = fmax(a1, fabs(r));
           if (A.exact) {
-            const double d = vc - __ldg(A.exact + p);
+            const double d = vc - xq;
             a2 += d * d;
             a3 = fmax(a3, fabs(d));
           }
@@ -95,6 +119,14 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
       }
       vd = vc;
       vc = vu;
+      if (MODE == kMarchUpdate) vu = __dadd_rn(pu, __dmul_rn(s, pe));
+      else if (MODE == kMarchDots) vu = pe;
+      else vu = pu;
+      hL = nL;
+      hR = nR;
+      bq = nb;
+      rq = nr;
+      xq = nx;
       buf ^= 1;
     }
   }
@@ -117,38 +149,65 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
   const i64 sy = A.g.stride[1], sz = A.g.stride[2];
   const Stencil& st = A.st;
-  Src<MODE> V{cur ? A.u1 : A.u0, A.e, s};
+  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  const double* __restrict__ ee = A.e;
+  Src<MODE> V{uu, ee, s};
   const double* __restrict__ rcur = cur ? A.r1 : A.r0;
   double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
   double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
   __shared__ double pl[2][TY3 + 2][TX3 + 2];
+  const int SZ = A.strip;
   const int ntx = (Nx + TX3 - 1) / TX3, nty = (Ny + TY3 - 1) / TY3;
   int b = blockIdx.x;
   const int bx = b % ntx;
   b /= ntx;
   const int by = b % nty;
   const int bz = b / nty;
-  const int x0 = bx * TX3, y0 = by * TY3, z0 = bz * SZ3;
-  const int z1 = min(z0 + SZ3, Nz);
+  const int x0 = bx * TX3, y0 = by * TY3, z0 = bz * SZ;
+  const int z1 = min(z0 + SZ, Nz);
   const int tx = threadIdx.x % TX3, ty = threadIdx.x / TX3;
   const int x = x0 + tx, y = y0 + ty;
   const bool in = x < Nx && y < Ny;
+  // halo roles (each edge thread owns at most one x- and one y-halo cell)
+  const bool hxl = in && tx == 0 && x > 0;
+  const bool hxr = in && (tx == TX3 - 1 || x == Nx - 1) && x + 1 < Nx;
+  const bool hyl = in && ty == 0 && y > 0;
+  const bool hyr = in && (ty == TY3 - 1 || y == Ny - 1) && y + 1 < Ny;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (work) {
     const i64 pxy = x + y * sy;
     double vd = (in && z0 > 0) ? V(pxy + (z0 - 1) * sz) : 0.0;
     double vc = in ? V(pxy + z0 * sz) : 0.0;
+    double vu = (in && z0 + 1 < Nz) ? V(pxy + (z0 + 1) * sz) : 0.0;
+    const i64 p0 = pxy + z0 * sz;
+    double hXL = hxl ? V(p0 - 1) : 0.0, hXR = hxr ? V(p0 + 1) : 0.0;
+    double hYL = hyl ? V(p0 - sy) : 0.0, hYR = hyr ? V(p0 + sy) : 0.0;
+    double bq = (in && MODE != kMarchDots) ? __ldg(A.b + p0) : 0.0;
+    double rq = (in && MODE == kMarchDots) ? __ldg(rcur + p0) : 0.0;
+    double xq = (in && A.exact && MODE != kMarchDots) ? __ldg(A.exact + p0) : 0.0;
     int buf = 0;
     for (int z = z0; z < z1; ++z) {
       const i64 p = pxy + z * sz;
-      const double vu = (in && z + 1 < Nz) ? V(p + sz) : 0.0;
-      pl[buf][ty + 1][tx + 1] = vc;
-      if (in) {
-        if (tx == 0) pl[buf][ty + 1][0] = x > 0 ? V(p - 1) : 0.0;
-        if (tx == TX3 - 1 || x == Nx - 1) pl[buf][ty + 1][tx + 2] = x + 1 < Nx ? V(p + 1) : 0.0;
-        if (ty == 0) pl[buf][0][tx + 1] = y > 0 ? V(p - sy) : 0.0;
-        if (ty == TY3 - 1 || y == Ny - 1) pl[buf][ty + 2][tx + 1] = y + 1 < Ny ? V(p + sy) : 0.0;
+      double pu = 0.0, pe = 0.0, nXL = 0.0, nXR = 0.0, nYL = 0.0, nYR = 0.0, nb = 0.0, nr = 0.0, nx = 0.0;
+      if (in && z + 2 < Nz) {
+        pu = (MODE == kMarchDots) ? 0.0 : __ldg(uu + p + 2 * sz);
+        if (MODE != kMarchResidual) pe = __ldg(ee + p + 2 * sz);
       }
+      if (z + 1 < z1) {
+        const i64 pn = p + sz;
+        if (hxl) nXL = V(pn - 1);
+        if (hxr) nXR = V(pn + 1);
+        if (hyl) nYL = V(pn - sy);
+        if (hyr) nYR = V(pn + sy);
+        if (in && MODE != kMarchDots) nb = __ldg(A.b + pn);
+        if (in && MODE == kMarchDots) nr = __ldg(rcur + pn);
+        if (in && A.exact && MODE != kMarchDots) nx = __ldg(A.exact + pn);
+      }
+      pl[buf][ty + 1][tx + 1] = vc;
+      if (tx == 0) pl[buf][ty + 1][0] = hXL;
+      if (tx == TX3 - 1 || x == Nx - 1) pl[buf][ty + 1][tx + 2] = hXR;
+      if (ty == 0) pl[buf][0][tx + 1] = hYL;
+      if (ty == TY3 - 1 || y == Ny - 1) pl[buf][ty + 2][tx + 1] = hYR;
       __syncthreads();
       if (in) {
         double acc = 0.0;
@@ -160,17 +219,16 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
         if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], pl[buf][ty + 2][tx + 1]));
         if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(st.right[2], vu));
         if (MODE == kMarchDots) {
-          const double rp = __ldg(rcur + p);
-          a0 += rp * acc;
+          a0 += rq * acc;
           a2 += acc * acc;
         } else {
-          const double r = __dsub_rn(__ldg(A.b + p), acc);
+          const double r = __dsub_rn(bq, acc);
           ro[p] = r;
           if (MODE == kMarchUpdate) uo[p] = vc;
           a0 += r * r;
           a1 = fmax(a1, fabs(r));
           if (A.exact) {
-            const double d = vc - __ldg(A.exact + p);
+            const double d = vc - xq;
             a2 += d * d;
             a3 = fmax(a3, fabs(d));
           }
@@ -178,6 +236,16 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
       }
       vd = vc;
       vc = vu;
+      if (MODE == kMarchUpdate) vu = __dadd_rn(pu, __dmul_rn(s, pe));
+      else if (MODE == kMarchDots) vu = pe;
+      else vu = pu;
+      hXL = nXL;
+      hXR = nXR;
+      hYL = nYL;
+      hYR = nYR;
+      bq = nb;
+      rq = nr;
+      xq = nx;
       buf ^= 1;
     }
   }
@@ -187,12 +255,34 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
 
 }  // namespace
 
-unsigned march_blocks(const FineGeom& g) {
-  if (g.dim == 2) return static_cast<unsigned>(((g.ext[0] + TX2 - 1) / TX2) * ((g.ext[1] + SY2 - 1) / SY2));
-  return static_cast<unsigned>(((g.ext[0] + TX3 - 1) / TX3) * ((g.ext[1] + TY3 - 1) / TY3) * ((g.ext[2] + SZ3 - 1) / SZ3));
+int march_strip(const FineGeom& g) {
+  // enough CTAs to cover 148 SMs several times, strips of 4..32 rows (planes in 3D)
+  if (g.dim == 3) {
+    const long long nt = ((g.ext[0] + TX3 - 1) / TX3) * ((g.ext[1] + TY3 - 1) / TY3);
+    long long sz = (static_cast<long long>(g.ext[2]) * nt) / (4LL * kNumSms);
+    if (sz < 4) sz = 4;
+    if (sz > 64) sz = 64;
+    return static_cast<int>(sz);
+  }
+  const long long ntx = (g.ext[0] + TX2 - 1) / TX2;
+  long long sy = (static_cast<long long>(g.ext[1]) * ntx) / (8LL * kNumSms);
+  if (sy < 4) sy = 4;
+  if (sy > 32) sy = 32;
+  return static_cast<int>(sy);
 }
 
-void launch_march(int mode, const MarchArgs& A, cudaStream_t s) {
+unsigned march_blocks(const FineGeom& g) {
+  if (g.dim == 2) {
+    const int sy = march_strip(g);
+    return static_cast<unsigned>(((g.ext[0] + TX2 - 1) / TX2) * ((g.ext[1] + sy - 1) / sy));
+  }
+  const int sz = march_strip(g);
+  return static_cast<unsigned>(((g.ext[0] + TX3 - 1) / TX3) * ((g.ext[1] + TY3 - 1) / TY3) * ((g.ext[2] + sz - 1) / sz));
+}
+
+void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
+  MarchArgs A = A0;
+  A.strip = march_strip(A.g);
   const unsigned nb = march_blocks(A.g);
   if (nb > static_cast<unsigned>(kRedStride)) throw AsdsmError(kUnsupported, "fine grid too large for the partial buffer");
   if (A.g.dim == 2) {

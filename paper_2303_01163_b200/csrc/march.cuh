@@ -23,8 +23,10 @@ struct MarchArgs {
   DevState* state;
   CtrlArgs ctrl;
   double* history;
+  int strip;  // 2D rows per CTA (set by launch_march)
 };
 
+int march_strip(const FineGeom& g);
 unsigned march_blocks(const FineGeom& g);
 void launch_march(int mode, const MarchArgs& A, cudaStream_t s);
 
