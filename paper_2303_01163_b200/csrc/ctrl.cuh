@@ -221,8 +221,8 @@ __device__ inline void block_reduce4_march(double s0, double m1, double s2, doub
 // Last-block fold: after every block has written its partials, the last block to finish
 // reduces them in a fixed order and applies the control op -- no separate ctrl launch.
 
-__device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history) {
-  if (c.op < 0) return;
+__device__ inline bool fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history) {
+  if (c.op < 0) return false;
   __shared__ int last;
   const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
   __syncthreads();
@@ -232,7 +232,7 @@ __device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* 
     last = (t == nblocks - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   double s0, m1, s2, m3;
   ctrl_reduce4(partials, static_cast<int>(nblocks), s0, m1, s2, m3);
@@ -241,6 +241,7 @@ __device__ inline void fold_ctrl(const CtrlArgs& c, double* partials, DevState* 
     S->red_counter = 0;
     __threadfence();
   }
+  return true;
 }
 
 

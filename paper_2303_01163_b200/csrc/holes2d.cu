@@ -135,18 +135,92 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
   }
 }
 
+// Same algorithm with every table slice this CTA needs (Wt[:, kblock], ipiv/cp[:, kblock])
+// bulk-loaded into shared memory up front: one coalesced, fully overlapped load phase, then
+// the transforms and both sweeps run out of shared memory (the kernel is latency bound:
+// ~2 warps per SM exist in total, so memory-level parallelism has to come from the bulk load).
+__global__ void hole2d_fwd_thomas_smem_kernel(const double* __restrict__ e, double* __restrict__ modes, Hole2DArgs A,
+                                              const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  extern __shared__ double sm[];
+  const int m0 = A.m0, m1 = A.m1, KB = blockDim.x;
+  double* fL = sm;
+  double* fR = fL + m1;
+  double* fB = fR + m1;
+  double* fT = fB + m0;
+  double* sW = fT + m0;          // [m0][KB]
+  double* sI = sW + m0 * KB;     // [m1][KB]
+  double* sC = sI + m1 * KB;     // [m1][KB]
+  double* ys = sC + m1 * KB;     // [m1][KB]
+  const int hole = blockIdx.x;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  const int ox = hx * A.n0, oy = hy * A.n1;
+  const int kbase = blockIdx.y * KB;
+  const int kcnt = min(KB, m0 - kbase);
+  for (int t = threadIdx.x; t < m0 * KB; t += KB) {
+    const int i = t / KB, kk = t % KB;
+    sW[t] = kk < kcnt ? __ldg(A.Wt + static_cast<i64>(i) * m0 + kbase + kk) : 0.0;
+  }
+  for (int t = threadIdx.x; t < m1 * KB; t += KB) {
+    const int j = t / KB, kk = t % KB;
+    sI[t] = kk < kcnt ? __ldg(A.ipiv + static_cast<i64>(j) * m0 + kbase + kk) : 0.0;
+    sC[t] = kk < kcnt ? __ldg(A.cp + static_cast<i64>(j) * m0 + kbase + kk) : 0.0;
+  }
+  for (int t = threadIdx.x; t < m1; t += KB) {
+    fL[t] = ring_rhs(e, A, ox, oy, 0, t);
+    fR[t] = ring_rhs(e, A, ox, oy, m0 - 1, t);
+  }
+  for (int t = threadIdx.x; t < m0; t += KB) {
+    fB[t] = ring_rhs(e, A, ox, oy, t, 0);
+    fT[t] = ring_rhs(e, A, ox, oy, t, m1 - 1);
+  }
+  __syncthreads();
+  const int kk = threadIdx.x;
+  const int k = kbase + kk;
+  if (kk >= kcnt) return;
+  double fb = 0.0, ft = 0.0;
+  for (int i = 0; i < m0; ++i) {
+    const double w = sW[i * KB + kk];
+    fb = fma(w, fB[i], fb);
+    ft = fma(w, fT[i], ft);
+  }
+  const double w0 = sW[kk], wm = sW[(m0 - 1) * KB + kk];
+  const double l = A.line_left;
+  double y = 0.0;
+  for (int j = 0; j < m1; ++j) {
+    double f;
+    if (j == 0) f = fb;
+    else if (j == m1 - 1) f = ft;
+    else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
+    const double iv = sI[j * KB + kk];
+    y = (j == 0) ? f * iv : (f - l * y) * iv;
+    ys[j * KB + kk] = y;
+  }
+  double* out = modes + static_cast<i64>(hole) * m0 * m1;
+  double x = y;
+  out[static_cast<i64>(m1 - 1) * m0 + k] = x;
+  for (int j = m1 - 2; j >= 0; --j) {
+    x = ys[j * KB + kk] - sC[j * KB + kk] * x;
+    out[static_cast<i64>(j) * m0 + k] = x;
+  }
+}
+
 }  // namespace
 
-size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem) {
+size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem) {
+  if (tables_in_smem)
+    return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0) +
+                             static_cast<size_t>(m0 + 3 * m1) * kb);
   return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0) +
                            (y_in_smem ? static_cast<size_t>(m1) * kb : 0));
 }
 
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s) {
   const int kb = A.kb;
-  const size_t smem = hole2d_smem_bytes(A.m0, A.m1, kb, A.y_in_smem);
+  const size_t smem = hole2d_smem_bytes(A.m0, A.m1, kb, A.y_in_smem, A.tables_in_smem);
   dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m0 + kb - 1) / kb));
-  hole2d_fwd_thomas_kernel<<<grid, kb, smem, s>>>(e, modes, A, state);
+  if (A.tables_in_smem) hole2d_fwd_thomas_smem_kernel<<<grid, kb, smem, s>>>(e, modes, A, state);
+  else hole2d_fwd_thomas_kernel<<<grid, kb, smem, s>>>(e, modes, A, state);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }
@@ -156,6 +230,8 @@ void hole2d_prepare(size_t smem) {
   if (done) return;
   done = true;
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
 }
 

@@ -15,9 +15,10 @@ struct Hole2DArgs {
   const double* cp;    // Thomas upper factors [j][k]
   double line_left;
   int y_in_smem;     // park the forward sweep in shared memory (else in the mode buffer)
+  int tables_in_smem;  // bulk-load this CTA's slices of Wt / ipiv / cp into shared memory first
 };
 
-size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem);
+size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem = false);
 void hole2d_prepare(size_t smem);
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);
 

@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "spline.cuh"
 #include "ctrl.cuh"
+#include "skel2d.cuh"
 
 namespace asdsm_b200 {
 
@@ -532,6 +533,102 @@ void launch_skeleton2d(const Skel2DArgs& a, DevState* state, cudaStream_t s) {
   skel2d_write_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(a, state);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
+}
+
+namespace {
+
+__global__ void skel2d_ccspline_fast_kernel(Skel2DArgs a, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  skel2d_ccspline_block(a);
+}
+
+// skeleton points from the precomputed segment coefficients (no divisions per point)
+__global__ void skel2d_write_fast_kernel(Skel2DArgs a, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const MeshDev& m = a.m;
+  const int nc0 = m.nc[0], nc1 = m.nc[1];
+  const double nfc = a.norm_fc ? *a.norm_fc : 1.0;
+  const double ncf = a.norm_cf ? *a.norm_cf : 1.0;
+  const i64 nrow_pts = static_cast<i64>(nc1) * m.nf[0];
+  const i64 ncol_pts = static_cast<i64>(nc0) * m.nf[1];
+  auto ut_cf = [&](int I, int j) {
+    double u = a.u_cf[I + static_cast<i64>(nc0) * j];
+    if (a.norm_cf) u = u / ncf;
+    return __dadd_rn(u, skel_seg_eval(a.sp_tab[1], a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1), nc1, m.n[1], m.h[1], j + 1));
+  };
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < nrow_pts + ncol_pts;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    if (t < nrow_pts) {
+      const int i = static_cast<int>(t % m.nf[0]);
+      const int J = static_cast<int>(t / m.nf[0]);
+      const int j = (J + 1) * m.n[1] - 1;
+      double ufc = a.u_fc[i + static_cast<i64>(m.nf[0]) * J];
+      if (a.norm_fc) ufc = ufc / nfc;
+      const double av = __dadd_rn(ufc, skel_seg_eval(a.sp_tab[0], a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1), nc0,
+                                                     m.n[0], m.h[0], i + 1));
+      double val = av;
+      if ((i + 1) % m.n[0] == 0) {
+        const double bv = ut_cf((i + 1) / m.n[0] - 1, j);
+        val = __dadd_rn(__dadd_rn(av, bv), -bv);
+      }
+      a.out[i + static_cast<i64>(m.nf[0]) * j] = val;
+    } else {
+      const i64 tc = t - nrow_pts;
+      const int j = static_cast<int>(tc % m.nf[1]);
+      const int I = static_cast<int>(tc / m.nf[1]);
+      if ((j + 1) % m.n[1] == 0) continue;
+      const int i = (I + 1) * m.n[0] - 1;
+      a.out[i + static_cast<i64>(m.nf[0]) * j] = ut_cf(I, j);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_skel2d_ccspline_fast(const Skel2DArgs& a, DevState* state, cudaStream_t s) {
+  skel2d_ccspline_fast_kernel<<<1, 256, 0, s>>>(a, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_skel2d_write_fast(const Skel2DArgs& a, DevState* state, cudaStream_t s) {
+  const i64 npts = static_cast<i64>(a.m.nc[1]) * a.m.nf[0] + static_cast<i64>(a.m.nc[0]) * a.m.nf[1];
+  const i64 nb = std::min<i64>((npts + 255) / 256, 4 * kNumSms);
+  skel2d_write_fast_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(a, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+// zero_clamped_spline + CubicSpline ctor (spline.cpp:9-37, 58-76): the knot-only terms, in
+// the reference's operation order (host compiled with -ffp-contract=off).
+std::vector<double> spline_axis_table(int nc, int n, double h) {
+  const int np = nc + 2, ni = nc;
+  std::vector<double> x(static_cast<size_t>(np));
+  x[0] = 0.0;
+  for (int c = 1; c <= nc; ++c) x[static_cast<size_t>(c)] = static_cast<double>(static_cast<long long>(c) * n) * h;
+  x[static_cast<size_t>(np - 1)] = 1.0;
+  std::vector<double> hl(static_cast<size_t>(ni)), hr(static_cast<size_t>(ni)), w(static_cast<size_t>(ni), 0.0),
+      dg(static_cast<size_t>(ni)), up(static_cast<size_t>(ni));
+  for (int i = 0; i < ni; ++i) {
+    hl[static_cast<size_t>(i)] = x[static_cast<size_t>(i + 1)] - x[static_cast<size_t>(i)];
+    hr[static_cast<size_t>(i)] = x[static_cast<size_t>(i + 2)] - x[static_cast<size_t>(i + 1)];
+    dg[static_cast<size_t>(i)] = (hl[static_cast<size_t>(i)] + hr[static_cast<size_t>(i)]) / 3.0;
+    up[static_cast<size_t>(i)] = hr[static_cast<size_t>(i)] / 6.0;
+  }
+  for (int i = 1; i < ni; ++i) {
+    const double lower = (x[static_cast<size_t>(i + 1)] - x[static_cast<size_t>(i)]) / 6.0;
+    const double wi = lower / dg[static_cast<size_t>(i - 1)];
+    w[static_cast<size_t>(i)] = wi;
+    dg[static_cast<size_t>(i)] -= wi * up[static_cast<size_t>(i - 1)];
+  }
+  std::vector<double> tab;
+  tab.insert(tab.end(), x.begin(), x.end());
+  tab.insert(tab.end(), hl.begin(), hl.end());
+  tab.insert(tab.end(), hr.begin(), hr.end());
+  tab.insert(tab.end(), w.begin(), w.end());
+  tab.insert(tab.end(), dg.begin(), dg.end());
+  tab.insert(tab.end(), up.begin(), up.end());
+  return tab;
 }
 
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,

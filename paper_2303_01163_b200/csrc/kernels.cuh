@@ -2,6 +2,8 @@
 #pragma once
 #include "plan.hpp"
 
+#include <vector>
+
 namespace asdsm_b200 {
 
 constexpr int kRedBlocks = 4 * kNumSms;  // fixed grid => deterministic reduction order
@@ -96,8 +98,19 @@ struct Skel2DArgs {
   double* out;          // fine array: skeleton points written
   const double* norm_fc;  // error mode: ||u_fc||_2 (values are divided by it, solver.cpp:79-84), else null
   const double* norm_cf;
+  // fast path (coarse counts <= 62): data-independent spline terms precomputed on the host
+  // per axis [x (nc+2) | hl | hr | w | diag | upper (nc each)], and per-line segment
+  // coefficients (y_c, c1, c2, c3) x (nc+1) written by the cc/spline phase.
+  const double* sp_tab[2];
+  double* seg1;  // nc1 lines along x
+  double* seg2;  // nc0 lines along y
 };
 void launch_skeleton2d(const Skel2DArgs& a, DevState* state, cudaStream_t s);
+// fast path pieces: cross values + spline segment coefficients (one CTA), skeleton write
+void launch_skel2d_ccspline_fast(const Skel2DArgs& a, DevState* state, cudaStream_t s);
+void launch_skel2d_write_fast(const Skel2DArgs& a, DevState* state, cudaStream_t s);
+// host: the data-independent spline terms of one axis (bitwise the reference's values)
+std::vector<double> spline_axis_table(int nc, int n, double h);
 
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
                      DevState* state, cudaStream_t s);

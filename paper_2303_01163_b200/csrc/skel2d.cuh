@@ -1,0 +1,89 @@
+// 2D skeleton fast path: cross values, corrections and spline segment coefficients
+// (solver.cpp:166-187 with CubicSpline, spline.cpp:9-56) computed by ONE block, using the
+// data-independent spline terms precomputed on the host.  Header-only so the slab
+// back-transform's last block can run it right after the norms are known.
+#pragma once
+#include "kernels.cuh"
+
+namespace asdsm_b200 {
+
+constexpr int kSkelMaxKnots = 64;
+
+// per-line: second derivatives via the pre-eliminated tridiagonal system, then per-segment
+// (y_c, c1, c2, c3); y has nc+2 entries (y[0] = y[nc+1] = 0).
+__device__ inline void skel_line_segments(const double* tab, int nc, const double* y, double* seg) {
+  const int n = nc + 2, ni = nc;
+  const double* x = tab;
+  const double* hl = tab + n;
+  const double* hr = hl + ni;
+  const double* w = hr + ni;
+  const double* dg = w + ni;
+  const double* up = dg + ni;
+  double rhs[kSkelMaxKnots], m[kSkelMaxKnots];
+  for (int i = 0; i < n; ++i) m[i] = 0.0;
+  for (int i = 0; i < ni; ++i) rhs[i] = __dsub_rn(__dsub_rn(y[i + 2], y[i + 1]) / hr[i], __dsub_rn(y[i + 1], y[i]) / hl[i]);
+  for (int i = 1; i < ni; ++i) rhs[i] = __dsub_rn(rhs[i], __dmul_rn(w[i], rhs[i - 1]));
+  if (ni > 0) {
+    m[ni] = rhs[ni - 1] / dg[ni - 1];
+    for (int i = ni - 1; i >= 1; --i) m[i] = __dsub_rn(rhs[i - 1], __dmul_rn(up[i - 1], m[i + 1])) / dg[i - 1];
+  }
+  for (int c = 0; c <= nc; ++c) {
+    const double h = __dsub_rn(x[c + 1], x[c]);
+    seg[4 * c + 0] = y[c];
+    seg[4 * c + 1] = __dsub_rn(__dsub_rn(y[c + 1], y[c]) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m[c]), m[c + 1])) / 6.0);
+    seg[4 * c + 2] = m[c] / 2.0;
+    seg[4 * c + 3] = __dsub_rn(m[c + 1], m[c]) / __dmul_rn(6.0, h);
+  }
+}
+
+// evaluation at fine index fi (1-based) along an axis with factor n: same as CubicSpline()
+__device__ __forceinline__ double skel_seg_eval(const double* tab, const double* seg, int nc, int n, double hfine,
+                                                int fi) {
+  int c = fi / n;
+  if (c > nc) c = nc;
+  const double x = static_cast<double>(fi) * hfine;
+  const double t = __dsub_rn(x, tab[c]);
+  const double* s = seg + 4 * c;
+  return __dadd_rn(s[0], __dmul_rn(t, __dadd_rn(s[1], __dmul_rn(t, __dadd_rn(s[2], __dmul_rn(t, s[3]))))));
+}
+
+// the whole cc + spline phase, executed by all threads of one block
+__device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
+  const MeshDev& m = a.m;
+  const int nc0 = m.nc[0], nc1 = m.nc[1];
+  const double nfc = a.norm_fc ? *a.norm_fc : 1.0;
+  const double ncf = a.norm_cf ? *a.norm_cf : 1.0;
+  for (int t = threadIdx.x; t < nc0 * nc1; t += blockDim.x) {
+    const int I = t % nc0, J = t / nc0;
+    double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
+    double u2 = a.u_cf[I + static_cast<i64>(nc0) * ((J + 1) * m.n[1] - 1)];
+    if (a.norm_fc) {
+      u1 = u1 / nfc;
+      u2 = u2 / ncf;
+    }
+    double uh;
+    if (a.u_cc) uh = __dsub_rn(__dadd_rn(u1, u2), a.u_cc[t]);
+    else uh = (a.coin[0] == 0) ? u2 : u1;
+    a.e1[t] = __dsub_rn(uh, u1);
+    a.e2[t] = __dsub_rn(uh, u2);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nc0 + nc1; t += blockDim.x) {
+    double y[kSkelMaxKnots];
+    if (t < nc1) {
+      const int J = t;
+      y[0] = 0.0;
+      for (int C = 0; C < nc0; ++C) y[C + 1] = a.e1[C + static_cast<i64>(nc0) * J];
+      y[nc0 + 1] = 0.0;
+      skel_line_segments(a.sp_tab[0], nc0, y, a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1));
+    } else {
+      const int I = t - nc1;
+      y[0] = 0.0;
+      for (int C = 0; C < nc1; ++C) y[C + 1] = a.e2[I + static_cast<i64>(nc0) * C];
+      y[nc1 + 1] = 0.0;
+      skel_line_segments(a.sp_tab[1], nc1, y, a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1));
+    }
+  }
+}
+
+}  // namespace asdsm_b200

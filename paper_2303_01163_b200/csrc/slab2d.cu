@@ -6,6 +6,7 @@
 //            (solver.cpp:79-84), the last block finalizing both norms.
 #include "slab2d.cuh"
 #include "ctrl.cuh"
+#include "skel2d.cuh"
 
 #include <type_traits>
 
@@ -14,7 +15,7 @@ namespace asdsm_b200 {
 namespace {
 
 constexpr int kThreads = 1024;
-constexpr int kMaxSmem = 200 * 1024;
+constexpr int kMaxSmem = 220 * 1024;
 
 template <typename T>
 __device__ __forceinline__ T ld(const double* p, i64 i);
@@ -72,6 +73,34 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
       st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
     return;
   }
+  if (A.pcr_smem) {  // every level's factors bulk-loaded next to the line: pure smem PCR
+    double* sk1 = reinterpret_cast<double*>(x1 + nf);
+    double* sk2 = sk1 + static_cast<i64>(L) * nf;
+    const i64 base = static_cast<i64>(k) * L * nf;
+    for (int i = threadIdx.x; i < L * nf; i += blockDim.x) {
+      sk1[i] = __ldg(K1 + base + i);
+      sk2[i] = __ldg(K2 + base + i);
+    }
+    __syncthreads();
+    int s = 1;
+    for (int lev = 0; lev < L; ++lev, s <<= 1) {
+      const double* c1 = sk1 + static_cast<i64>(lev) * nf;
+      const double* c2 = sk2 + static_cast<i64>(lev) * nf;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        T v = x0[i];
+        if (i - s >= 0) v = v - c1[i] * x0[i - s];
+        if (i + s < nf) v = v - c2[i] * x0[i + s];
+        x1[i] = v;
+      }
+      __syncthreads();
+      T* t = x0;
+      x0 = x1;
+      x1 = t;
+    }
+    for (int i = threadIdx.x; i < nf; i += blockDim.x)
+      st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
+    return;
+  }
   constexpr int E = 6;  // elements per thread (line length <= 6144)
   T c1[E], c2[E];
 #pragma unroll
@@ -116,7 +145,8 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
 
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, double* partials, DevState* S,
-                                                                   double* history, CtrlArgs c) {
+                                                                   double* history, CtrlArgs c, Skel2DArgs sk,
+                                                                   int with_skel) {
   if (!S->active) return;
   const MeshDev& m = A.m;
   double ss[2] = {0.0, 0.0};
@@ -159,7 +189,10 @@ __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, 
       }
     }
   }
-  fold_ctrl(c, partials, S, history);
+  if (fold_ctrl(c, partials, S, history) && with_skel) {
+    __syncthreads();
+    if (S->have_e) skel2d_ccspline_block(sk);
+  }
 }
 
 }  // namespace
@@ -175,22 +208,30 @@ void slab2d_prepare() {
 void launch_slab2d_fwd(const Slab2DArgs& A, DevState* st, cudaStream_t s) {
   const int ncmax = std::max(A.m.nc[0], A.m.nc[1]);
   const int nfmax = std::max(A.m.nf[0], A.m.nf[1]);
-  const size_t smem = 2 * static_cast<size_t>(nfmax) * (A.cplx ? sizeof(cplx) : sizeof(double));
+  size_t smem = 2 * static_cast<size_t>(nfmax) * (A.cplx ? sizeof(cplx) : sizeof(double));
+  const int lmax = std::max(A.levels[0], A.levels[1]);
+  const size_t smem_full = smem + 2 * static_cast<size_t>(lmax) * nfmax * sizeof(double);
+  Slab2DArgs B = A;
+  B.pcr_smem = (!A.cplx && smem_full <= kMaxSmem) ? 1 : 0;
+  if (B.pcr_smem) smem = smem_full;
   if (!A.cplx && nfmax > 6 * kThreads) throw AsdsmError(kUnsupported, "2D slab line longer than 6144");
   if (smem > kMaxSmem) throw AsdsmError(kUnsupported, "2D slab line longer than shared memory allows");
   dim3 grid(static_cast<unsigned>(ncmax), 2);
-  if (A.cplx) slab2d_fwd_kernel<cplx><<<grid, kThreads, smem, s>>>(A, st);
-  else slab2d_fwd_kernel<double><<<grid, kThreads, smem, s>>>(A, st);
+  if (A.cplx) slab2d_fwd_kernel<cplx><<<grid, kThreads, smem, s>>>(B, st);
+  else slab2d_fwd_kernel<double><<<grid, kThreads, smem, s>>>(B, st);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }
 
 void launch_slab2d_back(const Slab2DArgs& A, double* partials, DevState* st, double* history, bool with_norms,
-                        cudaStream_t s) {
+                        cudaStream_t s, const Skel2DArgs* skel) {
   CtrlArgs c{};
   c.op = with_norms ? kCtrlSlabNorms2 : -1;
-  if (A.cplx) slab2d_back_kernel<cplx><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c);
-  else slab2d_back_kernel<double><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c);
+  Skel2DArgs sk{};
+  if (skel) sk = *skel;
+  const int ws = (skel && with_norms) ? 1 : 0;
+  if (A.cplx) slab2d_back_kernel<cplx><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c, sk, ws);
+  else slab2d_back_kernel<double><<<kRedBlocks, kRedThreads, 0, s>>>(A, partials, st, history, c, sk, ws);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

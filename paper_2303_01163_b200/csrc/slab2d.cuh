@@ -19,12 +19,14 @@ struct Slab2DArgs {
   const double* in_slab[2];       // smooth mode: assembled slab rhs
   double* modes[2];               // mode buffers [k][x] (T)
   double* sol[2];                 // slab solutions, slab layout
+  int pcr_smem;                   // set by the launcher: PCR factors staged in shared memory
 };
 
 void launch_slab2d_fwd(const Slab2DArgs& A, DevState* st, cudaStream_t s);
 // back transform + per-slab squared norms; the last block sets slab_norm[0..1] / have_e
+// with `skel`: the last block also runs the skeleton's cross-value/spline phase (error mode)
 void launch_slab2d_back(const Slab2DArgs& A, double* partials, DevState* st, double* history, bool with_norms,
-                        cudaStream_t s);
+                        cudaStream_t s, const Skel2DArgs* skel = nullptr);
 void slab2d_prepare();
 
 }  // namespace asdsm_b200

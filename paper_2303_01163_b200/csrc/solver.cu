@@ -131,8 +131,14 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
     }
     if (fast2d_) {
       slab2d_prepare();
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 2; ++a) {
         slab_modes_[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[1 - a] * 2);
+        const std::vector<double> tab = spline_axis_table(m.nc[a], m.n[a], m.h[a]);
+        sp_tab_[a] = dev_.alloc<double>(tab.size());
+        ASDSM_CUDA_CHECK(cudaMemcpy(sp_tab_[a], tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+      }
+      seg1_ = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * 4 * (m.nc[0] + 1));
+      seg2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * 4 * (m.nc[1] + 1));
     }
   }
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
@@ -185,6 +191,29 @@ void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
   launch_norm_sq(b_, g_fine_.size, partials_, state_, s, &c, history_);
 }
 
+Skel2DArgs Solver::skel2d_args(const double* const* sol, const double* u_cc, const int* coin, double* out) {
+  Skel2DArgs a{};
+  a.m = md_;
+  a.u_fc = sol[1];
+  a.u_cf = sol[0];
+  a.u_cc = u_cc;
+  a.coin = coin;
+  a.e1 = cc_e1_;
+  a.e2 = cc_e2_;
+  a.m1 = spl_m1_;
+  a.m2 = spl_m2_;
+  a.out = out;
+  if (coin != nullptr) {  // error mode: normalized on the fly (values / norm, as normalize_or_throw)
+    a.norm_fc = &state_->slab_norm[1];
+    a.norm_cf = &state_->slab_norm[0];
+  }
+  a.sp_tab[0] = sp_tab_[0];
+  a.sp_tab[1] = sp_tab_[1];
+  a.seg1 = seg1_;
+  a.seg2 = seg2_;
+  return a;
+}
+
 void Solver::skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s) {
   if (mesh_.dim == 3) {
     Merge3DArgs A = m3_;
@@ -205,9 +234,11 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
   a.m1 = spl_m1_;
   a.m2 = spl_m2_;
   a.out = out;
-  if (fast2d_ && coin != nullptr) {  // normalized on the fly (values / norm, as normalize_or_throw)
-    a.norm_fc = &state_->slab_norm[1];
-    a.norm_cf = &state_->slab_norm[0];
+  if (fast2d_) {
+    const Skel2DArgs f = skel2d_args(sol, u_cc, coin, out);
+    launch_skel2d_ccspline_fast(f, state_, s);
+    launch_skel2d_write_fast(f, state_, s);
+    return;
   }
   launch_skeleton2d(a, state_, s);
 }
@@ -227,9 +258,13 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nf1 = mesh_.nf[1];
     A.nbox0 = mesh_.nc[0] + 1;
     A.nbox1 = mesh_.nc[1] + 1;
-    A.kb = 64;
-    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 100 * 1024 ? 1 : 0;
-    hole2d_prepare(100 * 1024);
+    hole2d_prepare(220 * 1024);
+    A.kb = 32;
+    A.tables_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 110 * 1024 ? 1 : 0;  // 2 CTAs/SM
+    if (!A.tables_in_smem) {
+      A.kb = 64;
+      A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 100 * 1024 ? 1 : 0;
+    }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
     A.ipiv = H.th_ipiv;
@@ -330,10 +365,11 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
     Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
     A.in_fine0 = r0;
     A.in_fine1 = r1;
-    launch_slab2d_fwd(A, state_, s);
-    launch_slab2d_back(A, partials_, state_, history_, true, s);
     const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
-    skeleton(sol, nullptr, coins_ + 4 * k, out, s);
+    const Skel2DArgs sk = skel2d_args(sol, nullptr, coins_ + 4 * k, out);
+    launch_slab2d_fwd(A, state_, s);
+    launch_slab2d_back(A, partials_, state_, history_, true, s, &sk);  // + cc/spline phase in its last block
+    launch_skel2d_write_fast(sk, state_, s);
     fill(out, nullptr, s);
     return;
   }

@@ -109,6 +109,10 @@ class Solver {
   Merge3DArgs m3_{};
   bool fast2d_ = false;          // fused 2D slab/skeleton/hole path
   double* slab_modes_[2] = {nullptr, nullptr};
+  double* sp_tab_[2] = {nullptr, nullptr};
+  double* seg1_ = nullptr;
+  double* seg2_ = nullptr;
+  Skel2DArgs skel2d_args(const double* const* sol, const double* u_cc, const int* coin, double* out);
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
   double* partials_ = nullptr;
