@@ -68,6 +68,14 @@ __host__ __device__ inline void fma_acc(cplx& acc, cplx a, double b) {
 // Non-contracted arithmetic: the residual/stencil kernels reproduce the reference's
 // rounding sequence (CSR row dot in column order, proj/src/sparse.cpp:66-72) exactly.
 #ifdef __CUDACC__
+// Asynchronous global->shared copies (LDGSTS): many in flight per thread, no register staging.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }

@@ -157,22 +157,55 @@ __global__ void hole2d_fwd_thomas_smem_kernel(const double* __restrict__ e, doub
   const int ox = hx * A.n0, oy = hy * A.n1;
   const int kbase = blockIdx.y * KB;
   const int kcnt = min(KB, m0 - kbase);
+  // stage the table slices and the skeleton neighbours of the ring with cp.async
+  double* sBl = ys + m1 * KB;  // skeleton row below / above (m0 each), column left / right (m1 each)
+  double* sAb = sBl + m0;
+  double* sLe = sAb + m0;
+  double* sRi = sLe + m1;
   for (int t = threadIdx.x; t < m0 * KB; t += KB) {
     const int i = t / KB, kk = t % KB;
-    sW[t] = kk < kcnt ? __ldg(A.Wt + static_cast<i64>(i) * m0 + kbase + kk) : 0.0;
+    if (kk < kcnt) cp_async8(sW + t, A.Wt + static_cast<i64>(i) * m0 + kbase + kk);
+    else sW[t] = 0.0;
   }
   for (int t = threadIdx.x; t < m1 * KB; t += KB) {
     const int j = t / KB, kk = t % KB;
-    sI[t] = kk < kcnt ? __ldg(A.ipiv + static_cast<i64>(j) * m0 + kbase + kk) : 0.0;
-    sC[t] = kk < kcnt ? __ldg(A.cp + static_cast<i64>(j) * m0 + kbase + kk) : 0.0;
+    if (kk < kcnt) {
+      cp_async8(sI + t, A.ipiv + static_cast<i64>(j) * m0 + kbase + kk);
+      cp_async8(sC + t, A.cp + static_cast<i64>(j) * m0 + kbase + kk);
+    }
+  }
+  const i64 Nx = A.nf0;
+  for (int t = threadIdx.x; t < m0; t += KB) {
+    if (oy > 0) cp_async8(sBl + t, e + static_cast<i64>(oy - 1) * Nx + ox + t);
+    else sBl[t] = 0.0;
+    if (oy + m1 < A.nf1) cp_async8(sAb + t, e + static_cast<i64>(oy + m1) * Nx + ox + t);
+    else sAb[t] = 0.0;
   }
   for (int t = threadIdx.x; t < m1; t += KB) {
-    fL[t] = ring_rhs(e, A, ox, oy, 0, t);
-    fR[t] = ring_rhs(e, A, ox, oy, m0 - 1, t);
+    if (ox > 0) cp_async8(sLe + t, e + static_cast<i64>(oy + t) * Nx + ox - 1);
+    else sLe[t] = 0.0;
+    if (ox + m0 < A.nf0) cp_async8(sRi + t, e + static_cast<i64>(oy + t) * Nx + ox + m0);
+    else sRi[t] = 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ring rhs from the staged neighbours, same term order as ring_rhs (row_dot column order)
+  const Stencil& st = A.st;
+  auto ring = [&](int i, int j) -> double {
+    double acc = 0.0;
+    if (j == 0 && oy > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], sBl[i]));
+    if (i == 0 && ox > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], sLe[j]));
+    if (i == m0 - 1 && ox + m0 < A.nf0 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], sRi[j]));
+    if (j == m1 - 1 && oy + m1 < A.nf1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], sAb[i]));
+    return __dsub_rn(0.0, acc);
+  };
+  for (int t = threadIdx.x; t < m1; t += KB) {
+    fL[t] = ring(0, t);
+    fR[t] = ring(m0 - 1, t);
   }
   for (int t = threadIdx.x; t < m0; t += KB) {
-    fB[t] = ring_rhs(e, A, ox, oy, t, 0);
-    fT[t] = ring_rhs(e, A, ox, oy, t, m1 - 1);
+    fB[t] = ring(t, 0);
+    fT[t] = ring(t, m1 - 1);
   }
   __syncthreads();
   const int kk = threadIdx.x;
@@ -209,7 +242,7 @@ __global__ void hole2d_fwd_thomas_smem_kernel(const double* __restrict__ e, doub
 
 size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem) {
   if (tables_in_smem)
-    return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0) +
+    return sizeof(double) * (4 * static_cast<size_t>(m1) + 4 * static_cast<size_t>(m0) +
                              static_cast<size_t>(m0 + 3 * m1) * kb);
   return sizeof(double) * (2 * static_cast<size_t>(m1) + 2 * static_cast<size_t>(m0) +
                            (y_in_smem ? static_cast<size_t>(m1) * kb : 0));

@@ -51,6 +51,8 @@ __device__ __forceinline__ double skel_seg_eval(const double* tab, const double*
 __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
   const MeshDev& m = a.m;
   const int nc0 = m.nc[0], nc1 = m.nc[1];
+  __shared__ double se1[kSkelMaxKnots * kSkelMaxKnots / 4], se2[kSkelMaxKnots * kSkelMaxKnots / 4];
+  const bool in_smem = nc0 * nc1 <= kSkelMaxKnots * kSkelMaxKnots / 4;
   const double nfc = a.norm_fc ? *a.norm_fc : 1.0;
   const double ncf = a.norm_cf ? *a.norm_cf : 1.0;
   for (int t = threadIdx.x; t < nc0 * nc1; t += blockDim.x) {
@@ -64,22 +66,29 @@ __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
     double uh;
     if (a.u_cc) uh = __dsub_rn(__dadd_rn(u1, u2), a.u_cc[t]);
     else uh = (a.coin[0] == 0) ? u2 : u1;
-    a.e1[t] = __dsub_rn(uh, u1);
-    a.e2[t] = __dsub_rn(uh, u2);
+    const double d1 = __dsub_rn(uh, u1), d2 = __dsub_rn(uh, u2);
+    a.e1[t] = d1;
+    a.e2[t] = d2;
+    if (in_smem) {
+      se1[t] = d1;
+      se2[t] = d2;
+    }
   }
   __syncthreads();
+  const double* E1 = in_smem ? se1 : a.e1;
+  const double* E2 = in_smem ? se2 : a.e2;
   for (int t = threadIdx.x; t < nc0 + nc1; t += blockDim.x) {
     double y[kSkelMaxKnots];
     if (t < nc1) {
       const int J = t;
       y[0] = 0.0;
-      for (int C = 0; C < nc0; ++C) y[C + 1] = a.e1[C + static_cast<i64>(nc0) * J];
+      for (int C = 0; C < nc0; ++C) y[C + 1] = E1[C + static_cast<i64>(nc0) * J];
       y[nc0 + 1] = 0.0;
       skel_line_segments(a.sp_tab[0], nc0, y, a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1));
     } else {
       const int I = t - nc1;
       y[0] = 0.0;
-      for (int C = 0; C < nc1; ++C) y[C + 1] = a.e2[I + static_cast<i64>(nc0) * C];
+      for (int C = 0; C < nc1; ++C) y[C + 1] = E2[I + static_cast<i64>(nc0) * C];
       y[nc1 + 1] = 0.0;
       skel_line_segments(a.sp_tab[1], nc1, y, a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1));
     }

@@ -41,12 +41,24 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
   const i64 Nx = m.nf[0];
   for (int x = threadIdx.x; x < nf; x += blockDim.x) {
     T acc = zero_of<T>();
-    for (int j = 0; j < nc; ++j) {
-      double v;
-      const int fj = (j + 1) * m.n[a] - 1;  // station on the coarse axis
-      if (rf) v = (a == 0) ? rf[fj + Nx * x] : rf[x + Nx * fj];
-      else v = (a == 0) ? A.in_slab[a][j + static_cast<i64>(nc) * x] : A.in_slab[a][x + static_cast<i64>(nf) * j];
-      fma_acc(acc, ld<T>(A.W[a], static_cast<i64>(k) * nc + j), v);
+    for (int j0 = 0; j0 < nc; j0 += 8) {  // 8 independent station loads in flight
+      double v[8];
+      T w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q;
+        v[q] = 0.0;
+        w[q] = zero_of<T>();
+        if (j < nc) {
+          const int fj = (j + 1) * m.n[a] - 1;  // station on the coarse axis
+          if (rf) v[q] = (a == 0) ? __ldg(rf + fj + Nx * x) : __ldg(rf + x + Nx * fj);
+          else v[q] = (a == 0) ? __ldg(A.in_slab[a] + j + static_cast<i64>(nc) * x) : __ldg(A.in_slab[a] + x + static_cast<i64>(nf) * j);
+          w[q] = ld<T>(A.W[a], static_cast<i64>(k) * nc + j);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (j0 + q < nc) fma_acc(acc, w[q], v[q]);
     }
     x0[x] = acc;
   }
@@ -78,9 +90,10 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
     double* sk2 = sk1 + static_cast<i64>(L) * nf;
     const i64 base = static_cast<i64>(k) * L * nf;
     for (int i = threadIdx.x; i < L * nf; i += blockDim.x) {
-      sk1[i] = __ldg(K1 + base + i);
-      sk2[i] = __ldg(K2 + base + i);
+      cp_async8(sk1 + i, K1 + base + i);
+      cp_async8(sk2 + i, K2 + base + i);
     }
+    cp_async_wait_all();
     __syncthreads();
     int s = 1;
     for (int lev = 0; lev < L; ++lev, s <<= 1) {
@@ -163,7 +176,18 @@ __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, 
         j = static_cast<int>(t / nf);
       }
       T acc = zero_of<T>();
-      for (int k = 0; k < nc; ++k) fma_acc(acc, ld<T>(A.V[a], static_cast<i64>(j) * nc + k), ld<T>(A.modes[a], static_cast<i64>(k) * nf + x));
+      for (int k0 = 0; k0 < nc; k0 += 8) {
+        T vv[8], mm[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int k = k0 + q;
+          vv[q] = k < nc ? ld<T>(A.V[a], static_cast<i64>(j) * nc + k) : zero_of<T>();
+          mm[q] = k < nc ? ld<T>(A.modes[a], static_cast<i64>(k) * nf + x) : zero_of<T>();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (k0 + q < nc) fma_acc(acc, vv[q], mm[q]);
+      }
       const double v = real_part(acc);
       A.sol[a][t] = v;
       ss[a] += v * v;
