@@ -258,12 +258,15 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nf1 = mesh_.nf[1];
     A.nbox0 = mesh_.nc[0] + 1;
     A.nbox1 = mesh_.nc[1] + 1;
-    hole2d_prepare(220 * 1024);
+    // (a variant staging every table slice in shared memory first measured slower: its time
+    // goes into a dependent shared-store chain; kept available as tables_in_smem)
+    static const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
+    hole2d_prepare(113 * 1024);
     A.kb = 32;
-    A.tables_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 110 * 1024 ? 1 : 0;  // 2 CTAs/SM
+    A.tables_in_smem = (staged && hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 113 * 1024) ? 1 : 0;
     if (!A.tables_in_smem) {
       A.kb = 64;
-      A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 100 * 1024 ? 1 : 0;
+      A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
     }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
