@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--all-configs", action="store_true", help="also time every BASELINE config (value only)")
+    ap.add_argument("--no-all-configs", dest="all_configs", action="store_false",
+                    help="skip timing every other BASELINE config (value only)")
     return ap.parse_args()
 
 
