@@ -359,6 +359,18 @@ void launch_line_solve(const SepSolver& S, const BoxArray& buf, cudaStream_t st)
 
 }  // namespace
 
+void sep_back_transform(const SepSolver& S, void* modes, const BoxArray& out, void* scratch, cudaStream_t st) {
+  if (S.complex_modes) throw AsdsmError(kUnsupported, "sep_back_transform: complex modes");
+  const BoxArray c0 = compact_layout(S, out, modes);
+  if (S.nd == 1) {
+    launch_transform<double, double, double>(S, S.dax[0], c0, out, S.V[S.dax[0]], st);
+    return;
+  }
+  const BoxArray c1 = compact_layout(S, out, scratch);
+  launch_transform<double, double, double>(S, S.dax[1], c0, c1, S.V[S.dax[1]], st);
+  launch_transform<double, double, double>(S, S.dax[0], c1, out, S.V[S.dax[0]], st);
+}
+
 void sep_prepare() {
   static bool done = false;
   if (done) return;

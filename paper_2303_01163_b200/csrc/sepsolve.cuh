@@ -10,6 +10,10 @@ namespace asdsm_b200 {
 void sep_solve(const SepSolver& S, const BoxArray& in, const BoxArray& out, void* scratch0,
                void* scratch1, cudaStream_t stream);
 
+// Back transforms only (real modes): mode-space solution in `modes` (compact layout, same
+// batch as `out`) -> `out`, via `scratch` when two axes are diagonalized.
+void sep_back_transform(const SepSolver& S, void* modes, const BoxArray& out, void* scratch, cudaStream_t stream);
+
 // One-time kernel attribute setup (large dynamic shared memory for PCR); call before any
 // stream capture.
 void sep_prepare();

@@ -6,6 +6,7 @@
 
 #include "dmma_gemm.cuh"
 #include "holes2d.cuh"
+#include "holes3d.cuh"
 #include "slab2d.cuh"
 #include "march.cuh"
 
@@ -289,6 +290,30 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
     launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
+    return;
+  }
+  if (!generic && mesh_.dim == 3 && b == nullptr && !H.complex_modes && H.nd == 2 && H.L == 2 && H.dax[0] == 0 &&
+      H.dax[1] == 1 && !H.use_pcr) {
+    // Error mode: face-sparse forward transform + Thomas along the line axis, DMMA back transforms.
+    Hole3DArgs A{};
+    for (int a = 0; a < 3; ++a) {
+      A.m[a] = H.ext[a];
+      A.n[a] = mesh_.n[a];
+      A.nf[a] = mesh_.nf[a];
+      A.nbox[a] = mesh_.nc[a] + 1;
+    }
+    A.st = st_fine_;
+    A.Wx = H.W[0];
+    A.Wy = H.W[1];
+    A.ipiv = H.th_ipiv;
+    A.cp = H.th_cp;
+    A.line_left = H.line_left;
+    const i64 nholes = static_cast<i64>(A.nbox[0]) * A.nbox[1] * A.nbox[2];
+    if (!faces3d_) faces3d_ = dev_.alloc<double>(static_cast<size_t>(nholes) * hole3d_face_doubles(A));
+    A.faces = faces3d_;
+    launch_hole3d_faces(e, A, state_, s);
+    launch_hole3d_thomas(static_cast<double*>(scratch0_), A, state_, s);
+    sep_back_transform(H, scratch0_, hole_array(e), scratch1_, s);
     return;
   }
   launch_hole_rhs(mesh_.dim, e, b, fg_, st_fine_, md_, state_, s);

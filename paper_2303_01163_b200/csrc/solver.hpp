@@ -112,6 +112,7 @@ class Solver {
   double* sp_tab_[2] = {nullptr, nullptr};
   double* seg1_ = nullptr;
   double* seg2_ = nullptr;
+  double* faces3d_ = nullptr;  // 3D fused fill: transformed hole faces
   Skel2DArgs skel2d_args(const double* const* sol, const double* u_cc, const int* coin, double* out);
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
