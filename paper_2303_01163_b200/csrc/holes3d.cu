@@ -164,16 +164,25 @@ __global__ void __launch_bounds__(128) hole3d_thomas_kernel(double* __restrict__
 
 }  // namespace
 
-void launch_hole3d_faces(const double* e, const Hole3DArgs& A, DevState* st, cudaStream_t s) {
+static size_t faces_smem(const Hole3DArgs& A) {
   const int mm = std::max(A.m[0], std::max(A.m[1], A.m[2]));
-  const size_t smem = sizeof(double) * (static_cast<size_t>(A.m[0]) * A.m[0] + static_cast<size_t>(A.m[1]) * A.m[1] +
-                                        2 * static_cast<size_t>(mm) * mm);
-  static size_t set = 0;
-  if (smem > 48 * 1024 && smem > set) {
+  return sizeof(double) * (static_cast<size_t>(A.m[0]) * A.m[0] + static_cast<size_t>(A.m[1]) * A.m[1] +
+                           2 * static_cast<size_t>(mm) * mm);
+}
+
+void hole3d_prepare(const Hole3DArgs& A) {
+  static size_t set = 48 * 1024;
+  const size_t smem = faces_smem(A);
+  if (smem > 220 * 1024) throw AsdsmError(kUnsupported, "3D hole faces exceed shared memory");
+  if (smem > set) {
     ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole3d_faces_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(smem)));
     set = smem;
   }
+}
+
+void launch_hole3d_faces(const double* e, const Hole3DArgs& A, DevState* st, cudaStream_t s) {
+  const size_t smem = faces_smem(A);
   const unsigned nh = static_cast<unsigned>(A.nbox[0] * A.nbox[1] * A.nbox[2]);
   hole3d_faces_kernel<<<nh, 256, smem, s>>>(e, A, st);
   ASDSM_CUDA_CHECK(cudaGetLastError());

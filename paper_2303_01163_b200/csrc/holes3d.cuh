@@ -23,6 +23,7 @@ __host__ __device__ inline size_t hole3d_face_doubles(const Hole3DArgs& A) {  //
   return 2 * static_cast<size_t>(A.m[2]) * A.m[1] + 2 * static_cast<size_t>(A.m[2]) * A.m[0] +
          2 * static_cast<size_t>(A.m[1]) * A.m[0];
 }
+void hole3d_prepare(const Hole3DArgs& A);  // shared-memory attribute, before any capture
 void launch_hole3d_faces(const double* e, const Hole3DArgs& A, DevState* st, cudaStream_t s);
 void launch_hole3d_thomas(double* modes, const Hole3DArgs& A, DevState* st, cudaStream_t s);
 

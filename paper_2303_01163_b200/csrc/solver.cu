@@ -121,6 +121,12 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
     }
   }
   partials_ = dev_.alloc<double>(4 * static_cast<size_t>(kRedStride));
+  if (m.dim == 3) {  // 3D fused fill buffers (allocated here: never during graph capture)
+    Hole3DArgs A{};
+    for (int a = 0; a < 3; ++a) A.m[a] = m.n[a] - 1;
+    faces3d_ = dev_.alloc<double>(static_cast<size_t>(nholes) * hole3d_face_doubles(A));
+    hole3d_prepare(A);
+  }
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
   if (m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
@@ -308,8 +314,6 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.ipiv = H.th_ipiv;
     A.cp = H.th_cp;
     A.line_left = H.line_left;
-    const i64 nholes = static_cast<i64>(A.nbox[0]) * A.nbox[1] * A.nbox[2];
-    if (!faces3d_) faces3d_ = dev_.alloc<double>(static_cast<size_t>(nholes) * hole3d_face_doubles(A));
     A.faces = faces3d_;
     launch_hole3d_faces(e, A, state_, s);
     launch_hole3d_thomas(static_cast<double*>(scratch0_), A, state_, s);
