@@ -109,6 +109,10 @@ __device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, doubl
       S->stop_at = c.tol * (S->b_l2 > 0.0 ? S->b_l2 : 1.0);
       break;
     }
+    case kCtrlSetStep: {
+      S->s = c.cell;
+      break;
+    }
     case kCtrlSlabNorms2: {
       const double n0 = sqrt(s0), n1 = sqrt(s2);
       S->slab_norm[0] = n0;

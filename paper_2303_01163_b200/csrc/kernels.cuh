@@ -69,6 +69,7 @@ enum CtrlOp {
   kCtrlAccept = 3,       // next norms; accept/revert; record row k; stop rules
   kCtrlInit = 4,         // ||b||_2 -> stop_at = tol * (||b|| > 0 ? ||b|| : 1)
   kCtrlSlabNorms2 = 5,   // slot 0 / slot 2 sums -> slab_norm[0], slab_norm[1]; have_e
+  kCtrlSetStep = 6,      // profiling only: s = CtrlArgs::cell
 };
 struct CtrlArgs {
   int op;

@@ -291,16 +291,39 @@ __global__ void m3_apply_kernel(Merge3DArgs A, int a, const DevState* st) {
 }
 
 // ---- M4 ----------------------------------------------------------------------------------
+// Skeleton points only, enumerated plane family by plane family without duplicates:
+// family 0: x-coarse planes (all y, z); family 1: y-coarse planes with x not coarse;
+// family 2: z-coarse planes with x, y not coarse.
 __global__ void m4_kernel(Merge3DArgs A, double* out, const DevState* st) {
   if (!st->active || !st->have_e) return;
   const MeshDev& m = A.m;
-  const i64 total = static_cast<i64>(m.nf[0]) * m.nf[1] * m.nf[2];
-  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+  const i64 nf0 = m.nf[0], nf1 = m.nf[1], nf2 = m.nf[2];
+  const i64 fx = nf0 - m.nc[0], fy = nf1 - m.nc[1];  // non-coarse counts per axis
+  const i64 n0 = static_cast<i64>(m.nc[0]) * nf1 * nf2;
+  const i64 n1 = fx * m.nc[1] * nf2;
+  const i64 n2 = fx * fy * m.nc[2];
+  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n0 + n1 + n2;
        t += static_cast<i64>(gridDim.x) * blockDim.x) {
     int f[3];
-    f[0] = static_cast<int>(t % m.nf[0]);
-    f[1] = static_cast<int>((t / m.nf[0]) % m.nf[1]);
-    f[2] = static_cast<int>(t / (static_cast<i64>(m.nf[0]) * m.nf[1]));
+    auto noncoarse = [&](int a, i64 q) {  // q-th non-coarse fine index along axis a
+      return static_cast<int>(q + q / (m.n[a] - 1));
+    };
+    if (t < n0) {
+      const i64 q = t;
+      f[0] = (static_cast<int>(q % m.nc[0]) + 1) * m.n[0] - 1;
+      f[1] = static_cast<int>((q / m.nc[0]) % nf1);
+      f[2] = static_cast<int>(q / (m.nc[0] * nf1));
+    } else if (t < n0 + n1) {
+      const i64 q = t - n0;
+      f[0] = noncoarse(0, q % fx);
+      f[1] = (static_cast<int>((q / fx) % m.nc[1]) + 1) * m.n[1] - 1;
+      f[2] = static_cast<int>(q / (fx * m.nc[1]));
+    } else {
+      const i64 q = t - n0 - n1;
+      f[0] = noncoarse(0, q % fx);
+      f[1] = noncoarse(1, (q / fx) % fy);
+      f[2] = (static_cast<int>(q / (fx * fy)) + 1) * m.n[2] - 1;
+    }
     bool on[3];
     int cc[3];
     int non = 0;
@@ -309,7 +332,6 @@ __global__ void m4_kernel(Merge3DArgs A, double* out, const DevState* st) {
       cc[a] = (f[a] + 1) / m.n[a] - 1;
       non += on[a];
     }
-    if (non == 0) continue;
     double v = 0.0;
     for (int a = 0; a < 3; ++a) {
       if (!on[a]) continue;
@@ -326,7 +348,7 @@ __global__ void m4_kernel(Merge3DArgs A, double* out, const DevState* st) {
         v = __dadd_rn(v, -A.T[pair_slot(a, b)][kind_ext(m, (1u << a) | (1u << b)).lin(q[0], q[1], q[2])]);
       }
     if (non == 3) v = __dadd_rn(v, A.u_hat[cc[0] + static_cast<i64>(m.nc[0]) * (cc[1] + static_cast<i64>(m.nc[1]) * cc[2])]);
-    out[t] = v;
+    out[f[0] + nf0 * (f[1] + nf1 * static_cast<i64>(f[2]))] = v;
   }
 }
 
@@ -364,8 +386,10 @@ void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_
     m3_apply_kernel<<<nblk(ns, 256), 256, 0, s>>>(A, a, st);
     g_kernel_launches += 3;
   }
-  const i64 nfine = static_cast<i64>(m.nf[0]) * m.nf[1] * m.nf[2];
-  m4_kernel<<<nblk(nfine, 256), 256, 0, s>>>(A, out, st);
+  const i64 nskel = static_cast<i64>(m.nc[0]) * m.nf[1] * m.nf[2] +
+                   static_cast<i64>(m.nf[0] - m.nc[0]) * m.nc[1] * m.nf[2] +
+                   static_cast<i64>(m.nf[0] - m.nc[0]) * (m.nf[1] - m.nc[1]) * m.nc[2];
+  m4_kernel<<<nblk(nskel, 256, 32 * kNumSms), 256, 0, s>>>(A, out, st);
   ++g_kernel_launches;
   ASDSM_CUDA_CHECK(cudaGetLastError());
 }
