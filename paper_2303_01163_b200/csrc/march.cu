@@ -11,6 +11,8 @@
 #include "ctrl.cuh"
 #include "march.cuh"
 
+#include <cstdlib>
+
 namespace asdsm_b200 {
 
 namespace {
@@ -253,6 +255,83 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+// Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
+// thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
+// ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
+constexpr int ZC = 8;
+template <int MODE>
+__global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const int cur = S->cur;
+  double s = 0.0;
+  bool work = true;
+  if (MODE == kMarchUpdate) {
+    s = S->s;
+    work = s != 0.0;
+  }
+  if (MODE == kMarchDots) work = S->have_e != 0;
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
+  const i64 sy = A.g.stride[1], sz = A.g.stride[2];
+  const Stencil& st = A.st;
+  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  Src<MODE> V{uu, A.e, s};
+  const double* __restrict__ rcur = cur ? A.r1 : A.r0;
+  double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
+  double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
+  const int ntx = (Nx + 31) / 32, nty = (Ny + 7) / 8, ntz = (Nz + ZC - 1) / ZC;
+  const long long ntiles = static_cast<long long>(ntx) * nty * ntz;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (long long tile = work ? blockIdx.x : ntiles; tile < ntiles; tile += gridDim.x) {
+    const int bx = static_cast<int>(tile % ntx);
+    const int by = static_cast<int>((tile / ntx) % nty);
+    const int bz = static_cast<int>(tile / (static_cast<long long>(ntx) * nty));
+    const int x = bx * 32 + tx, y = by * 8 + ty, z0 = bz * ZC;
+    if (x >= Nx || y >= Ny) continue;
+    const i64 pxy = x + y * sy;
+    double vz[ZC + 2];
+#pragma unroll
+    for (int q = 0; q < ZC + 2; ++q) {
+      const int z = z0 - 1 + q;
+      vz[q] = (z >= 0 && z < Nz) ? V(pxy + z * sz) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < ZC; ++q) {
+      const int z = z0 + q;
+      if (z >= Nz) break;
+      const i64 p = pxy + z * sz;
+      double acc = 0.0;
+      if (z > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[2], vz[q]));
+      if (y > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], V(p - sy)));
+      if (x > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], V(p - 1)));
+      const double vc = vz[q + 1];
+      acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
+      if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], V(p + 1)));
+      if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], V(p + sy)));
+      if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(st.right[2], vz[q + 2]));
+      if (MODE == kMarchDots) {
+        const double rp = __ldg(rcur + p);
+        a0 += rp * acc;
+        a2 += acc * acc;
+      } else {
+        const double r = __dsub_rn(__ldg(A.b + p), acc);
+        ro[p] = r;
+        if (MODE == kMarchUpdate) uo[p] = vc;
+        a0 += r * r;
+        a1 = fmax(a1, fabs(r));
+        if (A.exact) {
+          const double d = vc - __ldg(A.exact + p);
+          a2 += d * d;
+          a3 = fmax(a3, fabs(d));
+        }
+      }
+    }
+  }
+  block_reduce4_march(a0, a1, a2, a3, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
 }  // namespace
 
 int march_strip(const FineGeom& g) {
@@ -289,6 +368,11 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     if (mode == kMarchResidual) march2d_kernel<kMarchResidual><<<nb, TX2, 0, s>>>(A);
     else if (mode == kMarchUpdate) march2d_kernel<kMarchUpdate><<<nb, TX2, 0, s>>>(A);
     else march2d_kernel<kMarchDots><<<nb, TX2, 0, s>>>(A);
+  } else if (std::getenv("ASDSM_MARCH3D") == nullptr) {
+    const unsigned nbz = 8 * kNumSms;
+    if (mode == kMarchResidual) stencil3d_zc_kernel<kMarchResidual><<<nbz, 256, 0, s>>>(A);
+    else if (mode == kMarchUpdate) stencil3d_zc_kernel<kMarchUpdate><<<nbz, 256, 0, s>>>(A);
+    else stencil3d_zc_kernel<kMarchDots><<<nbz, 256, 0, s>>>(A);
   } else {
     if (mode == kMarchResidual) march3d_kernel<kMarchResidual><<<nb, TX3 * TY3, 0, s>>>(A);
     else if (mode == kMarchUpdate) march3d_kernel<kMarchUpdate><<<nb, TX3 * TY3, 0, s>>>(A);
