@@ -368,7 +368,9 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     if (mode == kMarchResidual) march2d_kernel<kMarchResidual><<<nb, TX2, 0, s>>>(A);
     else if (mode == kMarchUpdate) march2d_kernel<kMarchUpdate><<<nb, TX2, 0, s>>>(A);
     else march2d_kernel<kMarchDots><<<nb, TX2, 0, s>>>(A);
-  } else if (std::getenv("ASDSM_MARCH3D") == nullptr) {
+  } else if (std::getenv("ASDSM_MARCH3D") == nullptr && mode != kMarchUpdate) {
+    // measured (config 3/4): the barrier-free z-coarsened pass streams the residual and the
+    // dot-product passes faster; the smem-plane march is faster for the 5-array update pass
     const unsigned nbz = 8 * kNumSms;
     if (mode == kMarchResidual) stencil3d_zc_kernel<kMarchResidual><<<nbz, 256, 0, s>>>(A);
     else if (mode == kMarchUpdate) stencil3d_zc_kernel<kMarchUpdate><<<nbz, 256, 0, s>>>(A);
