@@ -102,6 +102,11 @@ int cmd_iterate(int argc, char** argv) {
   o.tol = 0.0;
   o.max_iter = iters;
   o.stagnation_window = 0;
+  if (std::getenv("REF_DUMP_DEFAULT_OPTS")) {  // the reference's IterateOptions defaults (solver.hpp:56-68)
+    o.tol = 1e-12;
+    o.stagnation_window = 3;
+    o.stagnation_ratio = 0.99;
+  }
   o.rng_seed = std::strtoull(argv[6], nullptr, 10);
   if (argc > 8) o.subsample = std::atof(argv[8]);
   std::vector<double> u0, r0;

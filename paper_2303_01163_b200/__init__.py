@@ -27,7 +27,14 @@ from .asdsm import (  # noqa: F401
     UnknownExample,
     Unsupported,
     ZeroNormSolution,
+    RunConfig,
+    RunResult,
     asdsm_iterate,
+    example_mesh,
+    format_history_csv,
+    residual_snapshot,
+    run_experiment,
+    write_text_file,
     baseline_mesh,
     baseline_problem,
     build_projector,

@@ -514,3 +514,76 @@ def hole_positions(config: MeshConfig, plan: SolverContext = None) -> np.ndarray
 
 def nan_to_none(x):
     return None if (x is None or math.isnan(x)) else x
+
+
+# ---------------------------------------------------------------- runner (runner.hpp) -------
+@dataclass
+class RunConfig:
+    """RunConfig (proj/include/asdsm/runner.hpp:16-27)."""
+    example: int = 1
+    setting: int = 1
+    nf: int = 99
+    nc: int = 9
+    tol: float = 1e-12
+    max_iter: int = 20
+    subsample: float = 0.0
+    seed: int = 0
+    out: str = ""
+
+
+@dataclass
+class RunResult:
+    state: IterationState
+    csv: str
+
+
+def _g17(v: float) -> str:
+    return "%.17g" % v
+
+
+def format_history_csv(history: Sequence[IterationRecord]) -> str:
+    """format_history_csv (runner.hpp:37, runner.cpp:34-46): fixed header, %.17g floats."""
+    lines = ["k,res_l2,res_inf,err_max,err_l2,s_hat,wall_ms"]
+    for h in history:
+        lines.append(",".join([str(int(h.k))] + [_g17(v) for v in (h.res_l2, h.res_inf, h.err_max, h.err_l2,
+                                                                     h.s_hat, h.wall_ms)]))
+    return "\n".join(lines) + "\n"
+
+
+def write_text_file(path: str, content: str):
+    """write_text_file (runner.hpp:50)."""
+    try:
+        with open(path, "w", newline="") as f:
+            f.write(content)
+    except OSError as e:
+        raise Error(f"cannot write {path}") from e
+
+
+def run_experiment(config: RunConfig) -> RunResult:
+    """run_experiment (runner.hpp:41, runner.cpp:48-56)."""
+    mesh = example_mesh(config.example, config.setting, config.nf, config.nc)
+    prob = make_problem(config.example, config.setting)
+    opts = IterateOptions(tol=config.tol, max_iter=config.max_iter, subsample=config.subsample,
+                          rng_seed=config.seed)
+    st = asdsm_iterate(prob, mesh, opts)
+    csv = format_history_csv(st.history)
+    if config.out:
+        write_text_file(config.out, csv)
+    return RunResult(st, csv)
+
+
+def residual_snapshot(config: RunConfig, at_iter: int) -> str:
+    """residual_snapshot (runner.hpp:46, runner.cpp:58-83): |r| after exactly at_iter
+    iterations, one CSV row per axis-1 line.  2D meshes only."""
+    if at_iter < 0 or at_iter > config.max_iter:
+        raise Error(f"snapshot iteration {at_iter} outside [0, max_iter]")
+    mesh = example_mesh(config.example, config.setting, config.nf, config.nc)
+    if mesh.dim != 2:
+        raise DimensionMismatch("residual snapshots need a 2D mesh")
+    prob = make_problem(config.example, config.setting)
+    opts = IterateOptions(tol=0.0, max_iter=at_iter, stagnation_window=0, subsample=config.subsample,
+                          rng_seed=config.seed)
+    st = asdsm_iterate(prob, mesh, opts)
+    n0, n1 = mesh.fine_counts
+    r = np.abs(st.r).reshape(n1, n0)
+    return "".join(",".join(_g17(v) for v in row) + "\n" for row in r)

@@ -84,7 +84,9 @@ __device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, doubl
     row[3] = S->err_max;
     row[4] = S->err_l2;
     row[5] = s_hat;
-    row[6] = 0.0;
+    unsigned long long tns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+    row[6] = static_cast<double>(tns);  // absolute ns; converted to per-row wall_ms on fetch
     S->nrec = k + 1;
   };
   switch (c.op) {

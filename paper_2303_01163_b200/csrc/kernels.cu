@@ -432,6 +432,9 @@ __global__ void state_init_kernel(DevState* S, int active, int have_e) {
   h.cur = 0;
   h.active = active;
   h.have_e = have_e;
+  unsigned long long tns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+  h.t0_ns = static_cast<double>(tns);
   *S = h;
 }
 

@@ -26,6 +26,7 @@ struct DevState {
   double slab_norm[3];
   double stop_at;                // tol * ||b||_2 (or tol when b == 0)
   double b_l2;
+  double t0_ns;                  // %globaltimer at state init (history wall_ms origin)
 };
 
 struct FineGeom {

@@ -529,6 +529,14 @@ int Solver::history(std::vector<double>& rows, int& stop_code, cudaStream_t s) c
   if (h.nrec > 0)
     ASDSM_CUDA_CHECK(cudaMemcpyAsync(rows.data(), history_, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
   ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  // wall_ms: time since the previous record (row 0: since the solve started), as the
+  // reference's record() does (solver.cpp:586-610), from the device %globaltimer
+  double prev = h.t0_ns;
+  for (int k = 0; k < h.nrec; ++k) {
+    const double t = rows[static_cast<size_t>(k) * 7 + 6];
+    rows[static_cast<size_t>(k) * 7 + 6] = (t - prev) / 1e6;
+    prev = t;
+  }
   stop_code = h.stop == 0 ? 3 : h.stop;
   return h.nrec;
 }
