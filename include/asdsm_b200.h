@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define ASDSM_B200_ABI_VERSION 1
+#define ASDSM_B200_ABI_VERSION 2
 
 /* Status codes <-> errors.hpp exception classes. */
 enum asdsm_status {
@@ -52,8 +52,9 @@ typedef struct {
   int32_t max_iter;         /* default 20                                                */
   int32_t stagnation_window;/* 0 disables; default 3                                     */
   double stagnation_ratio;  /* default 0.99                                              */
-  double subsample;         /* must be 0 on this path (all rows)                         */
+  double subsample;         /* fraction of skeleton rows for the step length; 0 = all     */
   uint64_t rng_seed;        /* default 0                                                 */
+  int32_t sparse_residual;  /* evaluate residual updates on skeleton rows only; default 0 */
 } asdsm_iterate_options;
 
 const char* asdsm_last_error(void);

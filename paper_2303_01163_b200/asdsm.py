@@ -94,7 +94,7 @@ def library_path() -> str:
 class _Options(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32),
                 ("stagnation_window", ctypes.c_int32), ("stagnation_ratio", ctypes.c_double),
-                ("subsample", ctypes.c_double), ("rng_seed", ctypes.c_uint64)]
+                ("subsample", ctypes.c_double), ("rng_seed", ctypes.c_uint64), ("sparse_residual", ctypes.c_int32)]
 
 
 def load_library():
@@ -350,10 +350,11 @@ class IterateOptions:
     stagnation_ratio: float = 0.99
     subsample: float = 0.0
     rng_seed: int = 0
+    sparse_residual: bool = False
 
     def _c(self):
         return _Options(self.tol, self.max_iter, self.stagnation_window, self.stagnation_ratio, self.subsample,
-                        self.rng_seed)
+                        self.rng_seed, int(self.sparse_residual))
 
 
 @dataclass

@@ -65,6 +65,7 @@ void asdsm_default_options(asdsm_iterate_options* o) {
   o->stagnation_ratio = 0.99;
   o->subsample = 0.0;
   o->rng_seed = 0;
+  o->sparse_residual = 0;
 }
 
 int asdsm_problem_example(int example, int setting, asdsm_problem** out) {
@@ -218,7 +219,8 @@ static RunOptions to_run(const asdsm_iterate_options* o) {
     r.subsample = o->subsample;
     r.rng_seed = o->rng_seed;
   }
-  if (r.subsample != 0.0) throw AsdsmError(kUnsupported, "subsample > 0 is not supported on the B200 path yet");
+  if (o) r.sparse_residual = o->sparse_residual != 0;
+  if (r.subsample < 0.0) r.subsample = 0.0;
   if (r.max_iter < 0) r.max_iter = 0;
   return r;
 }

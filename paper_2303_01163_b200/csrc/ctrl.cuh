@@ -128,8 +128,13 @@ __device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, doubl
       if (!(n > 0.0)) S->have_e = 0;
       break;
     }
-    case kCtrlStep: {
-      double s = 0.0;
+    case kCtrlSubDots: {
+      S->num_sub = s0;
+      S->den_sub = s2;
+      break;
+    }
+    case kCtrlStep: {  // optimal_scaling (solver.cpp:447-484), clamp at zero
+      double s = 0.0, ssub = 0.0;
       if (S->have_e) {
         S->num = s0;
         S->den = s2;
@@ -137,12 +142,26 @@ __device__ inline void ctrl_apply(const CtrlArgs& c, double s0, double m1, doubl
           const double q = s0 / s2;
           s = (0.0 < q) ? q : 0.0;
         }
+        if (c.subsample && S->den_sub > 0.0) {
+          const double q = S->num_sub / S->den_sub;
+          ssub = (0.0 < q) ? q : 0.0;
+        }
       }
-      S->s = s;
+      S->s_full = s;
+      S->s = c.subsample ? ssub : s;
+      S->retry = 0;
       break;
     }
-    case kCtrlAccept: {
+    case kCtrlAccept:
+    case kCtrlAccept2: {  // residual-growth guard + record + stop rules (solver.cpp:648-677)
+      if (c.op == kCtrlAccept2 && !S->retry) break;  // no retry was needed: already recorded
       double s = S->s;
+      if (c.op == kCtrlAccept && c.subsample && s != 0.0 && sqrt(s0) > S->res_l2 * c.tol_growth) {
+        S->retry = 1;  // the subsampled step grew the residual: retry with all rows
+        S->s = S->s_full;
+        break;
+      }
+      S->retry = 0;
       if (s != 0.0) {
         const double nl2 = sqrt(s0);
         if (nl2 > S->res_l2 * c.tol_growth) {

@@ -634,6 +634,49 @@ std::vector<double> spline_axis_table(int nc, int n, double h) {
   return tab;
 }
 
+namespace {
+
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads) subsample_dots_kernel(const long long* rows, int nrows, const double* e,
+                                                                      const double* r0, const double* r1, FineGeom g,
+                                                                      Stencil st, double* partials, DevState* S,
+                                                                      double* history, CtrlArgs c) {
+  if (!S->active) return;
+  const double* r = S->cur ? r1 : r0;
+  double num = 0.0, den = 0.0;
+  if (S->have_e) {
+    auto V = [&](i64 q, int, int) -> double { return e[q]; };
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * blockDim.x) {
+      const i64 p = rows[t];
+      const int i = static_cast<int>(p % g.ext[0]);
+      const int j = static_cast<int>((p / g.ext[0]) % g.ext[1]);
+      const int k = DIM == 3 ? static_cast<int>(p / (static_cast<i64>(g.ext[0]) * g.ext[1])) : 0;
+      double vp;
+      const double w = apply_row<DIM>(g, st, p, i, j, k, V, vp);
+      num += r[p] * w;
+      den += w * w;
+    }
+  }
+  block_reduce4_march(num, 0.0, den, 0.0, partials);
+  fold_ctrl(c, partials, S, history);
+}
+
+}  // namespace
+
+void launch_subsample_dots(int dim, const long long* rows, int nrows, const double* e, const double* r0,
+                           const double* r1, const FineGeom& g, const Stencil& st, double* partials,
+                           DevState* state, double* history, cudaStream_t s) {
+  CtrlArgs c{};
+  c.op = kCtrlSubDots;
+  const unsigned nb = static_cast<unsigned>(std::max(1, std::min((nrows + 255) / 256, kRedBlocks)));
+  if (dim == 2)
+    subsample_dots_kernel<2><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c);
+  else
+    subsample_dots_kernel<3><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
                      DevState* state, cudaStream_t s) {
   if (dim == 2) hole_rhs_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);

@@ -27,6 +27,10 @@ struct DevState {
   double stop_at;                // tol * ||b||_2 (or tol when b == 0)
   double b_l2;
   double t0_ns;                  // %globaltimer at state init (history wall_ms origin)
+  double num_sub, den_sub;       // subsampled <r,Ae>, <Ae,Ae> (subsample > 0)
+  double s_full;                 // all-rows step, for the residual-growth retry
+  int retry;                     // subsampled step grew the residual: second update pending
+  int pad2_;
 };
 
 struct FineGeom {
@@ -71,6 +75,8 @@ enum CtrlOp {
   kCtrlInit = 4,         // ||b||_2 -> stop_at = tol * (||b|| > 0 ? ||b|| : 1)
   kCtrlSlabNorms2 = 5,   // slot 0 / slot 2 sums -> slab_norm[0], slab_norm[1]; have_e
   kCtrlSetStep = 6,      // profiling only: s = CtrlArgs::cell
+  kCtrlSubDots = 7,      // subsampled dots -> num_sub, den_sub
+  kCtrlAccept2 = 8,      // outcome of the all-rows retry update (subsample > 0)
 };
 struct CtrlArgs {
   int op;
@@ -83,6 +89,7 @@ struct CtrlArgs {
   double stagnation_pow;  // ratio^window
   int max_iter;
   double tol;
+  int subsample;        // subsample > 0: step from the seeded row subset, all-rows retry
 };
 void launch_ctrl(const CtrlArgs& a, const double* partials, DevState* state, double* history, cudaStream_t s);
 
@@ -116,6 +123,12 @@ std::vector<double> spline_axis_table(int nc, int n, double h);
 
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
                      DevState* state, cudaStream_t s);
+
+// subsample > 0: <r, Ae>, <Ae, Ae> over a sorted list of skeleton rows (solver.cpp:462-481),
+// folded into kCtrlSubDots.
+void launch_subsample_dots(int dim, const long long* rows, int nrows, const double* e, const double* r0,
+                           const double* r1, const FineGeom& g, const Stencil& st, double* partials,
+                           DevState* state, double* history, cudaStream_t s);
 
 // Dense coarse solve x = Ainv b (small), single CTA.
 void launch_dense_matvec(const double* Ainv, const double* b, double* x, int n, DevState* state, cudaStream_t s);

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
   bool work = true;
   if (MODE == kMarchUpdate) {
     s = S->s;
-    work = s != 0.0;
+    work = s != 0.0 && (!A.retry_pass || S->retry);
   }
   if (MODE == kMarchDots) work = S->have_e != 0;
   const int Nx = A.g.ext[0], Ny = A.g.ext[1];
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
           a0 += rq * acc;
           a2 += acc * acc;
         } else {
-          const double r = __dsub_rn(bq, acc);
+          double r = __dsub_rn(bq, acc);
+          if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
           ro[p] = r;
           if (MODE == kMarchUpdate) uo[p] = vc;
           a0 += r * r;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   bool work = true;
   if (MODE == kMarchUpdate) {
     s = S->s;
-    work = s != 0.0;
+    work = s != 0.0 && (!A.retry_pass || S->retry);
   }
   if (MODE == kMarchDots) work = S->have_e != 0;
   const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
@@ -224,7 +225,8 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
           a0 += rq * acc;
           a2 += acc * acc;
         } else {
-          const double r = __dsub_rn(bq, acc);
+          double r = __dsub_rn(bq, acc);
+          if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
           ro[p] = r;
           if (MODE == kMarchUpdate) uo[p] = vc;
           a0 += r * r;
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
   bool work = true;
   if (MODE == kMarchUpdate) {
     s = S->s;
-    work = s != 0.0;
+    work = s != 0.0 && (!A.retry_pass || S->retry);
   }
   if (MODE == kMarchDots) work = S->have_e != 0;
   const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
@@ -315,7 +317,10 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
         a0 += rp * acc;
         a2 += acc * acc;
       } else {
-        const double r = __dsub_rn(__ldg(A.b + p), acc);
+        double r = __dsub_rn(__ldg(A.b + p), acc);
+        if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0 &&
+            (z + 1) % A.n[2] != 0)
+          r = 0.0;
         ro[p] = r;
         if (MODE == kMarchUpdate) uo[p] = vc;
         a0 += r * r;

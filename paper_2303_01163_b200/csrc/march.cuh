@@ -24,6 +24,9 @@ struct MarchArgs {
   CtrlArgs ctrl;
   double* history;
   int strip;  // 2D rows per CTA (set by launch_march)
+  int retry_pass;  // UPDATE: the all-rows retry of a subsampled step (runs only if state->retry)
+  int sparse;      // UPDATE: sparse_residual -- hole rows get r = 0 (solver.cpp:638-643)
+  int n[3];        // refinement factors (hole-row test for sparse)
 };
 
 int march_strip(const FineGeom& g);

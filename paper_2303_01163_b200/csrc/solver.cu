@@ -10,6 +10,7 @@
 #include "slab2d.cuh"
 #include "march.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -350,6 +351,10 @@ static MarchArgs march_args(const double* u0, const double* u1, const double* e,
   return A;
 }
 
+static void set_factors(MarchArgs& A, const Mesh& m) {
+  for (int a = 0; a < 3; ++a) A.n[a] = a < m.dim ? m.n[a] : 1;
+}
+
 static Slab2DArgs slab2d_args(const MeshDev& md, const SepSolver* S, double* const* modes, double* const* sol) {
   Slab2DArgs A{};
   A.m = md;
@@ -455,6 +460,48 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
   }
   ASDSM_CUDA_CHECK(cudaMemcpyAsync(coins_, coins.data(), coins.size() * sizeof(int), cudaMemcpyHostToDevice, s));
 
+  // subsample > 0 (solver.cpp:462-475): per iteration a fresh mt19937_64(seed_k) partial
+  // Fisher-Yates over the ascending skeleton rows, the first m kept and sorted.
+  sub_m_ = 0;
+  if (o.subsample > 0.0) {
+    if (skel_rows_.empty()) {
+      for (i64 p = 0; p < g_fine_.size; ++p) {
+        i64 q = p;
+        bool sk = false;
+        for (int a = 0; a < mesh_.dim; ++a) {
+          const int ia = static_cast<int>(q % mesh_.nf[a]);
+          q /= mesh_.nf[a];
+          if ((ia + 1) % mesh_.n[a] == 0) sk = true;
+        }
+        if (sk) skel_rows_.push_back(p);
+      }
+    }
+    const i64 total = static_cast<i64>(skel_rows_.size());
+    i64 m = std::llround(o.subsample * static_cast<double>(total));
+    m = std::min<i64>(std::max<i64>(m, 1), total);
+    sub_m_ = static_cast<int>(m);
+    std::vector<long long> all(static_cast<size_t>(m) * cap);
+    for (int k = 1; k < cap; ++k) {
+      std::vector<long long> rows = skel_rows_;
+      std::mt19937_64 eng(mix_seed(o.rng_seed, static_cast<std::uint64_t>(k)));
+      for (i64 i = 0; i < m; ++i) {
+        const i64 j = i + static_cast<i64>(eng() % static_cast<std::uint64_t>(total - i));
+        std::swap(rows[static_cast<size_t>(i)], rows[static_cast<size_t>(j)]);
+      }
+      std::sort(rows.begin(), rows.begin() + m);
+      std::copy(rows.begin(), rows.begin() + m, all.begin() + static_cast<i64>(m) * k);
+    }
+    if (all.size() > sub_cap_) {
+      sub_rows_ = dev_.alloc<long long>(all.size());
+      sub_cap_ = all.size();
+      if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+      }
+    }
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(sub_rows_, all.data(), all.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  }
+
   static const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
   if (no_graph || s == nullptr) {
     const long long l0 = g_kernel_launches;
@@ -464,7 +511,8 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
   }
   const bool same = graph_exec_ && graph_opts_.tol == o.tol && graph_opts_.max_iter == o.max_iter &&
                     graph_opts_.stagnation_window == o.stagnation_window &&
-                    graph_opts_.stagnation_ratio == o.stagnation_ratio;
+                    graph_opts_.stagnation_ratio == o.stagnation_ratio && graph_opts_.subsample == o.subsample &&
+                    graph_opts_.sparse_residual == o.sparse_residual;
   if (!same) {
     if (graph_exec_) {
       cudaGraphExecDestroy(graph_exec_);
@@ -501,6 +549,7 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   c.stagnation_pow = std::pow(o.stagnation_ratio, o.stagnation_window);
   c.max_iter = o.max_iter;
   c.tol = o.tol;
+  c.subsample = sub_m_ > 0 ? 1 : 0;
 
   smooth_guess(u_[0], s);
   c.op = kCtrlResidualK0;
@@ -511,13 +560,24 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
 
   for (int k = 1; k <= o.max_iter; ++k) {
     error_mode_guess(r_[0], r_[1], k, e_, s);
+    if (sub_m_ > 0)
+      launch_subsample_dots(mesh_.dim, sub_rows_ + static_cast<i64>(sub_m_) * k, sub_m_, e_, r_[0], r_[1], fg_,
+                            st_fine_, partials_, state_, history_, s);
     c.op = kCtrlStep;
     c.k = k;
     launch_march(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
                                         st_fine_, partials_, state_, c, history_), s);
     c.op = kCtrlAccept;
-    launch_march(kMarchUpdate, march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_,
-                                          partials_, state_, c, history_), s);
+    MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_, partials_, state_,
+                              c, history_);
+    set_factors(up, mesh_);
+    up.sparse = o.sparse_residual ? 1 : 0;
+    launch_march(kMarchUpdate, up, s);
+    if (sub_m_ > 0) {  // all-rows retry when the subsampled step grew the residual
+      up.ctrl.op = kCtrlAccept2;
+      up.retry_pass = 1;
+      launch_march(kMarchUpdate, up, s);
+    }
   }
 }
 

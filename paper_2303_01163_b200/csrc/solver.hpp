@@ -20,6 +20,7 @@ struct RunOptions {
   double stagnation_ratio = 0.99;
   double subsample = 0.0;
   std::uint64_t rng_seed = 0;
+  bool sparse_residual = false;
 };
 
 std::uint64_t mix_seed(std::uint64_t base, std::uint64_t k);  // solver.cpp:88-96
@@ -113,6 +114,10 @@ class Solver {
   double* seg1_ = nullptr;
   double* seg2_ = nullptr;
   double* faces3d_ = nullptr;  // 3D fused fill: transformed hole faces
+  std::vector<long long> skel_rows_;  // ascending skeleton rows (subsample > 0), built lazily
+  long long* sub_rows_ = nullptr;     // per-iteration sorted subsets, [k][m]
+  size_t sub_cap_ = 0;
+  int sub_m_ = 0;
   Skel2DArgs skel2d_args(const double* const* sol, const double* u_cc, const int* coin, double* out);
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;

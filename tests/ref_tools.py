@@ -25,13 +25,14 @@ def _meta(prefix):
     return dim, ta, nf, nc
 
 
-def ref_iterate(spec, nf, nc, iters, seed, env=None):
+def ref_iterate(spec, nf, nc, iters, seed, env=None, extra=None):
     with tempfile.TemporaryDirectory() as d:
         prefix = os.path.join(d, "run")
         e = dict(os.environ)
         if env:
             e.update(env)
-        subprocess.check_call([REF_DUMP, "iterate", spec, str(nf), str(nc), str(iters), str(seed), prefix], env=e)
+        subprocess.check_call([REF_DUMP, "iterate", spec, str(nf), str(nc), str(iters), str(seed), prefix]
+                              + list(extra or []), env=e)
         rows = []
         stop = None
         with open(prefix + ".hist.txt") as f:

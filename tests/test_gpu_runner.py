@@ -50,3 +50,34 @@ def test_cli_run_and_errors(tmp_path, capsys):
     assert cli.main(["run", "--config", str(cfgf), "--seed", "1"]) == 0
     out = capsys.readouterr().out.splitlines()
     assert out[0].startswith("k,res_l2") and len(out) == 1 + 4
+
+
+@pytest.mark.parametrize("spec,ex,st,nf,nc,sub,seed", [("ex:1:1", 1, 1, 99, 9, 0.05, 17), ("ex:1:1", 1, 1, 24, 4, 0.3, 3),
+                                                       ("ex:4:1", 4, 1, 24, 4, 0.1, 5)])
+def test_subsample_matches_reference(spec, ex, st, nf, nc, sub, seed):
+    """subsample > 0: the seeded skeleton-row subset for the step length and the all-rows
+    retry (solver.cpp:462-481, 648-657) give the reference's steps and history."""
+    mesh = pb.example_mesh(ex, st, nf, nc)
+    state = pb.asdsm_iterate(pb.make_problem(ex, st), mesh,
+                             pb.IterateOptions(tol=0.0, max_iter=10, stagnation_window=0, subsample=sub, rng_seed=seed))
+    ref = ref_iterate(spec, nf, nc, 10, seed, extra=[str(sub)])
+    got = np.array([h.res_l2 for h in state.history])
+    want = ref["hist"][:, 1]
+    floor = eval_floor(ref_bundle(spec, nf, nc), ref["u"])
+    assert np.all(np.abs(got - want) <= np.maximum(1e-8 * want, 10 * floor))
+    s_got = np.array([h.s_hat for h in state.history[1:]])
+    s_ref = ref["hist"][1:, 5]
+    assert np.array_equal(s_got == 0.0, s_ref == 0.0)
+    assert np.allclose(s_got, s_ref, rtol=1e-6, atol=0)
+
+
+def test_sparse_residual_zero_on_holes():
+    mesh = pb.example_mesh(1, 1, 99, 9)
+    full = pb.asdsm_iterate(pb.make_problem(1, 1), mesh, pb.IterateOptions(tol=0.0, max_iter=5, stagnation_window=0))
+    sp = pb.asdsm_iterate(pb.make_problem(1, 1), mesh,
+                          pb.IterateOptions(tol=0.0, max_iter=5, stagnation_window=0, sparse_residual=True))
+    holes = pb.hole_positions(mesh)
+    assert np.all(sp.r[holes] == 0.0)
+    # test_solver.cpp "skeleton-row residual evaluation tracks the full residual": 1e-6
+    for a, b in zip(full.history, sp.history):
+        assert abs(a.res_l2 - b.res_l2) <= 1e-6 * a.res_l2
