@@ -84,6 +84,12 @@ int asdsm_sample_exact(const asdsm_problem* p, int dim, const int* fine_counts, 
 /* Constant per-axis coefficients alpha[3], beta[3] (spatial axes; time axis ignored). */
 int asdsm_plan_create(int dim, const int* fine_counts, const int* coarse_counts, int time_axis,
                       const double* alpha, const double* beta, asdsm_plan** out);
+/* Plan for a catalogue problem: constant coefficients take the separable fast solvers;
+ * variable coefficients (fdm.hpp:18-30 ProblemSpec with per-point alpha/beta) are sampled on
+ * the host as assemble_operator does (fdm.cpp:63-126) and solved with block Thomas. */
+int asdsm_plan_create_problem(const asdsm_problem* problem, int dim, const int* fine_counts,
+                              const int* coarse_counts, int time_axis, asdsm_plan** out);
+int asdsm_plan_is_variable(const asdsm_plan* plan);
 void asdsm_plan_destroy(asdsm_plan* plan);
 /* MeshConfig::point_count (mesh.hpp:72) for a tensor kind (coarse mask) or the holes kind. */
 int asdsm_point_count(const asdsm_plan* plan, unsigned coarse_mask, int holes, int64_t* out);

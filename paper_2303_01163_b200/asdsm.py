@@ -123,6 +123,8 @@ def load_library():
         "asdsm_sample_exact": (I, [P, I, IP, IP, I, D]),
         "asdsm_plan_create": (I, [I, IP, IP, I, D, D, ctypes.POINTER(P)]),
         "asdsm_plan_destroy": (None, [P]),
+        "asdsm_plan_create_problem": (I, [P, I, IP, IP, I, ctypes.POINTER(P)]),
+        "asdsm_plan_is_variable": (I, [P]),
         "asdsm_point_count": (I, [P, ctypes.c_uint, I, I64]),
         "asdsm_projector_map": (I, [P, ctypes.c_uint, ctypes.c_uint, I, I64]),
         "asdsm_set_bundle": (I, [P, D, ctypes.POINTER(D), D, D, I]),
@@ -384,15 +386,13 @@ class SolverContext:
             raise DimensionMismatch("problem/mesh dimension mismatch")
         if problem.time_dependent != (config.time_axis >= 0):
             raise DimensionMismatch("problem and mesh disagree about a time axis")
-        if not problem.constant_coeffs:
-            raise Unsupported("variable coefficients are not on the B200 path (constant per-axis alpha/beta only)")
         self.config = config
         self.problem = problem
         lib = load_library()
         self._lib = lib
         h = ctypes.c_void_p()
-        _check(lib.asdsm_plan_create(config.dim, _i32(config.fine_counts), _i32(config.coarse_counts),
-                                     config.time_axis, _d3(problem.alpha), _d3(problem.beta), ctypes.byref(h)))
+        _check(lib.asdsm_plan_create_problem(problem._h, config.dim, _i32(config.fine_counts),
+                                             _i32(config.coarse_counts), config.time_axis, ctypes.byref(h)))
         self._h = h
         self.bundle = bundle if bundle is not None else self.assembled_bundle()
         self.exact = problem.sample_exact(config) if problem.has_exact else None
@@ -466,6 +466,10 @@ class SolverContext:
         rows = hist[: nrec.value * 7].reshape(-1, 7)
         history = [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in rows]
         return IterationState(u, r, history, _STOP.get(stop.value, "max_iter"))
+
+    def variable(self) -> bool:
+        """True when the plan runs the variable-coefficient (block-Thomas) path."""
+        return bool(self._lib.asdsm_plan_is_variable(self._h))
 
     def launch_count(self) -> int:
         return int(self._lib.asdsm_last_launch_count(self._h))

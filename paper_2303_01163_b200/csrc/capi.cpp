@@ -154,6 +154,22 @@ int asdsm_plan_create(int dim, const int* fine_counts, const int* coarse_counts,
   });
 }
 
+int asdsm_plan_create_problem(const asdsm_problem* problem, int dim, const int* fine_counts, const int* coarse_counts,
+                              int time_axis, asdsm_plan** out) {
+  return guarded([&] {
+    const Mesh m = mesh_from(dim, fine_counts, coarse_counts, time_axis);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw CudaError("no CUDA device: the B200 path has no CPU fallback");
+    auto plan = std::make_unique<asdsm_plan>();
+    ASDSM_CUDA_CHECK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    plan->solver = std::make_unique<Solver>(m, problem->p);
+    *out = plan.release();
+  });
+}
+
+int asdsm_plan_is_variable(const asdsm_plan* plan) { return plan->solver->variable() ? 1 : 0; }
+
 void asdsm_plan_destroy(asdsm_plan* plan) {
   if (!plan) return;
   if (plan->stream) cudaStreamSynchronize(plan->stream);

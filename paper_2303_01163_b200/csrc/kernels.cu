@@ -640,7 +640,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kRedThreads) subsample_dots_kernel(const long long* rows, int nrows, const double* e,
                                                                       const double* r0, const double* r1, FineGeom g,
                                                                       Stencil st, double* partials, DevState* S,
-                                                                      double* history, CtrlArgs c) {
+                                                                      double* history, CtrlArgs c, const double* coef) {
   if (!S->active) return;
   const double* r = S->cur ? r1 : r0;
   double num = 0.0, den = 0.0;
@@ -651,8 +651,22 @@ __global__ void __launch_bounds__(kRedThreads) subsample_dots_kernel(const long 
       const int i = static_cast<int>(p % g.ext[0]);
       const int j = static_cast<int>((p / g.ext[0]) % g.ext[1]);
       const int k = DIM == 3 ? static_cast<int>(p / (static_cast<i64>(g.ext[0]) * g.ext[1])) : 0;
-      double vp;
-      const double w = apply_row<DIM>(g, st, p, i, j, k, V, vp);
+      double w;
+      if (coef) {  // per-point coefficients, same CSR order
+        const int idx[3] = {i, j, k};
+        double acc = 0.0;
+        int slot = 0;
+        for (int a = DIM - 1; a >= 0; --a, ++slot)
+          if (idx[a] > 0) acc = __dadd_rn(acc, __dmul_rn(coef[slot * g.size + p], e[p - g.stride[a]]));
+        acc = __dadd_rn(acc, __dmul_rn(coef[slot * g.size + p], e[p]));
+        ++slot;
+        for (int a = 0; a < DIM; ++a, ++slot)
+          if (idx[a] < g.ext[a] - 1 && st.has_right[a]) acc = __dadd_rn(acc, __dmul_rn(coef[slot * g.size + p], e[p + g.stride[a]]));
+        w = acc;
+      } else {
+        double vp;
+        w = apply_row<DIM>(g, st, p, i, j, k, V, vp);
+      }
       num += r[p] * w;
       den += w * w;
     }
@@ -665,14 +679,14 @@ __global__ void __launch_bounds__(kRedThreads) subsample_dots_kernel(const long 
 
 void launch_subsample_dots(int dim, const long long* rows, int nrows, const double* e, const double* r0,
                            const double* r1, const FineGeom& g, const Stencil& st, double* partials,
-                           DevState* state, double* history, cudaStream_t s) {
+                           DevState* state, double* history, cudaStream_t s, const double* coef) {
   CtrlArgs c{};
   c.op = kCtrlSubDots;
   const unsigned nb = static_cast<unsigned>(std::max(1, std::min((nrows + 255) / 256, kRedBlocks)));
   if (dim == 2)
-    subsample_dots_kernel<2><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c);
+    subsample_dots_kernel<2><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c, coef);
   else
-    subsample_dots_kernel<3><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c);
+    subsample_dots_kernel<3><<<nb, kRedThreads, 0, s>>>(rows, nrows, e, r0, r1, g, st, partials, state, history, c, coef);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

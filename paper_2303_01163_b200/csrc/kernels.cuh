@@ -128,7 +128,7 @@ void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, con
 // folded into kCtrlSubDots.
 void launch_subsample_dots(int dim, const long long* rows, int nrows, const double* e, const double* r0,
                            const double* r1, const FineGeom& g, const Stencil& st, double* partials,
-                           DevState* state, double* history, cudaStream_t s);
+                           DevState* state, double* history, cudaStream_t s, const double* coef = nullptr);
 
 // Dense coarse solve x = Ainv b (small), single CTA.
 void launch_dense_matvec(const double* Ainv, const double* b, double* x, int n, DevState* state, cudaStream_t s);

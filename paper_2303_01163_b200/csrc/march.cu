@@ -32,7 +32,7 @@ struct Src {
   }
 };
 
-template <int MODE>
+template <int MODE, bool VAR>
 __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
@@ -97,12 +97,14 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
       if (t == TX2 - 1 || x == Nx - 1) row[buf][t + 2] = hR;
       __syncthreads();
       if (in) {
+        const i64 N = A.g.size;
+        auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
         double acc = 0.0;
-        if (y > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], vd));
-        if (x > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], row[buf][t]));
-        acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
-        if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], row[buf][t + 2]));
-        if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], vu));
+        if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[1]), vd));
+        if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[0]), row[buf][t]));
+        acc = __dadd_rn(acc, __dmul_rn(C(2, st.diag), vc));
+        if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(3, st.right[0]), row[buf][t + 2]));
+        if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[1]), vu));
         if (MODE == kMarchDots) {
           a0 += rq * acc;
           a2 += acc * acc;
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
-template <int MODE>
+template <int MODE, bool VAR>
 __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
@@ -213,14 +215,16 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
       if (ty == TY3 - 1 || y == Ny - 1) pl[buf][ty + 2][tx + 1] = hYR;
       __syncthreads();
       if (in) {
+        const i64 N = A.g.size;
+        auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
         double acc = 0.0;
-        if (z > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[2], vd));
-        if (y > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], pl[buf][ty][tx + 1]));
-        if (x > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], pl[buf][ty + 1][tx]));
-        acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
-        if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], pl[buf][ty + 1][tx + 2]));
-        if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], pl[buf][ty + 2][tx + 1]));
-        if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(st.right[2], vu));
+        if (z > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[2]), vd));
+        if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[1]), pl[buf][ty][tx + 1]));
+        if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(2, st.left[0]), pl[buf][ty + 1][tx]));
+        acc = __dadd_rn(acc, __dmul_rn(C(3, st.diag), vc));
+        if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[0]), pl[buf][ty + 1][tx + 2]));
+        if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(5, st.right[1]), pl[buf][ty + 2][tx + 1]));
+        if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(C(6, st.right[2]), vu));
         if (MODE == kMarchDots) {
           a0 += rq * acc;
           a2 += acc * acc;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
 constexpr int ZC = 8;
-template <int MODE>
+template <int MODE, bool VAR>
 __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
@@ -303,15 +307,17 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
       const int z = z0 + q;
       if (z >= Nz) break;
       const i64 p = pxy + z * sz;
+      const i64 N = A.g.size;
+      auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
       double acc = 0.0;
-      if (z > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[2], vz[q]));
-      if (y > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], V(p - sy)));
-      if (x > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], V(p - 1)));
+      if (z > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[2]), vz[q]));
+      if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[1]), V(p - sy)));
+      if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(2, st.left[0]), V(p - 1)));
       const double vc = vz[q + 1];
-      acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
-      if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], V(p + 1)));
-      if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], V(p + sy)));
-      if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(st.right[2], vz[q + 2]));
+      acc = __dadd_rn(acc, __dmul_rn(C(3, st.diag), vc));
+      if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[0]), V(p + 1)));
+      if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(5, st.right[1]), V(p + sy)));
+      if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(C(6, st.right[2]), vz[q + 2]));
       if (MODE == kMarchDots) {
         const double rp = __ldg(rcur + p);
         a0 += rp * acc;
@@ -369,22 +375,30 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   A.strip = march_strip(A.g);
   const unsigned nb = march_blocks(A.g);
   if (nb > static_cast<unsigned>(kRedStride)) throw AsdsmError(kUnsupported, "fine grid too large for the partial buffer");
+  const bool var = A.coef != nullptr;
+#define ASDSM_MARCH_DISPATCH(KERNEL, GRID, BLOCK)                                        \
+  do {                                                                                  \
+    if (var) {                                                                          \
+      if (mode == kMarchResidual) KERNEL<kMarchResidual, true><<<GRID, BLOCK, 0, s>>>(A); \
+      else if (mode == kMarchUpdate) KERNEL<kMarchUpdate, true><<<GRID, BLOCK, 0, s>>>(A); \
+      else KERNEL<kMarchDots, true><<<GRID, BLOCK, 0, s>>>(A);                         \
+    } else {                                                                            \
+      if (mode == kMarchResidual) KERNEL<kMarchResidual, false><<<GRID, BLOCK, 0, s>>>(A); \
+      else if (mode == kMarchUpdate) KERNEL<kMarchUpdate, false><<<GRID, BLOCK, 0, s>>>(A); \
+      else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
+    }                                                                                   \
+  } while (0)
   if (A.g.dim == 2) {
-    if (mode == kMarchResidual) march2d_kernel<kMarchResidual><<<nb, TX2, 0, s>>>(A);
-    else if (mode == kMarchUpdate) march2d_kernel<kMarchUpdate><<<nb, TX2, 0, s>>>(A);
-    else march2d_kernel<kMarchDots><<<nb, TX2, 0, s>>>(A);
+    ASDSM_MARCH_DISPATCH(march2d_kernel, nb, TX2);
   } else if (std::getenv("ASDSM_MARCH3D") == nullptr && mode != kMarchUpdate) {
     // measured (config 3/4): the barrier-free z-coarsened pass streams the residual and the
     // dot-product passes faster; the smem-plane march is faster for the 5-array update pass
     const unsigned nbz = 8 * kNumSms;
-    if (mode == kMarchResidual) stencil3d_zc_kernel<kMarchResidual><<<nbz, 256, 0, s>>>(A);
-    else if (mode == kMarchUpdate) stencil3d_zc_kernel<kMarchUpdate><<<nbz, 256, 0, s>>>(A);
-    else stencil3d_zc_kernel<kMarchDots><<<nbz, 256, 0, s>>>(A);
+    ASDSM_MARCH_DISPATCH(stencil3d_zc_kernel, nbz, 256);
   } else {
-    if (mode == kMarchResidual) march3d_kernel<kMarchResidual><<<nb, TX3 * TY3, 0, s>>>(A);
-    else if (mode == kMarchUpdate) march3d_kernel<kMarchUpdate><<<nb, TX3 * TY3, 0, s>>>(A);
-    else march3d_kernel<kMarchDots><<<nb, TX3 * TY3, 0, s>>>(A);
+    ASDSM_MARCH_DISPATCH(march3d_kernel, nb, TX3 * TY3);
   }
+#undef ASDSM_MARCH_DISPATCH
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

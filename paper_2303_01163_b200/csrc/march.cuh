@@ -27,6 +27,7 @@ struct MarchArgs {
   int retry_pass;  // UPDATE: the all-rows retry of a subsampled step (runs only if state->retry)
   int sparse;      // UPDATE: sparse_residual -- hole rows get r = 0 (solver.cpp:638-643)
   int n[3];        // refinement factors (hole-row test for sparse)
+  const double* coef;  // variable coefficients: coef[slot * N + p] in CSR column order, or null
 };
 
 int march_strip(const FineGeom& g);

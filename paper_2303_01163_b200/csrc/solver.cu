@@ -33,6 +33,31 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
     alpha_[a] = alpha[a];
     beta_[a] = beta[a];
   }
+  init(nullptr);
+}
+
+Solver::Solver(const Mesh& m, const asdsm_cat::Problem& problem) : mesh_(m) {
+  if (problem.dim != m.dim) throw AsdsmError(kDimensionMismatch, "problem/mesh dimension mismatch");
+  if (problem.time_dependent != (m.time_axis >= 0))
+    throw AsdsmError(kDimensionMismatch, "problem and mesh disagree about a time axis");
+  if (problem.constant_coeffs) {
+    for (int a = 0; a < 3; ++a) {
+      alpha_[a] = problem.alpha_c[static_cast<size_t>(a)];
+      beta_[a] = problem.beta_c[static_cast<size_t>(a)];
+    }
+    init(nullptr);
+    return;
+  }
+  for (int a = 0; a < 3; ++a) {  // stencil structure only (has_right, time axis); values per point
+    alpha_[a] = 1.0;
+    beta_[a] = 0.0;
+  }
+  init(&problem);
+}
+
+void Solver::init(const asdsm_cat::Problem* varprob) {
+  const Mesh& m = mesh_;
+  variable_ = varprob != nullptr;
   md_.dim = m.dim;
   for (int a = 0; a < 3; ++a) {
     md_.nf[a] = a < m.dim ? m.nf[a] : 1;
@@ -60,16 +85,44 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
 
   // Separable solvers: slabs (one box each), coarse box, hole boxes (all congruent).
   const int tax = m.time_axis;
-  for (int a = 0; a < m.dim; ++a)
-    sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
-  sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
   int hext[3] = {1, 1, 1};
   i64 nholes = 1;
   for (int a = 0; a < m.dim; ++a) {
     hext[a] = m.n[a] - 1;
     nholes *= m.nc[a] + 1;
   }
-  sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block");
+  if (!variable_) {
+    for (int a = 0; a < m.dim; ++a)
+      sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
+    sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
+    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block");
+  } else {
+    // per-point stencils (fdm.cpp:63-126 sampling) + block-Thomas factors for every box
+    const std::vector<double> cf = sample_kind_coefficients(m, 0u, *varprob);
+    coef_fine_ = dev_.alloc<double>(cf.size());
+    ASDSM_CUDA_CHECK(cudaMemcpy(coef_fine_, cf.data(), cf.size() * sizeof(double), cudaMemcpyHostToDevice));
+    auto upload_bt = [&](const BlockThomas& b, BTDev& d) {
+      d.dim = b.dim;
+      d.L = b.L;
+      d.B = b.B;
+      d.nb = b.nb;
+      for (int a = 0; a < 3; ++a) d.ext[a] = b.ext[a];
+      double* p0 = dev_.alloc<double>(b.dinv.size());
+      double* p1 = dev_.alloc<double>(b.lo.size());
+      double* p2 = dev_.alloc<double>(b.up.size());
+      ASDSM_CUDA_CHECK(cudaMemcpy(p0, b.dinv.data(), b.dinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+      ASDSM_CUDA_CHECK(cudaMemcpy(p1, b.lo.data(), b.lo.size() * sizeof(double), cudaMemcpyHostToDevice));
+      ASDSM_CUDA_CHECK(cudaMemcpy(p2, b.up.data(), b.up.size() * sizeof(double), cudaMemcpyHostToDevice));
+      d.dinv = p0;
+      d.lo = p1;
+      d.up = p2;
+    };
+    for (int a = 0; a < m.dim; ++a)
+      upload_bt(factor_kind_box(m, 1u << a, sample_kind_coefficients(m, 1u << a, *varprob), tax), bt_[a]);
+    const unsigned full_mask = (1u << m.dim) - 1u;
+    upload_bt(factor_kind_box(m, full_mask, sample_kind_coefficients(m, full_mask, *varprob), tax), bt_[3]);
+    upload_bt(factor_hole_boxes(m, cf), bt_[4]);
+  }
 
   const i64 nf = g_fine_.size;
   for (int i = 0; i < 2; ++i) {
@@ -79,15 +132,15 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   b_ = dev_.alloc<double>(static_cast<size_t>(nf));
   e_ = dev_.alloc<double>(static_cast<size_t>(nf));
   exact_ = dev_.alloc<double>(static_cast<size_t>(nf));
-  size_t scratch = sep_scratch_bytes(sep_hole_, nholes);
+  size_t scratch = variable_ ? 16 : sep_scratch_bytes(sep_hole_, nholes);
   for (int a = 0; a < m.dim; ++a) {
     const size_t n = static_cast<size_t>(g_slab_[a].size);
     b_slab_[a] = dev_.alloc<double>(n);
     rhs_slab_[a] = dev_.alloc<double>(n);
     sol_slab_[a] = dev_.alloc<double>(n);
-    scratch = std::max(scratch, sep_scratch_bytes(sep_slab_[a], 1));
+    if (!variable_) scratch = std::max(scratch, sep_scratch_bytes(sep_slab_[a], 1));
   }
-  scratch = std::max(scratch, sep_scratch_bytes(sep_coarse_, 1));
+  if (!variable_) scratch = std::max(scratch, sep_scratch_bytes(sep_coarse_, 1));
   scratch0_ = dev_.alloc<unsigned char>(scratch);
   scratch1_ = dev_.alloc<unsigned char>(scratch);
   b_coarse_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
@@ -122,7 +175,7 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
     }
   }
   partials_ = dev_.alloc<double>(4 * static_cast<size_t>(kRedStride));
-  if (m.dim == 3) {  // 3D fused fill buffers (allocated here: never during graph capture)
+  if (m.dim == 3 && !variable_) {  // 3D fused fill buffers (allocated here: never during graph capture)
     Hole3DArgs A{};
     for (int a = 0; a < 3; ++a) A.m[a] = m.n[a] - 1;
     faces3d_ = dev_.alloc<double>(static_cast<size_t>(nholes) * hole3d_face_doubles(A));
@@ -130,7 +183,7 @@ Solver::Solver(const Mesh& m, const double* alpha, const double* beta) : mesh_(m
   }
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
-  if (m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
+  if (!variable_ && m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
     fast2d_ = true;
     for (int a = 0; a < 2; ++a) {
       const SepSolver& S = sep_slab_[a];
@@ -251,7 +304,23 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
   launch_skeleton2d(a, state_, s);
 }
 
+void Solver::march_launch(int mode, MarchArgs A, cudaStream_t s) {
+  A.coef = coef_fine_;
+  launch_march(mode, A, s);
+}
+
+void Solver::solve_box(int which, double* data, cudaStream_t s) {
+  const BoxArray arr = which < 3 ? kind_array(g_slab_[which], data) : which == 3 ? kind_array(g_coarse_, data)
+                                                                                  : hole_array(data);
+  launch_block_thomas(bt_[which], arr, state_, s);
+}
+
 void Solver::fill(double* e, const double* b, cudaStream_t s) {
+  if (variable_) {
+    launch_hole_rhs_var(mesh_.dim, e, b, fg_, coef_fine_, md_, state_, s);
+    solve_box(4, e, s);
+    return;
+  }
   static const bool generic = std::getenv("ASDSM_GENERIC_FILL") != nullptr;
   const SepSolver& H = sep_hole_;
   if (!generic && mesh_.dim == 2 && b == nullptr && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
@@ -331,6 +400,7 @@ static MarchArgs march_args(const double* u0, const double* u1, const double* e,
                             const Stencil& st, double* partials, DevState* state, const CtrlArgs& c,
                             double* history) {
   MarchArgs A{};
+  A.coef = nullptr;
   A.u0 = u0;
   A.u1 = u1;
   A.e = e;
@@ -348,6 +418,7 @@ static MarchArgs march_args(const double* u0, const double* u1, const double* e,
   A.state = state;
   A.ctrl = c;
   A.history = history;
+  A.coef = nullptr;
   return A;
 }
 
@@ -374,6 +445,20 @@ static Slab2DArgs slab2d_args(const MeshDev& md, const SepSolver* S, double* con
 
 // Alg. 1 with the assembled bundle (solver.cpp:518-548, smooth mode).
 void Solver::smooth_guess(double* out, cudaStream_t s) {
+  if (variable_) {
+    for (int a = 0; a < mesh_.dim; ++a) {
+      ASDSM_CUDA_CHECK(cudaMemcpyAsync(sol_slab_[a], b_slab_[a], static_cast<size_t>(g_slab_[a].size) * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s));
+      solve_box(a, sol_slab_[a], s);
+    }
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_cc_, b_coarse_, static_cast<size_t>(g_coarse_.size) * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+    solve_box(3, u_cc_, s);
+    const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
+    skeleton(sol, u_cc_, nullptr, out, s);
+    fill(out, b_, s);
+    return;
+  }
   if (fast2d_) {
     Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
     A.in_slab[0] = b_slab_[0];
@@ -411,6 +496,11 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
     return;
   }
   for (int a = 0; a < mesh_.dim; ++a) {
+    if (variable_) {
+      launch_gather(r0, r1, sol_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
+      solve_box(a, sol_slab_[a], s);
+      continue;
+    }
     launch_gather(r0, r1, rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
     sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
               scratch1_, s);
@@ -555,28 +645,28 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   c.op = kCtrlResidualK0;
   c.k = 0;
   const double* ex = has_exact_ ? exact_ : nullptr;
-  launch_march(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], ex, fg_, st_fine_,
+  march_launch(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], ex, fg_, st_fine_,
                                           partials_, state_, c, history_), s);
 
   for (int k = 1; k <= o.max_iter; ++k) {
     error_mode_guess(r_[0], r_[1], k, e_, s);
     if (sub_m_ > 0)
       launch_subsample_dots(mesh_.dim, sub_rows_ + static_cast<i64>(sub_m_) * k, sub_m_, e_, r_[0], r_[1], fg_,
-                            st_fine_, partials_, state_, history_, s);
+                            st_fine_, partials_, state_, history_, s, coef_fine_);
     c.op = kCtrlStep;
     c.k = k;
-    launch_march(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+    march_launch(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
                                         st_fine_, partials_, state_, c, history_), s);
     c.op = kCtrlAccept;
     MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_, partials_, state_,
                               c, history_);
     set_factors(up, mesh_);
     up.sparse = o.sparse_residual ? 1 : 0;
-    launch_march(kMarchUpdate, up, s);
+    march_launch(kMarchUpdate, up, s);
     if (sub_m_ > 0) {  // all-rows retry when the subsampled step grew the residual
       up.ctrl.op = kCtrlAccept2;
       up.retry_pass = 1;
-      launch_march(kMarchUpdate, up, s);
+      march_launch(kMarchUpdate, up, s);
     }
   }
 }
@@ -619,7 +709,7 @@ void Solver::residual(const double* u, const double* b, double* r, cudaStream_t 
   launch_state_init(state_, 1, 1, s);
   CtrlArgs c{};
   c.op = -1;
-  launch_march(kMarchResidual, march_args(u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_,
+  march_launch(kMarchResidual, march_args(u, u, nullptr, b, nullptr, nullptr, r, r, nullptr, fg_, st_fine_, partials_,
                                           state_, c, nullptr), s);
 }
 
@@ -657,7 +747,7 @@ double Solver::optimal_scaling(const double* r, const double* e, cudaStream_t s)
   }
   CtrlArgs c{};
   c.op = kCtrlStep;
-  launch_march(kMarchDots, march_args(nullptr, nullptr, e, nullptr, nullptr, nullptr, const_cast<double*>(r),
+  march_launch(kMarchDots, march_args(nullptr, nullptr, e, nullptr, nullptr, nullptr, const_cast<double*>(r),
                                       const_cast<double*>(r), nullptr, fg_, st_fine_, partials_, state_, c, history_), s);
   DevState back{};
   ASDSM_CUDA_CHECK(cudaMemcpyAsync(&back, state_, sizeof(back), cudaMemcpyDeviceToHost, s));
@@ -704,7 +794,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   auto set_step = [&]() {
     CtrlArgs c{};
     c.op = kCtrlStep;
-    launch_march(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+    march_launch(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
                                         st_fine_, partials_, state_, c, history_), s);
   };
   const double ex = has_exact_ ? 1.0 : 0.0;
@@ -716,7 +806,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     launch_ctrl(cs, partials_, state_, history_, s);
     CtrlArgs c{};
     c.op = -1;
-    launch_march(kMarchUpdate, march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr,
+    march_launch(kMarchUpdate, march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr,
                                           fg_, st_fine_, partials_, state_, c, history_), s);
   });
   // the update-pass time alone: subtract the state-init + set-step part measured alone
@@ -775,7 +865,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   timed("residual", 8.0 * N * 3.0, 0.0, 1, [&] {
     CtrlArgs c{};
     c.op = -1;
-    launch_march(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+    march_launch(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
                                             st_fine_, partials_, state_, c, history_), s);
   });
   cudaEventDestroy(e0);

@@ -7,8 +7,11 @@
 
 #include "kernels.cuh"
 #include "merge3d.cuh"
+#include "march.cuh"
 #include "plan.hpp"
 #include "sepsolve.cuh"
+#include "varcoef.hpp"
+#include "vthomas.cuh"
 
 namespace asdsm_b200 {
 
@@ -28,6 +31,10 @@ std::uint64_t mix_seed(std::uint64_t base, std::uint64_t k);  // solver.cpp:88-9
 class Solver {
  public:
   Solver(const Mesh& m, const double* alpha, const double* beta);
+  // Variable coefficients (ProblemSpec with per-point alpha/beta): per-point stencils and
+  // block-Thomas direct solves.
+  Solver(const Mesh& m, const asdsm_cat::Problem& problem);
+  bool variable() const { return variable_; }
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
 
@@ -84,7 +91,13 @@ class Solver {
   BoxArray hole_array(double* p) const;
   BoxArray kind_array(const KindGeom& g, double* p) const;
 
+  void init(const asdsm_cat::Problem* varprob);
+  void solve_box(int which, double* data, cudaStream_t s);
+  void march_launch(int mode, struct MarchArgs A, cudaStream_t s);  // variable mode: 0..2 slab, 3 coarse, 4 holes
   Mesh mesh_;
+  bool variable_ = false;
+  double* coef_fine_ = nullptr;
+  BTDev bt_[5]{};
   double alpha_[3] = {0, 0, 0}, beta_[3] = {0, 0, 0};
   MeshDev md_{};
   KindGeom g_fine_, g_slab_[3], g_coarse_;

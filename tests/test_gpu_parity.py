@@ -136,3 +136,25 @@ def test_initial_guess_3d(spec, nf, nc):
 ])
 def test_iterate_history_3d(spec, nf, nc, iters, seed):
     test_iterate_history(spec, nf, nc, iters, seed)
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("ex:1:2", 24, 4, 10), ("ex:1:2", 99, 9, 20), ("ex:3:2", 99, 9, 20),
+                                              ("ex:4:2", 24, 4, 5)])
+def test_variable_coefficients_match_reference(spec, nf, nc, iters):
+    """Reference examples with variable alpha/beta (setting 2): per-point stencils and
+    block-Thomas direct solves on the device."""
+    ctx, mesh, prob = _ctx(spec, nf, nc)
+    assert not prob.constant_coeffs and ctx.variable()
+    bun = ref_bundle(spec, nf, nc)
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal(ctx.fine_size())
+    assert np.array_equal(ctx.residual(u), csr_residual_exact(bun, u))  # per-point stencil, bitwise
+    ref = ref_iterate(spec, nf, nc, iters, 0)
+    st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=0))
+    got = np.array([h.res_l2 for h in st.history])
+    want = ref["hist"][:, 1]
+    tol = np.maximum(want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, 0, ref)), eval_floor(bun, ref["u"]))
+    bad = np.abs(got - want) > tol
+    assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
+    assert np.array_equal(np.array([h.s_hat for h in st.history[1:]]) == 0.0, ref["hist"][1:, 5] == 0.0)
+    assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * np.max(np.abs(ref["u"]))
