@@ -254,17 +254,9 @@ def main():
              "gbs": cby[i] / (cms[i] / 1e3) / 1e9 if cms[i] > 0 else None,
              "tflops": cfl[i] / (cms[i] / 1e3) / 1e12 if cms[i] > 0 and cfl[i] > 0 else None}
         comps.append(c)
-    # dominant single kernel: hole_fill is the composite fwd+Thomas+back; in 2D its dense part
-    # is reported separately as hole_backtransform_dmma.
-    cand = [c for c in comps if c["name"] not in ("hole_fill", "step_dots", "residual")]
-    if any(c["name"] == "hole_backtransform_dmma" for c in comps):
-        hf = next(c for c in comps if c["name"] == "hole_fill")
-        hb = next(c for c in comps if c["name"] == "hole_backtransform_dmma")
-        cand.append({"name": "hole_fwd_thomas", "ms_per_launch": hf["ms_per_launch"] - hb["ms_per_launch"],
-                     "launches_per_solve": hf["launches_per_solve"], "bytes_per_launch": 8.0 * 3 * ctx.config.point_count(
-                         pb.MeshKind.holes_of(mesh.dim)), "flops_per_launch": 0.0})
-    else:
-        cand.append(next(c for c in comps if c["name"] == "hole_fill"))
+    # dominant kernel of the solve (the components are the individual kernels of one iteration;
+    # on the generic/3D path hole_fill / slab_solves / skeleton_merge are kernel groups)
+    cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
     dom = max(cand, key=lambda c: c["ms_per_launch"] * c["launches_per_solve"])
     if dom["flops_per_launch"] > 0 and dom["flops_per_launch"] / max(dom["bytes_per_launch"], 1) > FP64_PEAK_TFLOPS * 1e3 / hbm:
         ach = dom["flops_per_launch"] / (dom["ms_per_launch"] / 1e3) / 1e12

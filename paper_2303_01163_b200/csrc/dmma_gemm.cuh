@@ -15,6 +15,7 @@ struct GemmLines {
 };
 
 // in_es / out_es: element stride along the transform axis for input / output.
+void dmma_prepare();  // kernel attributes (call before any stream capture)
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s);
 

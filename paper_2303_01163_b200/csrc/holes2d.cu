@@ -81,7 +81,7 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
   double* out = modes + static_cast<i64>(hole) * m0 * m1;
   // forward sweep, pivots prefetched 8 rows ahead; y parked in smem or the mode buffer
   double y = 0.0;
-  constexpr int U = 8;
+  constexpr int U = 24;
   double ivn[U];
 #pragma unroll
   for (int q = 0; q < U; ++q) ivn[q] = q < m1 ? __ldg(ipiv + static_cast<i64>(q) * m0 + k) : 0.0;

@@ -183,6 +183,7 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   }
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
+  dmma_prepare();
   if (!variable_ && m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
     fast2d_ = true;
     for (int a = 0; a < 2; ++a) {
@@ -821,10 +822,39 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   out.pop_back();
   timed("step_dots", 8.0 * N * 2.0, 0.0, iters, [&] { set_step(); });
   const SepSolver& H = sep_hole_;
-  double hflops = 0;
-  for (int i = 0; i < H.nd; ++i) hflops += 2.0 * 2.0 * H.ext[H.dax[i]] * static_cast<double>(NH);
-  timed("hole_fill", 8.0 * NH * 3.0, hflops, iters, [&] { fill(e_, nullptr, s); });
-  if (mesh_.dim == 2 && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
+  i64 slab_pts = 0;
+  for (int a = 0; a < mesh_.dim; ++a) slab_pts += g_slab_[a].size;
+  if (fast2d_) {
+    // the kernels of one fast-path iteration, each timed alone
+    Slab2DArgs SA = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
+    SA.in_fine0 = r_[0];
+    SA.in_fine1 = r_[1];
+    const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
+    const Skel2DArgs sk = skel2d_args(sol, nullptr, coins_, e_);
+    const double cb = sep_slab_[0].complex_modes ? 16.0 : 8.0;
+    timed("slab2d_fwd_pcr", (8.0 + cb) * slab_pts, 0.0, iters, [&] { launch_slab2d_fwd(SA, state_, s); });
+    timed("slab2d_back_norms_ccspline", (8.0 + cb) * slab_pts, 0.0, iters,
+          [&] { launch_slab2d_back(SA, partials_, state_, history_, true, s, &sk); });
+    const i64 nskel = static_cast<i64>(mesh_.nc[1]) * mesh_.nf[0] + static_cast<i64>(mesh_.nc[0]) * mesh_.nf[1];
+    timed("skeleton_write", 16.0 * nskel, 0.0, iters, [&] { launch_skel2d_write_fast(sk, state_, s); });
+    Hole2DArgs A{};
+    A.m0 = H.ext[0];
+    A.m1 = H.ext[1];
+    A.n0 = mesh_.n[0];
+    A.n1 = mesh_.n[1];
+    A.nf0 = mesh_.nf[0];
+    A.nf1 = mesh_.nf[1];
+    A.nbox0 = mesh_.nc[0] + 1;
+    A.nbox1 = mesh_.nc[1] + 1;
+    A.kb = 64;
+    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
+    A.st = st_fine_;
+    A.Wt = H.Wt[0];
+    A.ipiv = H.th_ipiv;
+    A.cp = H.th_cp;
+    A.line_left = H.line_left;
+    timed("hole2d_fwd_thomas", 8.0 * NH * (A.y_in_smem ? 1.0 : 3.0), 0.0, iters,
+          [&] { launch_hole2d_fwd_thomas(e_, static_cast<double*>(scratch0_), A, state_, s); });
     GemmLines G{};
     G.o_ext[0] = H.ext[1];
     G.o_ext[1] = 1;
@@ -840,28 +870,27 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     G.nlines = static_cast<i64>(H.ext[1]) * G.nbox[0] * G.nbox[1];
     timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
           [&] { launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s); });
+  } else {
+    double hflops = 0;
+    if (!variable_)
+      for (int i = 0; i < H.nd; ++i) hflops += 2.0 * H.ext[H.dax[i]] * static_cast<double>(NH);
+    timed("hole_fill", 8.0 * NH * 3.0, hflops, iters, [&] { fill(e_, nullptr, s); });
+    timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
+      for (int a = 0; a < mesh_.dim; ++a) {
+        launch_gather(r_[0], r_[1], rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
+        if (variable_) {
+          solve_box(a, rhs_slab_[a], s);
+          continue;
+        }
+        sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
+                  scratch1_, s);
+      }
+    });
+    timed("skeleton_merge", 8.0 * slab_pts * 2.0, 0.0, iters, [&] {
+      const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
+      skeleton(sol, nullptr, coins_, e_, s);
+    });
   }
-  i64 slab_pts = 0;
-  for (int a = 0; a < mesh_.dim; ++a) slab_pts += g_slab_[a].size;
-  timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
-    if (fast2d_) {
-      Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
-      A.in_fine0 = r_[0];
-      A.in_fine1 = r_[1];
-      launch_slab2d_fwd(A, state_, s);
-      launch_slab2d_back(A, partials_, state_, history_, true, s);
-      return;
-    }
-    for (int a = 0; a < mesh_.dim; ++a) {
-      launch_gather(r_[0], r_[1], rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
-      sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
-                scratch1_, s);
-    }
-  });
-  timed("skeleton_merge", 8.0 * slab_pts * 2.0, 0.0, iters, [&] {
-    const double* sol[3] = {sol_slab_[0], sol_slab_[1], sol_slab_[2]};
-    skeleton(sol, nullptr, coins_, e_, s);
-  });
   timed("residual", 8.0 * N * 3.0, 0.0, 1, [&] {
     CtrlArgs c{};
     c.op = -1;
