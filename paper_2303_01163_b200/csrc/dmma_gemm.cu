@@ -29,16 +29,12 @@ __device__ __forceinline__ void line_base(const GemmLines& L, i64 p, i64& ib, i6
   ob = h0 * L.out_bs[0] + h1 * L.out_bs[1] + h2 * L.out_bs[2] + o0 * L.o_out[0] + o1 * L.o_out[1];
 }
 
-// 3-stage cp.async pipeline: tiles land in shared memory asynchronously (no register
-// staging), stage k+2 is in flight while stage k feeds the DMMAs.
-constexpr int NSTAGE = 3;
-constexpr int STAGE_DOUBLES = (BP + BQ) * (BK + PAD);
-
 template <bool kContigIn, bool kContigOut>
 __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                              const double* __restrict__ M, int m, i64 in_es, i64 out_es,
                                                              GemmLines L) {
-  extern __shared__ double smem_d[];
+  __shared__ double As[BP][BK + PAD];
+  __shared__ double Bs[BQ][BK + PAD];
   __shared__ i64 s_ib[BP], s_ob[BP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const i64 p0 = static_cast<i64>(blockIdx.y) * BP;  // grid = (q tiles, line blocks)
@@ -57,14 +53,8 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int wp = (warp >> 1) * 32, wq = (warp & 1) * 32;
   constexpr int PER = (BP * BK) / NTH;  // 16
-  const int nk = (m + BK - 1) / BK;
-  auto As = [&](int st, int p, int k) -> double& { return smem_d[st * STAGE_DOUBLES + p * (BK + PAD) + k]; };
-  auto Bs = [&](int st, int q, int k) -> double& {
-    return smem_d[st * STAGE_DOUBLES + BP * (BK + PAD) + q * (BK + PAD) + k];
-  };
-  auto issue = [&](int kt) {
-    const int st = kt % NSTAGE;
-    const int k0 = kt * BK;
+  double ra[PER], rb[PER];
+  auto load = [&](int k0) {
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
       const int e = tid + r * NTH;
@@ -77,38 +67,39 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
         kl = e / BP;
       }
       const int k = k0 + kl;
-      if (p0 + pl < L.nlines && k < m) cp_async8(&As(st, pl, kl), in + s_ib[pl] + static_cast<i64>(k) * in_es);
-      else As(st, pl, kl) = 0.0;
+      ra[r] = (p0 + pl < L.nlines && k < m) ? __ldg(in + s_ib[pl] + static_cast<i64>(k) * in_es) : 0.0;
       const int ql = e / BK, kq = e % BK;
-      if (q0 + ql < m && k0 + kq < m) cp_async8(&Bs(st, ql, kq), M + static_cast<i64>(q0 + ql) * m + k0 + kq);
-      else Bs(st, ql, kq) = 0.0;
+      rb[r] = (q0 + ql < m && k0 + kq < m) ? __ldg(M + static_cast<i64>(q0 + ql) * m + k0 + kq) : 0.0;
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  for (int kt = 0; kt < NSTAGE - 1; ++kt) {
-    if (kt < nk) issue(kt);
-    else asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(NSTAGE - 2) : "memory");
+  auto store = [&]() {
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int e = tid + r * NTH;
+      if (kContigIn) As[e / BK][e % BK] = ra[r];
+      else As[e % BP][e / BP] = ra[r];
+      Bs[e / BK][e % BK] = rb[r];
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < m; k0 += BK) {
+    store();
     __syncthreads();
-    if (kt + NSTAGE - 1 < nk) issue(kt + NSTAGE - 1);
-    else asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const int st = kt % NSTAGE;
+    if (k0 + BK < m) load(k0 + BK);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As(st, wp + i * 8 + (lane >> 2), kk + (lane & 3));
+      for (int i = 0; i < 4; ++i) a[i] = As[wp + i * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs(st, wq + j * 8 + (lane >> 2), kk + (lane & 3));
+      for (int j = 0; j < 4; ++j) b[j] = Bs[wq + j * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
     }
+    __syncthreads();
   }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int pl = wp + i * 8 + (lane >> 2);
@@ -135,16 +126,8 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
 
 }  // namespace
 
-void dmma_prepare() {
-  const size_t smem = sizeof(double) * NSTAGE * STAGE_DOUBLES;
-  static bool attr = false;
-  if (attr) return;
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_transform_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_transform_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_transform_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_transform_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  attr = true;
-}
+void dmma_prepare() {}  // the register-staged kernel needs no attributes (a 3-stage cp.async
+                        // variant measured slower on both m=102 and m=409 and was dropped)
 
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s) {
@@ -152,14 +135,12 @@ void launch_dmma_transform(const double* in, double* out, const double* M, int m
   const i64 pb = (L.nlines + BP - 1) / BP;
   const unsigned qb = static_cast<unsigned>((m + BQ - 1) / BQ);
   if (pb > 65535) throw AsdsmError(kUnsupported, "transform batch too large for the grid");
-  const dim3 grid(qb, static_cast<unsigned>(pb));
+  dim3 grid(qb, static_cast<unsigned>(pb));
   const bool ci = in_es == 1, co = out_es == 1;
-  const size_t smem = sizeof(double) * NSTAGE * STAGE_DOUBLES;
-  dmma_prepare();
-  if (ci && co) dmma_transform_kernel<true, true><<<grid, NTH, smem, s>>>(in, out, M, m, in_es, out_es, L);
-  else if (ci) dmma_transform_kernel<true, false><<<grid, NTH, smem, s>>>(in, out, M, m, in_es, out_es, L);
-  else if (co) dmma_transform_kernel<false, true><<<grid, NTH, smem, s>>>(in, out, M, m, in_es, out_es, L);
-  else dmma_transform_kernel<false, false><<<grid, NTH, smem, s>>>(in, out, M, m, in_es, out_es, L);
+  if (ci && co) dmma_transform_kernel<true, true><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
+  else if (ci) dmma_transform_kernel<true, false><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
+  else if (co) dmma_transform_kernel<false, true><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
+  else dmma_transform_kernel<false, false><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

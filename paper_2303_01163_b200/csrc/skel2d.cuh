@@ -9,6 +9,10 @@ namespace asdsm_b200 {
 
 constexpr int kSkelMaxKnots = 64;
 
+// Spline tables of both axes staged in shared memory by the calling block (every access of
+// the per-line recurrences would otherwise be an exposed L2 round trip).
+constexpr int kSkelTabMax = 6 * kSkelMaxKnots;
+
 // per-line: second derivatives via the pre-eliminated tridiagonal system, then per-segment
 // (y_c, c1, c2, c3); y has nc+2 entries (y[0] = y[nc+1] = 0).
 __device__ inline void skel_line_segments(const double* tab, int nc, const double* y, double* seg) {
@@ -55,6 +59,11 @@ __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
   const bool in_smem = nc0 * nc1 <= kSkelMaxKnots * kSkelMaxKnots / 4;
   const double nfc = a.norm_fc ? *a.norm_fc : 1.0;
   const double ncf = a.norm_cf ? *a.norm_cf : 1.0;
+  __shared__ double stab[2][kSkelTabMax];
+  const int tl0 = (nc0 + 2) + 5 * nc0, tl1 = (nc1 + 2) + 5 * nc1;
+  for (int q = threadIdx.x; q < tl0; q += blockDim.x) cp_async8(&stab[0][q], a.sp_tab[0] + q);
+  for (int q = threadIdx.x; q < tl1; q += blockDim.x) cp_async8(&stab[1][q], a.sp_tab[1] + q);
+  cp_async_wait_all();
   for (int t = threadIdx.x; t < nc0 * nc1; t += blockDim.x) {
     const int I = t % nc0, J = t / nc0;
     double u1 = a.u_fc[static_cast<i64>((I + 1) * m.n[0] - 1) + static_cast<i64>(m.nf[0]) * J];
@@ -84,13 +93,13 @@ __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
       y[0] = 0.0;
       for (int C = 0; C < nc0; ++C) y[C + 1] = E1[C + static_cast<i64>(nc0) * J];
       y[nc0 + 1] = 0.0;
-      skel_line_segments(a.sp_tab[0], nc0, y, a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1));
+      skel_line_segments(stab[0], nc0, y, a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1));
     } else {
       const int I = t - nc1;
       y[0] = 0.0;
       for (int C = 0; C < nc1; ++C) y[C + 1] = E2[I + static_cast<i64>(nc0) * C];
       y[nc1 + 1] = 0.0;
-      skel_line_segments(a.sp_tab[1], nc1, y, a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1));
+      skel_line_segments(stab[1], nc1, y, a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1));
     }
   }
 }
