@@ -76,62 +76,65 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
       ft = fma(w, fT[i], ft);
     }
   }
-  const double w0 = __ldg(A.Wt + k), wm = __ldg(A.Wt + static_cast<i64>(m0 - 1) * m0 + k);
+  const double w0 = __ldg(A.Wt + k);
+  const double wm = m0 > 1 ? __ldg(A.Wt + static_cast<i64>(m0 - 1) * m0 + k) : 0.0;  // m0 == 1: one column
   const double l = A.line_left;
-  double* out = modes + static_cast<i64>(hole) * m0 * m1;
-  // forward sweep, pivots prefetched 8 rows ahead; y parked in smem or the mode buffer
-  double y = 0.0;
-  constexpr int U = 24;
-  double ivn[U];
+  double* out = modes + static_cast<i64>(hole) * m0 * m1 + k;  // column k of [j][k]
+  // Lean sweeps: pointers advance by one row (m0) per step; pivots prefetched U rows ahead;
+  // y parked in shared memory when the CTA's slice fits, else in the mode buffer.
+  const double* __restrict__ ip = ipiv + k;
+  const double* __restrict__ cq = cpv + k;
+  double* yp = A.y_in_smem ? ys + threadIdx.x : out;
+  const int ys_stride = A.y_in_smem ? KB : m0;
+  constexpr int U = 16;
+  double y = fb * __ldg(ip);
+  yp[0] = y;
+  double ivq[U];
 #pragma unroll
-  for (int q = 0; q < U; ++q) ivn[q] = q < m1 ? __ldg(ipiv + static_cast<i64>(q) * m0 + k) : 0.0;
-  for (int j0 = 0; j0 < m1; j0 += U) {
-    double iv[U];
+  for (int q = 0; q < U; ++q) ivq[q] = (1 + q < m1) ? __ldg(ip + static_cast<i64>(1 + q) * m0) : 0.0;
+  int j = 1;
+  for (; j + U <= m1 - 1; j += U) {  // interior rows j .. j+U-1 (all < m1-1)
+    double nxt[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      iv[q] = ivn[q];
-      const int jn = j0 + U + q;
-      ivn[q] = jn < m1 ? __ldg(ipiv + static_cast<i64>(jn) * m0 + k) : 0.0;
+      const int jn = j + U + q;
+      nxt[q] = jn < m1 ? __ldg(ip + static_cast<i64>(jn) * m0) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const int j = j0 + q;
-      if (j >= m1) break;
-      double f;
-      if (j == 0) f = fb;
-      else if (j == m1 - 1) f = ft;
-      else f = (m0 > 1) ? fma(wm, fR[j], w0 * fL[j]) : w0 * fL[j];
-      y = (j == 0) ? f * iv[q] : (f - l * y) * iv[q];
-      if (A.y_in_smem) ys[j * KB + threadIdx.x] = y;
-      else out[static_cast<i64>(j) * m0 + k] = y;
+      const double f = fma(wm, fR[j + q], w0 * fL[j + q]);
+      y = (f - l * y) * ivq[q];
+      yp[static_cast<i64>(j + q) * ys_stride] = y;
     }
+#pragma unroll
+    for (int q = 0; q < U; ++q) ivq[q] = nxt[q];
   }
-  // backward sweep, mode layout [hole][j][k]
+  for (int q = 0; j < m1; ++j, ++q) {  // remaining rows (the last row uses the full transform)
+    const double f = (j == m1 - 1) ? ft : fma(wm, fR[j], w0 * fL[j]);
+    const double iv = q < U ? ivq[q] : __ldg(ip + static_cast<i64>(j) * m0);
+    y = (f - l * y) * iv;
+    yp[static_cast<i64>(j) * ys_stride] = y;
+  }
+  // backward sweep into the mode buffer
   double x = y;
-  out[static_cast<i64>(m1 - 1) * m0 + k] = x;
-  double cpn[U];
+  out[static_cast<i64>(m1 - 1) * m0] = x;
+  j = m1 - 2;
+  for (; j - U + 1 >= 0; j -= U) {
+    double cv[U], yv[U];
 #pragma unroll
-  for (int q = 0; q < U; ++q) {
-    const int j = m1 - 2 - q;
-    cpn[q] = j >= 0 ? __ldg(cpv + static_cast<i64>(j) * m0 + k) : 0.0;
+    for (int q = 0; q < U; ++q) {
+      cv[q] = __ldg(cq + static_cast<i64>(j - q) * m0);
+      yv[q] = yp[static_cast<i64>(j - q) * ys_stride];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      x = yv[q] - cv[q] * x;
+      out[static_cast<i64>(j - q) * m0] = x;
+    }
   }
-  for (int j0 = m1 - 2; j0 >= 0; j0 -= U) {
-    double cpj[U], yv[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      cpj[q] = cpn[q];
-      const int jn = j0 - U - q;
-      cpn[q] = jn >= 0 ? __ldg(cpv + static_cast<i64>(jn) * m0 + k) : 0.0;
-      const int j = j0 - q;
-      yv[q] = j >= 0 ? (A.y_in_smem ? ys[j * KB + threadIdx.x] : out[static_cast<i64>(j) * m0 + k]) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int j = j0 - q;
-      if (j < 0) break;
-      x = yv[q] - cpj[q] * x;
-      out[static_cast<i64>(j) * m0 + k] = x;
-    }
+  for (; j >= 0; --j) {
+    x = yp[static_cast<i64>(j) * ys_stride] - __ldg(cq + static_cast<i64>(j) * m0) * x;
+    out[static_cast<i64>(j) * m0] = x;
   }
 }
 

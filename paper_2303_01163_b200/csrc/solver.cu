@@ -345,6 +345,10 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     if (!A.tables_in_smem) {
       A.kb = 64;
       A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
+      if (!A.y_in_smem && hole2d_smem_bytes(A.m0, A.m1, 32, true) <= 48 * 1024) {
+        A.kb = 32;  // narrower CTAs so the forward sweep stays in shared memory
+        A.y_in_smem = 1;
+      }
     }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
@@ -848,6 +852,10 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     A.nbox1 = mesh_.nc[1] + 1;
     A.kb = 64;
     A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
+    if (!A.y_in_smem && hole2d_smem_bytes(A.m0, A.m1, 32, true) <= 48 * 1024) {
+      A.kb = 32;
+      A.y_in_smem = 1;
+    }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
     A.ipiv = H.th_ipiv;
