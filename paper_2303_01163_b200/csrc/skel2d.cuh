@@ -7,7 +7,7 @@
 
 namespace asdsm_b200 {
 
-constexpr int kSkelMaxKnots = 64;
+constexpr int kSkelMaxKnots = 24;  // 2D fast path: coarse counts <= 22 (shared-memory staging)
 
 // Spline tables of both axes staged in shared memory by the calling block (every access of
 // the per-line recurrences would otherwise be an exposed L2 round trip).
@@ -55,8 +55,8 @@ __device__ __forceinline__ double skel_seg_eval(const double* tab, const double*
 __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
   const MeshDev& m = a.m;
   const int nc0 = m.nc[0], nc1 = m.nc[1];
-  __shared__ double se1[kSkelMaxKnots * kSkelMaxKnots / 4], se2[kSkelMaxKnots * kSkelMaxKnots / 4];
-  const bool in_smem = nc0 * nc1 <= kSkelMaxKnots * kSkelMaxKnots / 4;
+  __shared__ double se1[kSkelMaxKnots * kSkelMaxKnots], se2[kSkelMaxKnots * kSkelMaxKnots];
+  const bool in_smem = nc0 * nc1 <= kSkelMaxKnots * kSkelMaxKnots;
   const double nfc = a.norm_fc ? *a.norm_fc : 1.0;
   const double ncf = a.norm_cf ? *a.norm_cf : 1.0;
   __shared__ double stab[2][kSkelTabMax];
@@ -86,21 +86,66 @@ __device__ inline void skel2d_ccspline_block(const Skel2DArgs& a) {
   __syncthreads();
   const double* E1 = in_smem ? se1 : a.e1;
   const double* E2 = in_smem ? se2 : a.e2;
-  for (int t = threadIdx.x; t < nc0 + nc1; t += blockDim.x) {
-    double y[kSkelMaxKnots];
-    if (t < nc1) {
-      const int J = t;
-      y[0] = 0.0;
-      for (int C = 0; C < nc0; ++C) y[C + 1] = E1[C + static_cast<i64>(nc0) * J];
-      y[nc0 + 1] = 0.0;
-      skel_line_segments(stab[0], nc0, y, a.seg1 + static_cast<i64>(J) * 4 * (nc0 + 1));
-    } else {
-      const int I = t - nc1;
-      y[0] = 0.0;
-      for (int C = 0; C < nc1; ++C) y[C + 1] = E2[I + static_cast<i64>(nc0) * C];
-      y[nc1 + 1] = 0.0;
-      skel_line_segments(stab[1], nc1, y, a.seg2 + static_cast<i64>(I) * 4 * (nc1 + 1));
+  // Phase 2, split so only the two short recurrences per line are sequential:
+  //  2a one thread per (line, i): rhs_i = (y[i+2]-y[i+1])/hr_i - (y[i+1]-y[i])/hl_i
+  //  2b one thread per line: forward elimination and back substitution (spline.cpp:29-36)
+  //  2c one thread per (line, segment): (y_c, c1, c2, c3) (spline.cpp:47-55)
+  constexpr int KM = kSkelMaxKnots;
+  __shared__ double srhs[2 * KM][KM];  // [line][i]   (lines: nc1 along x, then nc0 along y)
+  __shared__ double smm[2 * KM][KM];   // [line][c]   second derivatives
+  const int nlines = nc0 + nc1;
+  auto yval = [&](int line, int c) -> double {  // y[c], c = 0..nc+1
+    if (line < nc1) return (c == 0 || c == nc0 + 1) ? 0.0 : E1[(c - 1) + static_cast<i64>(nc0) * line];
+    const int I = line - nc1;
+    return (c == 0 || c == nc1 + 1) ? 0.0 : E2[I + static_cast<i64>(nc0) * (c - 1)];
+  };
+  for (int t = threadIdx.x; t < nc1 * nc0 + nc0 * nc1; t += blockDim.x) {
+    const int line = t < nc1 * nc0 ? t / nc0 : nc1 + (t - nc1 * nc0) / nc1;
+    const int nc = line < nc1 ? nc0 : nc1;
+    const int i = t < nc1 * nc0 ? t % nc0 : (t - nc1 * nc0) % nc1;
+    const double* tab = stab[line < nc1 ? 0 : 1];
+    const double* hl = tab + nc + 2;
+    const double* hr = hl + nc;
+    srhs[line][i] = __dsub_rn(__dsub_rn(yval(line, i + 2), yval(line, i + 1)) / hr[i],
+                              __dsub_rn(yval(line, i + 1), yval(line, i)) / hl[i]);
+  }
+  __syncthreads();
+  for (int line = threadIdx.x; line < nlines; line += blockDim.x) {
+    const int nc = line < nc1 ? nc0 : nc1, ni = nc, n = nc + 2;
+    const double* tab = stab[line < nc1 ? 0 : 1];
+    const double* w = tab + n + 2 * ni;
+    const double* dg = w + ni;
+    const double* up = dg + ni;
+    double* rhs = srhs[line];
+    double* m = smm[line];
+    for (int i = 1; i < ni; ++i) rhs[i] = __dsub_rn(rhs[i], __dmul_rn(w[i], rhs[i - 1]));
+    m[0] = 0.0;
+    m[n - 1] = 0.0;
+    if (ni > 0) {
+      m[ni] = rhs[ni - 1] / dg[ni - 1];
+      for (int i = ni - 1; i >= 1; --i) m[i] = __dsub_rn(rhs[i - 1], __dmul_rn(up[i - 1], m[i + 1])) / dg[i - 1];
     }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nc1 * (nc0 + 1) + nc0 * (nc1 + 1); t += blockDim.x) {
+    int line, c;
+    if (t < nc1 * (nc0 + 1)) {
+      line = t / (nc0 + 1);
+      c = t % (nc0 + 1);
+    } else {
+      line = nc1 + (t - nc1 * (nc0 + 1)) / (nc1 + 1);
+      c = (t - nc1 * (nc0 + 1)) % (nc1 + 1);
+    }
+    const double* x = stab[line < nc1 ? 0 : 1];
+    const double* m = smm[line];
+    const double y0 = yval(line, c), y1 = yval(line, c + 1);
+    const double h = __dsub_rn(x[c + 1], x[c]);
+    double* seg = line < nc1 ? a.seg1 + static_cast<i64>(line) * 4 * (nc0 + 1) + 4 * c
+                             : a.seg2 + static_cast<i64>(line - nc1) * 4 * (nc1 + 1) + 4 * c;
+    seg[0] = y0;
+    seg[1] = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m[c]), m[c + 1])) / 6.0);
+    seg[2] = m[c] / 2.0;
+    seg[3] = __dsub_rn(m[c + 1], m[c]) / __dmul_rn(6.0, h);
   }
 }
 

@@ -184,7 +184,7 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
   dmma_prepare();
-  if (!variable_ && m.dim == 2 && m.nc[0] <= 62 && m.nc[1] <= 62 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
+  if (!variable_ && m.dim == 2 && m.nc[0] <= 22 && m.nc[1] <= 22 && std::getenv("ASDSM_GENERIC_FILL") == nullptr) {
     fast2d_ = true;
     for (int a = 0; a < 2; ++a) {
       const SepSolver& S = sep_slab_[a];
