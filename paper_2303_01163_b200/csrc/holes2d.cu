@@ -10,6 +10,9 @@
 // runs both Thomas sweeps in shared memory; the dense back transform is the DMMA GEMM.
 #include "holes2d.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace asdsm_b200 {
 
 namespace {
@@ -109,11 +112,14 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
 #pragma unroll
     for (int q = 0; q < U; ++q) ivq[q] = nxt[q];
   }
-  for (int q = 0; j < m1; ++j, ++q) {  // remaining rows (the last row uses the full transform)
-    const double f = (j == m1 - 1) ? ft : fma(wm, fR[j], w0 * fL[j]);
-    const double iv = q < U ? ivq[q] : __ldg(ip + static_cast<i64>(j) * m0);
-    y = (f - l * y) * iv;
-    yp[static_cast<i64>(j) * ys_stride] = y;
+#pragma unroll
+  for (int q = 0; q < U; ++q) {  // remaining (<= U) rows; the last row uses the full transform
+    const int jj = j + q;          // (static indices keep ivq in registers)
+    if (jj < m1) {
+      const double f = (jj == m1 - 1) ? ft : fma(wm, fR[jj], w0 * fL[jj]);
+      y = (f - l * y) * ivq[q];
+      yp[static_cast<i64>(jj) * ys_stride] = y;
+    }
   }
   // backward sweep into the mode buffer
   double x = y;
@@ -241,6 +247,415 @@ __global__ void hole2d_fwd_thomas_smem_kernel(const double* __restrict__ e, doub
   }
 }
 
+
+// Whole-hole fused fill for small holes (m0, m1 <= 128): one CTA per hole runs the ring rhs,
+// the analytic forward transform and the Thomas sweeps for every mode into a shared-memory
+// mode tile, then the DMMA back transform (mma.sync.m8n8k4.f64) from shared memory straight
+// into the hole's fine-grid positions -- no mode buffer round trip, one launch instead of two.
+// Every table a phase needs (Wt, the Thomas pivots and upper factors, V) is bulk-staged into
+// shared memory with cp.async before that phase, so each phase waits on one L2 round trip
+// instead of one per serial step; the pivots are staged into the mode tile itself (the forward
+// sweep overwrites pivot (j, k) with y(j, k) in place).
+constexpr int kFusedThreads = 512;
+
+__device__ __forceinline__ void dmma_f64(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// rows x cols table (row stride ld in global, S in shared) -> shared, asynchronously.  Every
+// CTA reads the same table at the same time: each starts at a different rotation of the
+// element order so the requests spread over the L2 slices instead of queueing on one line.
+__device__ __forceinline__ void stage_table(double* dst, const double* __restrict__ src, int rows, int cols, int ld,
+                                            int S, int tid) {
+  if ((cols & 1) == 0 && (ld & 1) == 0) {
+    const int hc = cols >> 1, n = rows * hc;
+    const int rot = static_cast<int>((blockIdx.x * 977u) % static_cast<unsigned>(n));
+    for (int t0 = tid; t0 < n; t0 += kFusedThreads) {
+      int t = t0 + rot;
+      if (t >= n) t -= n;
+      const int r = t / hc, c = 2 * (t - r * hc);
+      cp_async16(dst + r * S + c, src + static_cast<i64>(r) * ld + c);
+    }
+  } else {
+    const int n = rows * cols;
+    const int rot = static_cast<int>((blockIdx.x * 977u) % static_cast<unsigned>(n));
+    for (int t0 = tid; t0 < n; t0 += kFusedThreads) {
+      int t = t0 + rot;
+      if (t >= n) t -= n;
+      const int r = t / cols, c = t - r * cols;
+      cp_async8(dst + r * S + c, src + static_cast<i64>(r) * ld + c);
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// One warp's share of the even/odd back transform: NA j tiles (32 S apart) x NB i tiles, an
+// E and an O accumulator per tile (K = kh each), the next k step's fragments loaded while the
+// current step's MMAs issue.  Static counts keep the MMAs unpredicated (the caller dispatches).
+template <int NA, int NB>
+__device__ __forceinline__ void fused_gemm_eo(double (&ae)[4][2][2], double (&ao)[4][2][2], const double* pa,
+                                              const double* pb, int kh) {
+  constexpr int S = kHole2DFusedStride;
+  double fe[NA], fo[NA], ge[NB], go[NB];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    fe[a] = pa[a * 32 * S];
+    fo[a] = pa[a * 32 * S + kh];
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    ge[b] = pb[b * 32 * S];
+    go[b] = pb[b * 32 * S + kh];
+  }
+  for (int kk = 0; kk < kh; kk += 4) {
+    const int kn = kk + 4 < kh ? kk + 4 : kk;
+    double ne[NA], no[NA], me[NB], mo[NB];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      ne[a] = pa[a * 32 * S + kn];
+      no[a] = pa[a * 32 * S + kh + kn];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      me[b] = pb[b * 32 * S + kn];
+      mo[b] = pb[b * 32 * S + kh + kn];
+    }
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        dmma_f64(ae[a][b], fe[a], ge[b]);
+        dmma_f64(ao[a][b], fo[a], go[b]);
+      }
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      fe[a] = ne[a];
+      fo[a] = no[a];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      ge[b] = me[b];
+      go[b] = mo[b];
+    }
+  }
+}
+
+// Error-mode hole fill, one CTA per hole (holes up to 108 x 128):
+//   P0  pivots -> shared (cp.async) ; ring rhs from the skeleton
+//   P1  full forward transforms of the first / last ring rows, W = c S D^-1 applied through
+//       the even/odd half sine table (W never leaves L2)
+//   P2  twisted Thomas per mode (top/bottom threads meet in the middle), modes x into shared
+//       memory with even/odd-permuted columns
+//   P4  half sine table -> shared over the dead pivots
+//   P5  back transform on the DMMA pipe, even/odd split: E = X_even S_e^T, O = X_odd S_o^T
+//       over ceil(m0/2) rows -- half the MMAs of a dense V, and out(i) = sc_i (E + O),
+//       out(m0-1-i) = sc_{m0-1-i} (E - O) written straight into the fine array
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    hole2d_fused_kernel(double* __restrict__ e, Hole2DArgs A, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+#ifdef ASDSM_FUSED_TRACE  // per-phase clock64 stamps of CTAs 0 and 55, printed at the end
+  long long T[8] = {clock64(), 0, 0, 0, 0, 0, 0, 0};
+#define FUSED_STAMP(i) T[i] = clock64()
+#else
+#define FUSED_STAMP(i)
+#endif
+  constexpr int S = kHole2DFusedStride;  // compile-time row stride: every row offset is an immediate
+  extern __shared__ __align__(16) double sm[];
+  const int m0 = A.m0, m1 = A.m1;
+  const int kh = half_sine_kh(m0), hr = half_sine_rows(m0);
+  const int mh = (m0 + 1) >> 1;  // rows of the half transform
+  const int JP = (m1 + 7) & ~7;
+  const int NP = m1 - ((m1 - 1) >> 1);  // pivot rows the twisted sweeps use (distance < NP)
+  const double* __restrict__ SH = A.half;               // [hr][2 kh]
+  const double* __restrict__ sc = A.half + hr * 2 * kh; // scale_i
+  const double* __restrict__ ci = sc + m0;              // (2/(m0+1)) / scale_i
+  double* sY = sm;            // [JP][S]: sweep values y / z, then the modes x (row j, permuted col)
+  double* sH = sY + JP * S;   // [hr][S]: half sine table (resident for P1 and P5)
+  double* sP = sH + hr * S;   // [NP][S]: Thomas pivots (row t = distance from the own end, mode k)
+  double* fL = sP + NP * S;
+  double* fR = fL + m1;
+  double* fB = fR + m1;
+  double* fT = fB + m0;
+  double* part = fT + m0;     // [4][2][128] partial sums of the full row transforms
+  double* xch = part + 1024;  // [2 sides][2][128] values exchanged at the meeting rows
+  double* scs = xch + 512;    // [m0] scale_i
+  double* hv = scs + 128;     // [4][64] ring-row pair sums h+ / h- of fB and fT
+  const int tid = threadIdx.x;
+  const int hole = blockIdx.x;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  const int ox = hx * A.n0, oy = hy * A.n1;
+  // P0
+  stage_table(sP, A.ipiv, NP, m0, m0, S, tid);
+  stage_table(sH, SH, hr, 2 * kh, 2 * kh, S, tid);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  {  // zero the k padding of the mode tile (even / odd mode counts me / mo)
+    const int me = (m0 + 1) >> 1, mo = m0 >> 1;
+    const int pe = kh - me, po = kh - mo;
+    for (int t = tid; t < JP * (pe + po); t += kFusedThreads) {
+      const int r = t / (pe + po), c = t % (pe + po);
+      sY[r * S + (c < pe ? me + c : kh + mo + (c - pe))] = 0.0;
+    }
+  }
+  if (tid >= 128 && tid - 128 < m0) scs[tid - 128] = __ldg(sc + tid - 128);
+  if (tid < m1) {
+    fL[tid] = ring_rhs(e, A, ox, oy, 0, tid);
+    fR[tid] = ring_rhs(e, A, ox, oy, m0 - 1, tid);
+  } else if (tid >= 256 && tid - 256 < m0) {
+    const int i = tid - 256;
+    const double c = __ldg(ci + i);  // the ring rows enter W through D^-1: pre-scale
+    fB[i] = ring_rhs(e, A, ox, oy, i, 0) * c;
+    fT[i] = ring_rhs(e, A, ox, oy, i, m1 - 1) * c;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  FUSED_STAMP(1);
+  // P1: fb[k] = sum_{i<mh} s_ik (g_i +- g_{m0-1-i}) (sign (-1)^k), g = c D^-1 f; i in four groups
+  const int side = tid >> 7, k = tid & 127;  // sweeps: warps 0-3 top side, warps 4-7 bottom side
+  const bool sweeper = side < 2 && k < m0;
+  const int colk = (k & 1) ? kh + (k >> 1) : (k >> 1);
+  double w0 = 0.0, wm = 0.0;
+  if (tid < mh) {  // pair sums of the pre-scaled ring rows: h+ (even k) and h- (odd k)
+    const int i = tid, im = m0 - 1 - tid;
+    hv[i] = im == i ? fB[i] : fB[i] + fB[im];
+    hv[64 + i] = im == i ? fB[i] : fB[i] - fB[im];
+    hv[128 + i] = im == i ? fT[i] : fT[i] + fT[im];
+    hv[192 + i] = im == i ? fT[i] : fT[i] - fT[im];
+  }
+  __syncthreads();
+  if (k < m0) {
+    const int g = tid >> 7;
+    const int q = (mh + 3) >> 2;
+    const int i0 = g * q, i1 = min(mh, i0 + q);
+    const bool odd = k & 1;
+    const double* hb = hv + (odd ? 64 : 0);
+    const double* ht = hv + (odd ? 192 : 128);
+    double pb = 0.0, pt = 0.0;
+#pragma unroll 4
+    for (int i = i0; i < i1; ++i) {
+      const double s = sH[i * S + colk];
+      pb = fma(s, hb[i], pb);
+      pt = fma(s, ht[i], pt);
+    }
+    part[(2 * g) * 128 + k] = pb;
+    part[(2 * g + 1) * 128 + k] = pt;
+    if (sweeper) {
+      const double s0 = sH[colk];
+      w0 = s0 * __ldg(ci);
+      wm = (odd ? -s0 : s0) * __ldg(ci + m0 - 1);
+    }
+  }
+  __syncthreads();
+  FUSED_STAMP(2);
+  // P2: twisted (two-sided) Thomas per mode: the top thread eliminates rows 0..p downward, the
+  // bottom thread rows m1-1..p+1 upward (the bottom-up pivots of a Toeplitz tridiagonal are the
+  // top-down ones by distance from the end), they meet in a 2x2 solve and substitute outward --
+  // chains half as long as one Thomas sweep.  Upper factors are r * pivot (top) / l * pivot.
+  const double l = A.line_left, rr = A.line_right;
+  const int p = (m1 - 1) >> 1;
+  const int n1 = side ? m1 - 1 - p : p + 1;  // rows this side eliminates
+  const double* pv = sP + k;                 // pivot t of this mode: pv[t * S]
+  if (sweeper) {
+    const double fb = ((part[k] + part[256 + k]) + part[512 + k]) + part[768 + k];
+    const double ft = ((part[128 + k] + part[384 + k]) + part[640 + k]) + part[896 + k];
+    const double cf = side ? rr : l, cb = side ? l : rr;
+    double y;
+    if (side == 0) {  // rows 0 .. p
+      double* yv = sY + colk;
+      y = fb * pv[0];
+      yv[0] = y;
+      int t = 1;
+      for (; t + 8 <= n1; t += 8) {
+        double pq[8], lq[8], rq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          pq[q] = pv[(t + q) * S];
+          lq[q] = fL[t + q];
+          rq[q] = fR[t + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          y = (fma(wm, rq[q], w0 * lq[q]) - cf * y) * pq[q];
+          yv[(t + q) * S] = y;
+        }
+      }
+      for (; t < n1; ++t) {
+        y = (fma(wm, fR[t], w0 * fL[t]) - cf * y) * pv[t * S];
+        yv[t * S] = y;
+      }
+    } else {  // rows m1-1 .. p+1
+      double* yv = sY + (m1 - 1) * S + colk;  // row m1-1-t at yv[-t * S]
+      const double* fl = fL + (m1 - 1);
+      const double* fr = fR + (m1 - 1);
+      y = ft * pv[0];
+      yv[0] = y;
+      int t = 1;
+      for (; t + 8 <= n1; t += 8) {
+        double pq[8], lq[8], rq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          pq[q] = pv[(t + q) * S];
+          lq[q] = fl[-(t + q)];
+          rq[q] = fr[-(t + q)];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          y = (fma(wm, rq[q], w0 * lq[q]) - cf * y) * pq[q];
+          yv[-(t + q) * S] = y;
+        }
+      }
+      for (; t < n1; ++t) {
+        y = (fma(wm, fr[-t], w0 * fl[-t]) - cf * y) * pv[t * S];
+        yv[-t * S] = y;
+      }
+    }
+    xch[(2 * side) * 128 + k] = y;
+    xch[(2 * side + 1) * 128 + k] = cb * pv[(n1 - 1) * S];
+  }
+  FUSED_STAMP(3);
+  __syncthreads();
+  if (sweeper) {
+    const double yp = xch[k], cpp = xch[128 + k];       // top: y_p, c'_p
+    const double zq = xch[256 + k], aq = xch[384 + k];  // bottom: z_{p+1}, a'_{p+1}
+    const double xp = (yp - cpp * zq) / (1.0 - cpp * aq);
+    const double xq = zq - aq * xp;
+    FUSED_STAMP(4);
+    const double cb = side ? l : rr;
+    // substitute back toward the own end: x_t = y_t - cb * piv_t * x_{t+1}
+    double x = side ? xq : xp;
+    int t = n1 - 2;
+    if (side == 0) {
+      double* yv = sY + colk;
+      yv[(n1 - 1) * S] = x;
+      for (; t - 7 >= 0; t -= 8) {
+        double yq[8], cq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          yq[q] = yv[(t - q) * S];
+          cq[q] = cb * pv[(t - q) * S];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x = yq[q] - cq[q] * x;
+          yv[(t - q) * S] = x;
+        }
+      }
+      for (; t >= 0; --t) {
+        x = yv[t * S] - (cb * pv[t * S]) * x;
+        yv[t * S] = x;
+      }
+    } else {
+      double* yv = sY + (m1 - 1) * S + colk;
+      yv[-(n1 - 1) * S] = x;
+      for (; t - 7 >= 0; t -= 8) {
+        double yq[8], cq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          yq[q] = yv[-(t - q) * S];
+          cq[q] = cb * pv[(t - q) * S];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x = yq[q] - cq[q] * x;
+          yv[-(t - q) * S] = x;
+        }
+      }
+      for (; t >= 0; --t) {
+        x = yv[-t * S] - (cb * pv[t * S]) * x;
+        yv[-t * S] = x;
+      }
+    }
+  }
+  FUSED_STAMP(6);
+  __syncthreads();
+  __syncthreads();
+  FUSED_STAMP(7);
+  // P5: 16 warps; warp w takes j tiles jg + 4a and half-row tiles ig + 4b with jg = w / 4,
+  // ig = (w + jg) % 4, so each SM sub-partition (w % 4) holds one warp of every (jg, ig)
+  // diagonal and the DMMA work is balanced across the four pipes.
+  const int lane = tid & 31, warp = tid >> 5;
+  const int jg = warp >> 2, ig = (warp + jg) & 3;
+  const int jt = JP >> 3, it = hr >> 3;
+  double ae[4][2][2], ao[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) ae[a][b][0] = ae[a][b][1] = ao[a][b][0] = ao[a][b][1] = 0.0;
+  const int r8 = lane >> 2, c4 = lane & 3;
+  const double* pa = sY + (jg * 8 + r8) * S + c4;
+  const double* pb = sH + (ig * 8 + r8) * S + c4;
+  const int na = min(4, max(0, (jt - jg + 3) >> 2));
+  const int nb = min(2, max(0, (it - ig + 3) >> 2));
+  switch (na * 3 + nb) {
+#define ASDSM_FUSED_CASE(NA, NB) \
+  case NA * 3 + NB:              \
+    fused_gemm_eo<NA, NB>(ae, ao, pa, pb, kh); \
+    break;
+    ASDSM_FUSED_CASE(1, 1) ASDSM_FUSED_CASE(1, 2) ASDSM_FUSED_CASE(2, 1) ASDSM_FUSED_CASE(2, 2)
+    ASDSM_FUSED_CASE(3, 1) ASDSM_FUSED_CASE(3, 2) ASDSM_FUSED_CASE(4, 1) ASDSM_FUSED_CASE(4, 2)
+#undef ASDSM_FUSED_CASE
+    default:
+      break;
+  }
+  FUSED_STAMP(5);
+  // epilogue: each lane holds E, O at rows (j, i), (j, i+1) of its tiles: out(i) = sc_i (E+O)
+  // and the mirror out(m0-1-i) = sc (E-O), stored as pairs (16-byte stores where aligned)
+  const i64 Nx = A.nf0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int j = (jg + 4 * a) * 8 + r8;
+    if (a >= na || j >= m1) continue;
+    double* row = e + static_cast<i64>(oy + j) * Nx + ox;
+    const bool al = ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (b >= nb) continue;
+      const int i = (ig + 4 * b) * 8 + 2 * c4;  // i even
+      if (i >= mh) continue;
+      const int im = m0 - 1 - i;
+      const double E0 = ae[a][b][0], O0 = ao[a][b][0], E1 = ae[a][b][1], O1 = ao[a][b][1];
+      const double lo0 = scs[i] * (E0 + O0), hi0 = scs[im] * (E0 - O0);
+      if (i + 1 < mh) {
+        const double lo1 = scs[i + 1] * (E1 + O1), hi1 = scs[im - 1] * (E1 - O1);
+        if (al) *reinterpret_cast<double2*>(row + i) = make_double2(lo0, lo1);
+        else {
+          row[i] = lo0;
+          row[i + 1] = lo1;
+        }
+        if (im - 1 > i + 1) {  // mirrors distinct from the direct pair
+          if (al && ((im - 1) & 1) == 0) *reinterpret_cast<double2*>(row + im - 1) = make_double2(hi1, hi0);
+          else {
+            row[im - 1] = hi1;
+            row[im] = hi0;
+          }
+        }
+      } else {
+        row[i] = lo0;
+        if (im != i) row[im] = hi0;
+      }
+    }
+  }
+#ifdef ASDSM_FUSED_TRACE
+  {
+    __syncthreads();
+    const long long T8 = clock64();
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 55))
+      printf("FUSEDDBG blk %d stage+ring %lld rowtf %lld elim %lld div %lld subst %lld gemm %lld epi %lld\n",
+             blockIdx.x, T[1] - T[0], T[2] - T[1], T[3] - T[2], T[4] - T[3], T[6] - T[4], T[5] - T[7], T8 - T[5]);
+  }
+#endif
+#undef FUSED_STAMP
+}
+
 }  // namespace
 
 size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem) {
@@ -261,6 +676,25 @@ void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& 
   ++g_kernel_launches;
 }
 
+size_t hole2d_fused_smem_bytes(int m0, int m1) {
+  const size_t S = kHole2DFusedStride;
+  const size_t jp = (m1 + 7) & ~7;
+  const size_t np = m1 - ((m1 - 1) >> 1);
+  return sizeof(double) * ((jp + half_sine_rows(m0) + np) * S + 2 * static_cast<size_t>(m0 + m1) + 15 * 128);
+}
+
+bool hole2d_fused_fits(int m0, int m1) {
+  return m0 >= 2 && m1 >= 2 && m0 <= 128 && m1 <= 128 && 2 * half_sine_kh(m0) <= kHole2DFusedStride &&
+         hole2d_fused_smem_bytes(m0, m1) <= kHole2DFusedMaxSmem;
+}
+
+void launch_hole2d_fused(double* e, const Hole2DArgs& A, DevState* state, cudaStream_t s) {
+  const size_t smem = hole2d_fused_smem_bytes(A.m0, A.m1);
+  hole2d_fused_kernel<<<static_cast<unsigned>(A.nbox0 * A.nbox1), kFusedThreads, smem, s>>>(e, A, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void hole2d_prepare(size_t smem) {
   static bool done = false;
   if (done) return;
@@ -269,6 +703,8 @@ void hole2d_prepare(size_t smem) {
                                         static_cast<int>(smem)));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kHole2DFusedMaxSmem)));
 }
 
 }  // namespace asdsm_b200

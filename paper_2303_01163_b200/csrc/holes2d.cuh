@@ -11,13 +11,23 @@ struct Hole2DArgs {
   int kb;            // modes per CTA
   Stencil st;        // fine stencil
   const double* Wt;  // forward eigenvectors along x, transposed: Wt[i*m0 + k] = W[k][i]
+  const double* half;  // even/odd half sine table + row scalings along x (SepSolver::half)
   const double* ipiv;  // Thomas pivots [j][k]
   const double* cp;    // Thomas upper factors [j][k]
-  double line_left;
+  double line_left, line_right;
   int y_in_smem;     // park the forward sweep in shared memory (else in the mode buffer)
   int tables_in_smem;  // bulk-load this CTA's slices of Wt / ipiv / cp into shared memory first
 };
 
+// fused whole-hole kernel (ring rhs + sweeps + DMMA back transform) for holes up to 128^2
+constexpr size_t kHole2DFusedMaxSmem = 220 * 1024;
+// shared row stride of the fused kernel's tiles (compile time, so row offsets are immediates):
+// = 12 (mod 16) doubles, so the 8 rows x 4 k of an m8n8k4 fragment load hit distinct bank
+// pairs; holes with up to 108 modes along x use the fused kernel
+constexpr int kHole2DFusedStride = 108;
+size_t hole2d_fused_smem_bytes(int m0, int m1);
+bool hole2d_fused_fits(int m0, int m1);
+void launch_hole2d_fused(double* e, const Hole2DArgs& A, DevState* state, cudaStream_t s);
 size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem = false);
 void hole2d_prepare(size_t smem);
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);

@@ -438,6 +438,21 @@ __global__ void state_init_kernel(DevState* S, int active, int have_e) {
   *S = h;
 }
 
+// Busy-waits on the global timer: queued ahead of a timed loop so the host enqueues every
+// launch while the device is still busy (the loop is then timed device-side, not host-bound).
+__global__ void spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+void launch_spin(double us, cudaStream_t s) {
+  spin_kernel<<<1, 1, 0, s>>>(static_cast<unsigned long long>(us * 1000.0));
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s) {
   state_init_kernel<<<1, 1, 0, s>>>(state, active, have_e);
   ASDSM_CUDA_CHECK(cudaGetLastError());

@@ -65,6 +65,7 @@ void launch_divide(double* x, i64 n, const double* divisor, DevState* state, cud
 
 // Device-side state initialization (capturable in a CUDA graph; no host memcpy).
 void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s);
+void launch_spin(double us, cudaStream_t s);
 
 // Final reductions + control (single CTA).
 enum CtrlOp {

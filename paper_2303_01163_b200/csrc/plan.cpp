@@ -114,6 +114,7 @@ struct AxisEigen {
   std::vector<cld> lam;  // m
   std::vector<cld> V;    // [j][k]
   std::vector<cld> W;    // [k][j]
+  std::vector<cld> scale;  // centred rho^j row scaling
   ld cond = 1;
 };
 
@@ -141,6 +142,7 @@ AxisEigen axis_eigen(int m, ld l, ld delta, ld r) {
     smin = std::min(smin, std::abs(scale[static_cast<size_t>(j)]));
   }
   e.cond = smax / smin;
+  e.scale = scale;
   e.V.resize(static_cast<size_t>(m) * m);
   e.W.resize(static_cast<size_t>(m) * m);
   const i64 period = 2LL * (m + 1);
@@ -152,6 +154,30 @@ AxisEigen axis_eigen(int m, ld l, ld delta, ld r) {
       e.W[static_cast<size_t>(k) * m + j] = (2.0L / static_cast<ld>(m + 1)) * s / scale[static_cast<size_t>(j)];
     }
   return e;
+}
+
+// Even/odd half of the sine factor of V = D S (plan.hpp SepSolver::half): rows i < ceil(m/2),
+// column col(k) = k/2 (k even) or kh + (k-1)/2 (k odd), zero padded; then scale_i and
+// (2/(m+1))/scale_i.  Row m-1-i of S is (-1)^k times row i, so a back transform needs only
+// these rows: out(i) = scale_i (E_i + O_i), out(m-1-i) = scale_{m-1-i} (E_i - O_i).
+std::vector<double> half_sine_tables(int m, const AxisEigen& e) {
+  const int kh = half_sine_kh(m), rows = half_sine_rows(m);
+  std::vector<double> t(static_cast<size_t>(rows) * 2 * kh + 2 * static_cast<size_t>(m), 0.0);
+  const ld pi = 3.141592653589793238462643383279502884L;
+  const i64 period = 2LL * (m + 1);
+  for (int i = 0; i < (m + 1) / 2; ++i)
+    for (int k = 0; k < m; ++k) {
+      const i64 q = (static_cast<i64>(i + 1) * (k + 1)) % period;
+      const int col = (k & 1) ? kh + (k >> 1) : (k >> 1);
+      t[static_cast<size_t>(i) * 2 * kh + col] = static_cast<double>(std::sin(pi * static_cast<ld>(q) / static_cast<ld>(m + 1)));
+    }
+  double* sc = t.data() + static_cast<size_t>(rows) * 2 * kh;
+  for (int i = 0; i < m; ++i) {
+    const ld s = e.scale[static_cast<size_t>(i)].real();
+    sc[i] = static_cast<double>(s);
+    sc[m + i] = static_cast<double>((2.0L / static_cast<ld>(m + 1)) / s);
+  }
+  return t;
 }
 
 std::vector<double> to_real(const std::vector<cld>& v) {
@@ -230,6 +256,7 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
       for (int k = 0; k < m; ++k)
         for (int j = 0; j < m; ++j) wt[static_cast<size_t>(j) * m + k] = static_cast<double>(e.W[static_cast<size_t>(k) * m + j].real());
       s.Wt[a] = upload(dev, wt);
+      s.half[a] = upload(dev, half_sine_tables(m, e));
     }
   }
 

@@ -100,6 +100,9 @@ struct SepSolver {
   double* W[3] = {nullptr, nullptr, nullptr};  // forward V^{-1}: [k][j]
   double* V[3] = {nullptr, nullptr, nullptr};  // backward V: [j][k]
   double* Wt[3] = {nullptr, nullptr, nullptr}; // forward, transposed: [j][k] = W[k][j] (real only)
+  // real only: even/odd half sine table [half_sine_rows][2 kh] (col(k) = k/2 | kh + (k-1)/2),
+  // then scale_i [m] and (2/(m+1))/scale_i [m]  (plan.cpp half_sine_tables)
+  double* half[3] = {nullptr, nullptr, nullptr};
   double* th_ipiv = nullptr;  // [pos][combo]
   double* th_cp = nullptr;    // [pos][combo]
   int pcr_levels = 0;
@@ -108,6 +111,11 @@ struct SepSolver {
   double* pcr_invb = nullptr; // [combo][pos]
   i64 mode_size() const { return static_cast<i64>(ext[0]) * ext[1] * (dim == 3 ? ext[2] : 1); }
 };
+
+// even/odd split sizes of an m-point sine transform: kh = padded half width (multiple of 4),
+// rows = ceil(m/2) padded to a multiple of 8 (DMMA tile rows)
+__host__ __device__ inline int half_sine_kh(int m) { return (((m + 1) / 2) + 3) & ~3; }
+__host__ __device__ inline int half_sine_rows(int m) { return (((m + 1) / 2) + 7) & ~7; }
 
 struct DeviceAlloc {
   std::vector<void*> ptrs;

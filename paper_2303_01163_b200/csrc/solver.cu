@@ -352,9 +352,16 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
+    A.half = H.half[0];
     A.ipiv = H.th_ipiv;
     A.cp = H.th_cp;
     A.line_left = H.line_left;
+    A.line_right = H.line_right;
+    static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
+    if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
+      launch_hole2d_fused(e, A, state_, s);
+      return;
+    }
     double* modes = static_cast<double*>(scratch0_);
     launch_hole2d_fwd_thomas(e, modes, A, state_, s);
     GemmLines G{};
@@ -781,6 +788,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   auto timed = [&](const char* name, double bytes, double flops, int per_solve, auto&& body) {
     launch_state_init(state_, 1, 1, s);
     body();  // warm
+    launch_spin(3000.0, s);  // keep the device busy while the host enqueues the timed loop
     ASDSM_CUDA_CHECK(cudaEventRecord(e0, s));
     for (int i = 0; i < reps; ++i) body();
     ASDSM_CUDA_CHECK(cudaEventRecord(e1, s));
@@ -858,9 +866,17 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     }
     A.st = st_fine_;
     A.Wt = H.Wt[0];
+    A.half = H.half[0];
     A.ipiv = H.th_ipiv;
     A.cp = H.th_cp;
     A.line_left = H.line_left;
+    A.line_right = H.line_right;
+    static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
+    if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
+      // one kernel: ring rhs, sweeps, DMMA back transform (writes the hole interior once)
+      timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
+            [&] { launch_hole2d_fused(e_, A, state_, s); });
+    } else {
     timed("hole2d_fwd_thomas", 8.0 * NH * (A.y_in_smem ? 1.0 : 3.0), 0.0, iters,
           [&] { launch_hole2d_fwd_thomas(e_, static_cast<double*>(scratch0_), A, state_, s); });
     GemmLines G{};
@@ -878,6 +894,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     G.nlines = static_cast<i64>(H.ext[1]) * G.nbox[0] * G.nbox[1];
     timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
           [&] { launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s); });
+    }
   } else {
     double hflops = 0;
     if (!variable_)
