@@ -11,6 +11,7 @@
 #include "ctrl.cuh"
 #include "march.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace asdsm_b200 {
@@ -261,6 +262,83 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+// Barrier-free 2D variant: 32 x 8 threads over (32 x 8*YC) tiles; each thread owns YC
+// consecutive rows of one column and keeps the y-neighbours in registers (YC+2 loads for YC
+// points); x-neighbours come through L1 (the adjacent lanes' lines).  No shared memory and no
+// per-row barrier: every load of a thread is independent, so the pass is one deep wave of
+// loads -- the right shape when the arrays sit in L2 (config 1) and at HBM scale alike.
+constexpr int YC = 8;
+template <int MODE, bool VAR>
+__global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const int cur = S->cur;
+  double s = 0.0;
+  bool work = true;
+  if (MODE == kMarchUpdate) {
+    s = S->s;
+    work = s != 0.0 && (!A.retry_pass || S->retry);
+  }
+  if (MODE == kMarchDots) work = S->have_e != 0;
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1];
+  const i64 sy = A.g.stride[1];
+  const Stencil& st = A.st;
+  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  Src<MODE> V{uu, A.e, s};
+  const double* __restrict__ rcur = cur ? A.r1 : A.r0;
+  double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
+  double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
+  const int ntx = (Nx + 31) / 32, nty = (Ny + 8 * YC - 1) / (8 * YC);
+  const int ntiles = ntx * nty;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int tile = work ? static_cast<int>(blockIdx.x) : ntiles; tile < ntiles; tile += gridDim.x) {
+    const int bx = tile % ntx, by = tile / ntx;
+    const int x = bx * 32 + tx, y0 = (by * 8 + ty) * YC;
+    if (x >= Nx || y0 >= Ny) continue;
+    double vy[YC + 2];
+#pragma unroll
+    for (int q = 0; q < YC + 2; ++q) {
+      const int y = y0 - 1 + q;
+      vy[q] = (y >= 0 && y < Ny) ? V(x + y * sy) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < YC; ++q) {
+      const int y = y0 + q;
+      if (y >= Ny) break;
+      const i64 p = x + y * sy;
+      const i64 N = A.g.size;
+      auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
+      double acc = 0.0;
+      if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[1]), vy[q]));
+      if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[0]), V(p - 1)));
+      const double vc = vy[q + 1];
+      acc = __dadd_rn(acc, __dmul_rn(C(2, st.diag), vc));
+      if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(3, st.right[0]), V(p + 1)));
+      if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[1]), vy[q + 2]));
+      if (MODE == kMarchDots) {
+        const double rp = __ldg(rcur + p);
+        a0 += rp * acc;
+        a2 += acc * acc;
+      } else {
+        double r = __dsub_rn(__ldg(A.b + p), acc);
+        if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
+        ro[p] = r;
+        if (MODE == kMarchUpdate) uo[p] = vc;
+        a0 += r * r;
+        a1 = fmax(a1, fabs(r));
+        if (A.exact) {
+          const double d = vc - __ldg(A.exact + p);
+          a2 += d * d;
+          a3 = fmax(a3, fabs(d));
+        }
+      }
+    }
+  }
+  block_reduce4_march(a0, a1, a2, a3, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
 // Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
@@ -388,8 +466,13 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
     }                                                                                   \
   } while (0)
-  if (A.g.dim == 2) {
+  static const bool march2d = std::getenv("ASDSM_MARCH2D") != nullptr;
+  if (A.g.dim == 2 && march2d) {
     ASDSM_MARCH_DISPATCH(march2d_kernel, nb, TX2);
+  } else if (A.g.dim == 2) {
+    const long long tiles = static_cast<long long>((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 8 * YC - 1) / (8 * YC));
+    const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, 8LL * kNumSms));
+    ASDSM_MARCH_DISPATCH(stencil2d_yc_kernel, nb2, 256);
   } else if (std::getenv("ASDSM_MARCH3D") == nullptr && mode != kMarchUpdate) {
     // measured (config 3/4): the barrier-free z-coarsened pass streams the residual and the
     // dot-product passes faster; the smem-plane march is faster for the 5-array update pass
