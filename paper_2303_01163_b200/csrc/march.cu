@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
 // points); x-neighbours come through L1 (the adjacent lanes' lines).  No shared memory and no
 // per-row barrier: every load of a thread is independent, so the pass is one deep wave of
 // loads -- the right shape when the arrays sit in L2 (config 1) and at HBM scale alike.
-constexpr int YC = 8;
-template <int MODE, bool VAR>
+template <int MODE, bool VAR, int YC>
 __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
@@ -470,9 +469,25 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   if (A.g.dim == 2 && march2d) {
     ASDSM_MARCH_DISPATCH(march2d_kernel, nb, TX2);
   } else if (A.g.dim == 2) {
-    const long long tiles = static_cast<long long>((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 8 * YC - 1) / (8 * YC));
-    const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, 8LL * kNumSms));
-    ASDSM_MARCH_DISPATCH(stencil2d_yc_kernel, nb2, 256);
+    // measured (configs 1-2): 8-row segments, a persistent grid of 4 CTAs per SM (more CTAs
+    // pay in the completion count and block scheduling, fewer leave HBM latency exposed)
+    constexpr int kYc = 8;
+    const long long tiles = static_cast<long long>((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 8 * kYc - 1) / (8 * kYc));
+    const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, 4LL * kNumSms));
+#define ASDSM_YC_DISPATCH(YCV)                                                                              \
+  do {                                                                                                      \
+    if (var) {                                                                                              \
+      if (mode == kMarchResidual) stencil2d_yc_kernel<kMarchResidual, true, YCV><<<nb2, 256, 0, s>>>(A);    \
+      else if (mode == kMarchUpdate) stencil2d_yc_kernel<kMarchUpdate, true, YCV><<<nb2, 256, 0, s>>>(A);   \
+      else stencil2d_yc_kernel<kMarchDots, true, YCV><<<nb2, 256, 0, s>>>(A);                              \
+    } else {                                                                                                \
+      if (mode == kMarchResidual) stencil2d_yc_kernel<kMarchResidual, false, YCV><<<nb2, 256, 0, s>>>(A);   \
+      else if (mode == kMarchUpdate) stencil2d_yc_kernel<kMarchUpdate, false, YCV><<<nb2, 256, 0, s>>>(A);  \
+      else stencil2d_yc_kernel<kMarchDots, false, YCV><<<nb2, 256, 0, s>>>(A);                             \
+    }                                                                                                       \
+  } while (0)
+    ASDSM_YC_DISPATCH(kYc);
+#undef ASDSM_YC_DISPATCH
   } else if (std::getenv("ASDSM_MARCH3D") == nullptr && mode != kMarchUpdate) {
     // measured (config 3/4): the barrier-free z-coarsened pass streams the residual and the
     // dot-product passes faster; the smem-plane march is faster for the 5-array update pass
