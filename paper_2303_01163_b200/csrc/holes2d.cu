@@ -295,10 +295,6 @@ __device__ __forceinline__ void stage_table(double* dst, const double* __restric
   }
 }
 
-__device__ __forceinline__ void cp_async_commit_wait() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-
 // One warp's share of the even/odd back transform: NA j tiles (32 S apart) x NB i tiles, an
 // E and an O accumulator per tile (K = kh each), the next k step's fragments loaded while the
 // current step's MMAs issue.  Static counts keep the MMAs unpredicated (the caller dispatches).

@@ -34,113 +34,6 @@ struct Src {
 };
 
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(TX2) march2d_kernel(MarchArgs A) {
-  DevState* S = A.state;
-  if (!S->active) return;
-  const int cur = S->cur;
-  double s = 0.0;
-  bool work = true;
-  if (MODE == kMarchUpdate) {
-    s = S->s;
-    work = s != 0.0 && (!A.retry_pass || S->retry);
-  }
-  if (MODE == kMarchDots) work = S->have_e != 0;
-  const int Nx = A.g.ext[0], Ny = A.g.ext[1];
-  const i64 sy = A.g.stride[1];
-  const Stencil& st = A.st;
-  const double* __restrict__ uu = cur ? A.u1 : A.u0;
-  const double* __restrict__ ee = A.e;
-  Src<MODE> V{uu, ee, s};
-  const double* __restrict__ rcur = cur ? A.r1 : A.r0;
-  double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
-  double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
-  __shared__ double row[2][TX2 + 2];
-  const int SY = A.strip;
-  const int ntx = (Nx + TX2 - 1) / TX2;
-  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-  const int x0 = tx * TX2, y0 = ty * SY;
-  const int y1 = min(y0 + SY, Ny);
-  const int t = threadIdx.x;
-  const int x = x0 + t;
-  const bool in = x < Nx;
-  const bool hl = t == 0 && x0 > 0;                        // loads the left halo
-  const bool hr = (t == TX2 - 1 || x == Nx - 1) && x + 1 < Nx;  // loads the right halo
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // ssq/num, max, esq/den, emax
-  if (work) {
-    // register pipeline: vd (y-1), vc (y), vu (y+1); raw loads of row y+2 and of the next
-    // halos / b / r are issued one row ahead so their latency overlaps the current row
-    double vd = (in && y0 > 0) ? V(x + (y0 - 1) * sy) : 0.0;
-    double vc = in ? V(x + y0 * sy) : 0.0;
-    double vu = (in && y0 + 1 < Ny) ? V(x + (y0 + 1) * sy) : 0.0;
-    double hL = hl ? V(x0 - 1 + y0 * sy) : 0.0;
-    double hR = hr ? V(x + 1 + y0 * sy) : 0.0;
-    double bq = (in && MODE != kMarchDots) ? __ldg(A.b + x + y0 * sy) : 0.0;
-    double rq = (in && MODE == kMarchDots) ? __ldg(rcur + x + y0 * sy) : 0.0;
-    double xq = (in && A.exact && MODE != kMarchDots) ? __ldg(A.exact + x + y0 * sy) : 0.0;
-    int buf = 0;
-    for (int y = y0; y < y1; ++y) {
-      const i64 p = x + y * sy;
-      // prefetch row y+2 (raw), next halos, next b / r / exact
-      double pu = 0.0, pe = 0.0, nL = 0.0, nR = 0.0, nb = 0.0, nr = 0.0, nx = 0.0;
-      if (in && y + 2 < Ny) {
-        pu = (MODE == kMarchDots) ? 0.0 : __ldg(uu + p + 2 * sy);
-        if (MODE != kMarchResidual) pe = __ldg(ee + p + 2 * sy);
-      }
-      if (y + 1 < y1) {
-        if (hl) nL = V(x0 - 1 + (y + 1) * sy);
-        if (hr) nR = V(x + 1 + (y + 1) * sy);
-        if (in && MODE != kMarchDots) nb = __ldg(A.b + p + sy);
-        if (in && MODE == kMarchDots) nr = __ldg(rcur + p + sy);
-        if (in && A.exact && MODE != kMarchDots) nx = __ldg(A.exact + p + sy);
-      }
-      row[buf][t + 1] = vc;
-      if (t == 0) row[buf][0] = hL;
-      if (t == TX2 - 1 || x == Nx - 1) row[buf][t + 2] = hR;
-      __syncthreads();
-      if (in) {
-        const i64 N = A.g.size;
-        auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
-        double acc = 0.0;
-        if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[1]), vd));
-        if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[0]), row[buf][t]));
-        acc = __dadd_rn(acc, __dmul_rn(C(2, st.diag), vc));
-        if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(3, st.right[0]), row[buf][t + 2]));
-        if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[1]), vu));
-        if (MODE == kMarchDots) {
-          a0 += rq * acc;
-          a2 += acc * acc;
-        } else {
-          double r = __dsub_rn(bq, acc);
-          if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
-          ro[p] = r;
-          if (MODE == kMarchUpdate) uo[p] = vc;
-          a0 += r * r;
-          a1 = fmax(a1, fabs(r));
-          if (A.exact) {
-            const double d = vc - xq;
-            a2 += d * d;
-            a3 = fmax(a3, fabs(d));
-          }
-        }
-      }
-      vd = vc;
-      vc = vu;
-      if (MODE == kMarchUpdate) vu = __dadd_rn(pu, __dmul_rn(s, pe));
-      else if (MODE == kMarchDots) vu = pe;
-      else vu = pu;
-      hL = nL;
-      hR = nR;
-      bq = nb;
-      rq = nr;
-      xq = nx;
-      buf ^= 1;
-    }
-  }
-  block_reduce4_march(a0, a1, a2, a3, A.partials);
-  fold_ctrl(A.ctrl, A.partials, S, A.history);
-}
-
-template <int MODE, bool VAR>
 __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
@@ -287,6 +180,7 @@ __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
   const double* __restrict__ rcur = cur ? A.r1 : A.r0;
   double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
   double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
+  double* __restrict__ sta = MODE == kMarchUpdate ? (cur ? A.sta0 : A.sta1) : (cur ? A.sta1 : A.sta0);
   const int ntx = (Nx + 31) / 32, nty = (Ny + 8 * YC - 1) / (8 * YC);
   const int ntiles = ntx * nty;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -295,6 +189,13 @@ __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
     const int bx = tile % ntx, by = tile / ntx;
     const int x = bx * 32 + tx, y0 = (by * 8 + ty) * YC;
     if (x >= Nx || y0 >= Ny) continue;
+    // slab-station copies (2D fast path): the column's x-station index, and the row remainder
+    // of y0 + 1 modulo n1 advanced incrementally (no divisions in the row loop)
+    int xst = -1, yrem = 0;
+    if (sta) {
+      if ((x + 1) % A.n[0] == 0 && (x + 1) / A.n[0] <= A.nc[0]) xst = (x + 1) / A.n[0] - 1;
+      yrem = (y0 + 1) % A.n[1];
+    }
     double vy[YC + 2];
 #pragma unroll
     for (int q = 0; q < YC + 2; ++q) {
@@ -324,6 +225,12 @@ __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
         if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
         ro[p] = r;
         if (MODE == kMarchUpdate) uo[p] = vc;
+        if (sta) {
+          if (xst >= 0) sta[static_cast<i64>(xst) * Ny + y] = r;
+          if (yrem == 0 && (y + 1) / A.n[1] <= A.nc[1])
+            sta[static_cast<i64>(A.nc[0]) * Ny + static_cast<i64>((y + 1) / A.n[1] - 1) * Nx + x] = r;
+          yrem = yrem + 1 == A.n[1] ? 0 : yrem + 1;
+        }
         a0 += r * r;
         a1 = fmax(a1, fabs(r));
         if (A.exact) {
@@ -465,10 +372,7 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
     }                                                                                   \
   } while (0)
-  static const bool march2d = std::getenv("ASDSM_MARCH2D") != nullptr;
-  if (A.g.dim == 2 && march2d) {
-    ASDSM_MARCH_DISPATCH(march2d_kernel, nb, TX2);
-  } else if (A.g.dim == 2) {
+  if (A.g.dim == 2) {
     // measured (configs 1-2): 8-row segments, a persistent grid of 4 CTAs per SM (more CTAs
     // pay in the completion count and block scheduling, fewer leave HBM latency exposed)
     constexpr int kYc = 8;

@@ -28,6 +28,12 @@ struct MarchArgs {
   int sparse;      // UPDATE: sparse_residual -- hole rows get r = 0 (solver.cpp:638-643)
   int n[3];        // refinement factors (hole-row test for sparse)
   const double* coef;  // variable coefficients: coef[slot * N + p] in CSR column order, or null
+  // 2D fast path: compact copies of the residual on the slab stations, one per residual
+  // buffer (sta0 <-> r0, sta1 <-> r1): [j < nc0][y] (x = (j+1) n0 - 1) then [j < nc1][x]
+  // (y = (j+1) n1 - 1) -- written by RESIDUAL / UPDATE so the slab gather reads them coalesced
+  double* sta0;
+  double* sta1;
+  int nc[2];
 };
 
 int march_strip(const FineGeom& g);

@@ -156,6 +156,93 @@ AxisEigen axis_eigen(int m, ld l, ld delta, ld r) {
   return e;
 }
 
+// Thomas solve of tridiag(l, b, r) (size n) for rhs f, with the pivots ipiv (long double).
+void thomas_ld(int n, ld l, ld r, const std::vector<ld>& ipiv, std::vector<ld>& x) {
+  for (int t = 0; t < n; ++t) x[static_cast<size_t>(t)] = (t == 0 ? x[0] : x[static_cast<size_t>(t)] - l * x[static_cast<size_t>(t - 1)]) * ipiv[static_cast<size_t>(t)];
+  for (int t = n - 2; t >= 0; --t) x[static_cast<size_t>(t)] -= r * ipiv[static_cast<size_t>(t)] * x[static_cast<size_t>(t + 1)];
+}
+
+// SepSolver::part tables (see plan.hpp): one warp solves a line of length m -- every lane a
+// Thomas over its segment, a warp-PCR over the separators, then the segment reconstruction.
+void build_partition_tables(SepSolver& s, int m, ld l, ld r, ld dL, const std::vector<cld>& sigma, DeviceAlloc& dev) {
+  // segment lengths the device solve is instantiated for (slabstep2d.cu)
+  static const int kSegs[] = {2, 4, 8, 12, 16, 20, 24, 28, 32};
+  int SEG = 0, M = 0, P = 0, last = 0;
+  for (int sg : kSegs) {
+    M = sg + 1;
+    P = (m + 1 + M - 1) / M;
+    last = m - (P - 1) * M;
+    if (P <= 32 && P >= 2 && last >= 1 && last <= sg) {
+      SEG = sg;
+      break;
+    }
+  }
+  if (SEG == 0) return;
+  const int R = P - 1;
+  const int stride = part_stride(SEG);
+  std::vector<double> tab(static_cast<size_t>(stride) * s.ncombo, 0.0);
+  for (int c = 0; c < s.ncombo; ++c) {
+    const ld b = dL + sigma[static_cast<size_t>(c)].real();
+    std::vector<ld> ipiv(static_cast<size_t>(SEG));
+    ld prev_cp = 0;
+    for (int t = 0; t < SEG; ++t) {
+      const ld w = t == 0 ? b : b - l * prev_cp;
+      if (w == 0) throw AsdsmError(kSingularMatrix, "zero pivot in a partitioned line solve");
+      ipiv[static_cast<size_t>(t)] = 1.0L / w;
+      prev_cp = r * ipiv[static_cast<size_t>(t)];
+    }
+    std::vector<ld> g(static_cast<size_t>(M - 1), 0.0L), h(static_cast<size_t>(M - 1), 0.0L), gl(static_cast<size_t>(last), 0.0L);
+    g[0] = l;
+    thomas_ld(M - 1, l, r, ipiv, g);
+    h[static_cast<size_t>(M - 2)] = r;
+    thomas_ld(M - 1, l, r, ipiv, h);
+    gl[0] = l;
+    thomas_ld(last, l, r, ipiv, gl);
+    // reduced system over the separators q < R
+    std::vector<ld> A(static_cast<size_t>(std::max(R, 1)), 0.0L), B(A.size(), 0.0L), C(A.size(), 0.0L);
+    for (int q = 0; q < R; ++q) {
+      const bool next_full = q + 1 < P - 1;
+      A[static_cast<size_t>(q)] = q >= 1 ? -l * g[static_cast<size_t>(M - 2)] : 0.0L;
+      B[static_cast<size_t>(q)] = b - l * h[static_cast<size_t>(M - 2)] - r * (next_full ? g[0] : gl[0]);
+      C[static_cast<size_t>(q)] = next_full ? -r * h[0] : 0.0L;
+    }
+    double* T = tab.data() + static_cast<size_t>(c) * stride;
+    for (int t = 0; t < SEG; ++t) {
+      T[t] = static_cast<double>(ipiv[static_cast<size_t>(t)]);
+      T[part_off_g(SEG) + t] = static_cast<double>(g[static_cast<size_t>(t)]);
+      T[part_off_h(SEG) + t] = static_cast<double>(h[static_cast<size_t>(t)]);
+      if (t < last) T[part_off_gl(SEG) + t] = static_cast<double>(gl[static_cast<size_t>(t)]);
+    }
+    for (int lev = 0, stp = 1; lev < 5; ++lev, stp <<= 1) {
+      std::vector<ld> A2(A.size()), B2(B.size()), C2(C.size());
+      for (int i = 0; i < R; ++i) {
+        ld f1 = 0, f2 = 0;
+        const bool lo = i - stp >= 0, hi = i + stp < R;
+        if (lo) f1 = A[static_cast<size_t>(i)] / B[static_cast<size_t>(i - stp)];
+        if (hi) f2 = C[static_cast<size_t>(i)] / B[static_cast<size_t>(i + stp)];
+        A2[static_cast<size_t>(i)] = lo ? -A[static_cast<size_t>(i - stp)] * f1 : 0.0L;
+        C2[static_cast<size_t>(i)] = hi ? -C[static_cast<size_t>(i + stp)] * f2 : 0.0L;
+        B2[static_cast<size_t>(i)] = B[static_cast<size_t>(i)] - (lo ? C[static_cast<size_t>(i - stp)] * f1 : 0.0L) -
+                                    (hi ? A[static_cast<size_t>(i + stp)] * f2 : 0.0L);
+        T[part_off_k1(SEG) + lev * 32 + i] = static_cast<double>(f1);
+        T[part_off_k2(SEG) + lev * 32 + i] = static_cast<double>(f2);
+      }
+      A.swap(A2);
+      B.swap(B2);
+      C.swap(C2);
+    }
+    for (int i = 0; i < R; ++i) {
+      if (B[static_cast<size_t>(i)] == 0) throw AsdsmError(kSingularMatrix, "zero pivot in a separator solve");
+      T[part_off_ib(SEG) + i] = static_cast<double>(1.0L / B[static_cast<size_t>(i)]);
+    }
+  }
+  s.part = upload(dev, tab);
+  s.part_seg = SEG;
+  s.part_P = P;
+  s.part_last = last;
+  s.part_stride = stride;
+}
+
 // Even/odd half of the sine factor of V = D S (plan.hpp SepSolver::half): rows i < ceil(m/2),
 // column col(k) = k/2 (k even) or kh + (k-1)/2 (k odd), zero padded; then scale_i and
 // (2/(m+1))/scale_i.  Row m-1-i of S is (-1)^k times row i, so a back transform needs only
@@ -339,6 +426,7 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
         invb[static_cast<size_t>(c) * m + i] = cld(1, 0) / B[static_cast<size_t>(i)];
       }
     }
+    if (!s.complex_modes && m <= kPartMaxLine && m >= 2) build_partition_tables(s, m, l, r, dL, sigma, dev);
     if (s.complex_modes) {
       s.pcr_k1 = upload(dev, to_interleaved(k1));
       s.pcr_k2 = upload(dev, to_interleaved(k2));

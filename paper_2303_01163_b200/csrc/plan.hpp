@@ -109,6 +109,15 @@ struct SepSolver {
   double* pcr_k1 = nullptr;   // [combo][level][pos]
   double* pcr_k2 = nullptr;
   double* pcr_invb = nullptr; // [combo][pos]
+  // Partition (separator) solve of one line by one warp (real modes, m <= kPartMaxLine): rows
+  // q*M + M-1 (q < P-1, M = SEG + 1) are separators, lane q owns the SEG rows between
+  // separators q-1 and q (the last lane m - (P-1) M <= SEG of them).  Per combo (stride
+  // part_stride = 4 SEG + 352):
+  //   [ipiv (SEG)] [g (SEG)] [h (SEG)] [g_last (SEG, zero padded)] [k1 (5 x 32)] [k2 (5 x 32)] [invb (32)]
+  // ipiv: Thomas pivots of a segment; g/h: its responses to the left/right separator couplings;
+  // k1/k2/invb: PCR of the reduced tridiagonal system over the P-1 separators.
+  double* part = nullptr;
+  int part_seg = 0, part_P = 0, part_last = 0, part_stride = 0;
   i64 mode_size() const { return static_cast<i64>(ext[0]) * ext[1] * (dim == 3 ? ext[2] : 1); }
 };
 
@@ -116,6 +125,16 @@ struct SepSolver {
 // rows = ceil(m/2) padded to a multiple of 8 (DMMA tile rows)
 __host__ __device__ inline int half_sine_kh(int m) { return (((m + 1) / 2) + 3) & ~3; }
 __host__ __device__ inline int half_sine_rows(int m) { return (((m + 1) / 2) + 7) & ~7; }
+
+constexpr int kPartMaxSeg = 32;                         // rows per lane (registers)
+constexpr int kPartMaxLine = 32 * (kPartMaxSeg + 1) - 2; // longest line the warp solve handles
+__host__ __device__ inline int part_off_g(int seg) { return seg; }
+__host__ __device__ inline int part_off_h(int seg) { return 2 * seg; }
+__host__ __device__ inline int part_off_gl(int seg) { return 3 * seg; }
+__host__ __device__ inline int part_off_k1(int seg) { return 4 * seg; }
+__host__ __device__ inline int part_off_k2(int seg) { return 4 * seg + 160; }
+__host__ __device__ inline int part_off_ib(int seg) { return 4 * seg + 320; }
+__host__ __device__ inline int part_stride(int seg) { return 4 * seg + 352; }
 
 struct DeviceAlloc {
   std::vector<void*> ptrs;

@@ -16,6 +16,8 @@ namespace {
 
 constexpr int kThreads = 1024;
 constexpr int kMaxSmem = 220 * 1024;
+constexpr int kSlabWBytes = 24 * 16;                 // station weights (nc <= 24, complex)
+constexpr int kSlabWOffset = kMaxSmem - kSlabWBytes;  // at the top of the dynamic area
 
 template <typename T>
 __device__ __forceinline__ T ld(const double* p, i64 i);
@@ -27,9 +29,18 @@ __device__ __forceinline__ cplx ld<cplx>(const double* p, i64 i) { return cplx{_
 __device__ __forceinline__ void st_out(double* p, i64 i, double v) { p[i] = v; }
 __device__ __forceinline__ void st_out(double* p, i64 i, cplx v) { reinterpret_cast<cplx*>(p)[i] = v; }
 
+#ifdef ASDSM_SLAB_TRACE
+#define SLAB_STAMP(i) T_[i] = clock64()
+#define SLAB_TRACE_DECL long long T_[6] = {clock64(), 0, 0, 0, 0, 0};
+#else
+#define SLAB_STAMP(i)
+#define SLAB_TRACE_DECL
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, const DevState* S) {
   if (!S->active) return;
+  SLAB_TRACE_DECL
   extern __shared__ unsigned char smem[];
   const int a = blockIdx.y, f = 1 - a;
   const MeshDev& m = A.m;
@@ -37,35 +48,54 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
   if (k >= nc) return;
   T* x0 = reinterpret_cast<T*>(smem);
   T* x1 = x0 + nf;
+  const int L = A.levels[a];
+  const double* K1 = A.k1[a];
+  const double* K2 = A.k2[a];
+  if (std::is_same<T, double>::value && A.pcr_smem) {
+    // every level's factors bulk-loaded next to the line, in flight during the gather
+    double* sk1 = reinterpret_cast<double*>(x1 + nf);
+    double* sk2 = sk1 + static_cast<i64>(L) * nf;
+    const i64 base = static_cast<i64>(k) * L * nf;
+    for (int i = threadIdx.x; i < L * nf; i += blockDim.x) {
+      cp_async8(sk1 + i, K1 + base + i);
+      cp_async8(sk2 + i, K2 + base + i);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   const double* rf = A.in_fine0 ? (S->cur ? A.in_fine1 : A.in_fine0) : nullptr;
+  const double* rs = A.sta0 ? (S->cur ? A.sta1 : A.sta0) + (a == 0 ? 0 : static_cast<i64>(m.nc[0]) * m.nf[1]) : nullptr;
   const i64 Nx = m.nf[0];
+  // station weights W[k][:] staged in shared memory (broadcast reads), after the PCR area
+  T* sw = reinterpret_cast<T*>(smem + kSlabWOffset);
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) sw[j] = ld<T>(A.W[a], static_cast<i64>(k) * nc + j);
+  __syncthreads();
+  constexpr int kChunk = 10;  // station values of one fine point in flight at once
   for (int x = threadIdx.x; x < nf; x += blockDim.x) {
     T acc = zero_of<T>();
-    for (int j0 = 0; j0 < nc; j0 += 8) {  // 8 independent station loads in flight
-      double v[8];
-      T w[8];
+    for (int j0 = 0; j0 < nc; j0 += kChunk) {
+      double v[kChunk];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < kChunk; ++q) {
         const int j = j0 + q;
         v[q] = 0.0;
-        w[q] = zero_of<T>();
         if (j < nc) {
-          const int fj = (j + 1) * m.n[a] - 1;  // station on the coarse axis
-          if (rf) v[q] = (a == 0) ? __ldg(rf + fj + Nx * x) : __ldg(rf + x + Nx * fj);
-          else v[q] = (a == 0) ? __ldg(A.in_slab[a] + j + static_cast<i64>(nc) * x) : __ldg(A.in_slab[a] + x + static_cast<i64>(nf) * j);
-          w[q] = ld<T>(A.W[a], static_cast<i64>(k) * nc + j);
+          if (rs) v[q] = __ldg(rs + static_cast<i64>(j) * nf + x);
+          else if (rf) {
+            const int fj = (j + 1) * m.n[a] - 1;  // station on the coarse axis
+            v[q] = (a == 0) ? __ldg(rf + fj + Nx * x) : __ldg(rf + x + Nx * fj);
+          } else {
+            v[q] = (a == 0) ? __ldg(A.in_slab[a] + j + static_cast<i64>(nc) * x) : __ldg(A.in_slab[a] + x + static_cast<i64>(nf) * j);
+          }
         }
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (j0 + q < nc) fma_acc(acc, w[q], v[q]);
+      for (int q = 0; q < kChunk; ++q)
+        if (j0 + q < nc) fma_acc(acc, sw[j0 + q], v[q]);
     }
     x0[x] = acc;
   }
   __syncthreads();
-  const int L = A.levels[a];
-  const double* K1 = A.k1[a];
-  const double* K2 = A.k2[a];
+  SLAB_STAMP(1);
   if constexpr (std::is_same<T, cplx>::value) {  // complex: coefficients straight from L2
     int s = 1;
     for (int lev = 0; lev < L; ++lev, s <<= 1) {
@@ -85,16 +115,12 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
       st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
     return;
   }
-  if (A.pcr_smem) {  // every level's factors bulk-loaded next to the line: pure smem PCR
+  if (A.pcr_smem) {  // pure shared-memory PCR over the staged factors
     double* sk1 = reinterpret_cast<double*>(x1 + nf);
     double* sk2 = sk1 + static_cast<i64>(L) * nf;
-    const i64 base = static_cast<i64>(k) * L * nf;
-    for (int i = threadIdx.x; i < L * nf; i += blockDim.x) {
-      cp_async8(sk1 + i, K1 + base + i);
-      cp_async8(sk2 + i, K2 + base + i);
-    }
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
+    SLAB_STAMP(2);
     int s = 1;
     for (int lev = 0; lev < L; ++lev, s <<= 1) {
       const double* c1 = sk1 + static_cast<i64>(lev) * nf;
@@ -110,8 +136,16 @@ __global__ void __launch_bounds__(kThreads) slab2d_fwd_kernel(Slab2DArgs A, cons
       x0 = x1;
       x1 = t;
     }
+    SLAB_STAMP(3);
     for (int i = threadIdx.x; i < nf; i += blockDim.x)
       st_out(A.modes[a], static_cast<i64>(k) * nf + i, x0[i] * ld<T>(A.invb[a], static_cast<i64>(k) * nf + i));
+#ifdef ASDSM_SLAB_TRACE
+    __syncthreads();
+    SLAB_STAMP(4);
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+      printf("SLABDBG fwd a %d gather %lld stage %lld pcr %lld out %lld\n", a, T_[1] - T_[0], T_[2] - T_[1],
+             T_[3] - T_[2], T_[4] - T_[3]);
+#endif
     return;
   }
   constexpr int E = 6;  // elements per thread (line length <= 6144)
@@ -161,6 +195,7 @@ __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, 
                                                                    double* history, CtrlArgs c, Skel2DArgs sk,
                                                                    int with_skel) {
   if (!S->active) return;
+  SLAB_TRACE_DECL
   const MeshDev& m = A.m;
   double ss[2] = {0.0, 0.0};
   for (int a = 0; a < 2; ++a) {
@@ -213,9 +248,18 @@ __global__ void __launch_bounds__(kRedThreads) slab2d_back_kernel(Slab2DArgs A, 
       }
     }
   }
+  SLAB_STAMP(1);
   if (fold_ctrl(c, partials, S, history) && with_skel) {
     __syncthreads();
+    SLAB_STAMP(2);
     if (S->have_e) skel2d_ccspline_block(sk);
+#ifdef ASDSM_SLAB_TRACE
+    __syncthreads();
+    SLAB_STAMP(3);
+    if (threadIdx.x == 0)
+      printf("SLABDBG back blk %d compute %lld fold %lld ccspline %lld\n", blockIdx.x, T_[1] - T_[0], T_[2] - T_[1],
+             T_[3] - T_[2]);
+#endif
   }
 }
 
@@ -236,8 +280,10 @@ void launch_slab2d_fwd(const Slab2DArgs& A, DevState* st, cudaStream_t s) {
   const int lmax = std::max(A.levels[0], A.levels[1]);
   const size_t smem_full = smem + 2 * static_cast<size_t>(lmax) * nfmax * sizeof(double);
   Slab2DArgs B = A;
-  B.pcr_smem = (!A.cplx && smem_full <= kMaxSmem) ? 1 : 0;
+  B.pcr_smem = (!A.cplx && smem_full <= kSlabWOffset) ? 1 : 0;
   if (B.pcr_smem) smem = smem_full;
+  if (smem > kSlabWOffset) throw AsdsmError(kUnsupported, "2D slab line longer than shared memory allows");
+  smem = kMaxSmem;  // station weights sit at kSlabWOffset
   if (!A.cplx && nfmax > 6 * kThreads) throw AsdsmError(kUnsupported, "2D slab line longer than 6144");
   if (smem > kMaxSmem) throw AsdsmError(kUnsupported, "2D slab line longer than shared memory allows");
   dim3 grid(static_cast<unsigned>(ncmax), 2);

@@ -17,6 +17,8 @@ struct Slab2DArgs {
   const double* in_fine0;         // error mode: fine residual buffers (state selects), else null
   const double* in_fine1;
   const double* in_slab[2];       // smooth mode: assembled slab rhs
+  const double* sta0;             // error mode: station copies of in_fine0 / in_fine1 (or null):
+  const double* sta1;             //   [j < nc0][y] then [j < nc1][x]  (MarchArgs::sta0)
   double* modes[2];               // mode buffers [k][x] (T)
   double* sol[2];                 // slab solutions, slab layout
   int pcr_smem;                   // set by the launcher: PCR factors staged in shared memory

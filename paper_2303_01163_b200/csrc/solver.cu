@@ -8,6 +8,7 @@
 #include "holes2d.cuh"
 #include "holes3d.cuh"
 #include "slab2d.cuh"
+#include "slabstep2d.cuh"
 #include "march.cuh"
 
 #include <algorithm>
@@ -199,7 +200,11 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
         sp_tab_[a] = dev_.alloc<double>(tab.size());
         ASDSM_CUDA_CHECK(cudaMemcpy(sp_tab_[a], tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
       }
+      for (int b = 0; b < 2; ++b)  // residual on the slab stations, one copy per residual buffer
+        stations_[b] = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * m.nf[1] + static_cast<size_t>(m.nc[1]) * m.nf[0]);
       seg1_ = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * 4 * (m.nc[0] + 1));
+      step2d_ = std::getenv("ASDSM_NO_SLABSTEP") == nullptr && slabstep2d_supported(md_, sep_slab_);
+      if (step2d_) slabstep2d_prepare();
       seg2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * 4 * (m.nc[1] + 1));
     }
   }
@@ -276,6 +281,29 @@ Skel2DArgs Solver::skel2d_args(const double* const* sol, const double* u_cc, con
   return a;
 }
 
+SlabStep2DArgs Solver::slabstep2d_args(const int* coin, double* out) const {
+  SlabStep2DArgs A{};
+  A.m = md_;
+  for (int a = 0; a < 2; ++a) {
+    const SepSolver& S = sep_slab_[a];
+    A.W[a] = S.W[a];
+    A.V[a] = S.V[a];
+    A.part[a] = S.part;
+    A.pseg[a] = S.part_seg;
+    A.pP[a] = S.part_P;
+    A.plast[a] = S.part_last;
+    A.pstride[a] = S.part_stride;
+    A.line_l[a] = S.line_left;
+    A.line_r[a] = S.line_right;
+    A.sp_tab[a] = sp_tab_[a];
+  }
+  A.sta0 = stations_[0];
+  A.sta1 = stations_[1];
+  A.coin = coin;
+  A.out = out;
+  return A;
+}
+
 void Solver::skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s) {
   if (mesh_.dim == 3) {
     Merge3DArgs A = m3_;
@@ -307,6 +335,15 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
 
 void Solver::march_launch(int mode, MarchArgs A, cudaStream_t s) {
   A.coef = coef_fine_;
+  A.sta0 = A.sta1 = nullptr;
+  if (fast2d_ && mode != kMarchDots && A.ro0 == r_[0] && A.ro1 == r_[1]) {
+    A.sta0 = stations_[0];
+    A.sta1 = stations_[1];
+    for (int a = 0; a < 2; ++a) {
+      A.nc[a] = mesh_.nc[a];
+      A.n[a] = mesh_.n[a];
+    }
+  }
   launch_march(mode, A, s);
 }
 
@@ -499,6 +536,15 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
     Slab2DArgs A = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
     A.in_fine0 = r0;
     A.in_fine1 = r1;
+    if (r0 == r_[0] && r1 == r_[1]) {  // the station copies the residual passes keep
+      A.sta0 = stations_[0];
+      A.sta1 = stations_[1];
+      if (step2d_) {  // slab solves + normalization + cc/spline + skeleton write, one launch
+        launch_slabstep2d(slabstep2d_args(coins_ + 4 * k, out), state_, s);
+        fill(out, nullptr, s);
+        return;
+      }
+    }
     const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
     const Skel2DArgs sk = skel2d_args(sol, nullptr, coins_ + 4 * k, out);
     launch_slab2d_fwd(A, state_, s);
@@ -841,14 +887,21 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     Slab2DArgs SA = slab2d_args(md_, sep_slab_, slab_modes_, sol_slab_);
     SA.in_fine0 = r_[0];
     SA.in_fine1 = r_[1];
+    SA.sta0 = stations_[0];
+    SA.sta1 = stations_[1];
     const double* sol[3] = {sol_slab_[0], sol_slab_[1], nullptr};
     const Skel2DArgs sk = skel2d_args(sol, nullptr, coins_, e_);
     const double cb = sep_slab_[0].complex_modes ? 16.0 : 8.0;
-    timed("slab2d_fwd_pcr", (8.0 + cb) * slab_pts, 0.0, iters, [&] { launch_slab2d_fwd(SA, state_, s); });
-    timed("slab2d_back_norms_ccspline", (8.0 + cb) * slab_pts, 0.0, iters,
-          [&] { launch_slab2d_back(SA, partials_, state_, history_, true, s, &sk); });
     const i64 nskel = static_cast<i64>(mesh_.nc[1]) * mesh_.nf[0] + static_cast<i64>(mesh_.nc[0]) * mesh_.nf[1];
-    timed("skeleton_write", 16.0 * nskel, 0.0, iters, [&] { launch_skel2d_write_fast(sk, state_, s); });
+    if (step2d_) {
+      timed("slabstep2d", 8.0 * slab_pts + 8.0 * nskel, 0.0, iters,
+            [&] { launch_slabstep2d(slabstep2d_args(coins_, e_), state_, s); });
+    } else {
+      timed("slab2d_fwd_pcr", (8.0 + cb) * slab_pts, 0.0, iters, [&] { launch_slab2d_fwd(SA, state_, s); });
+      timed("slab2d_back_norms_ccspline", (8.0 + cb) * slab_pts, 0.0, iters,
+            [&] { launch_slab2d_back(SA, partials_, state_, history_, true, s, &sk); });
+      timed("skeleton_write", 16.0 * nskel, 0.0, iters, [&] { launch_skel2d_write_fast(sk, state_, s); });
+    }
     Hole2DArgs A{};
     A.m0 = H.ext[0];
     A.m1 = H.ext[1];

@@ -12,6 +12,7 @@
 #include "sepsolve.cuh"
 #include "varcoef.hpp"
 #include "vthomas.cuh"
+#include "slabstep2d.cuh"
 
 namespace asdsm_b200 {
 
@@ -123,6 +124,8 @@ class Solver {
   Merge3DArgs m3_{};
   bool fast2d_ = false;          // fused 2D slab/skeleton/hole path
   double* slab_modes_[2] = {nullptr, nullptr};
+  double* stations_[2] = {nullptr, nullptr};  // residual on the slab stations (per residual buffer)
+  bool step2d_ = false;                          // one-launch slab step (slabstep2d.cu) eligible
   double* sp_tab_[2] = {nullptr, nullptr};
   double* seg1_ = nullptr;
   double* seg2_ = nullptr;
@@ -132,6 +135,7 @@ class Solver {
   size_t sub_cap_ = 0;
   int sub_m_ = 0;
   Skel2DArgs skel2d_args(const double* const* sol, const double* u_cc, const int* coin, double* out);
+  SlabStep2DArgs slabstep2d_args(const int* coin, double* out) const;
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
   double* partials_ = nullptr;
