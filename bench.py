@@ -254,20 +254,36 @@ def main():
              "gbs": cby[i] / (cms[i] / 1e3) / 1e9 if cms[i] > 0 else None,
              "tflops": cfl[i] / (cms[i] / 1e3) / 1e12 if cms[i] > 0 and cfl[i] > 0 else None}
         comps.append(c)
-    # dominant kernel of the solve (the components are the individual kernels of one iteration;
-    # on the generic/3D path hole_fill / slab_solves / skeleton_merge are kernel groups)
-    cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
-    dom = max(cand, key=lambda c: c["ms_per_launch"] * c["launches_per_solve"])
-    if dom["flops_per_launch"] > 0 and dom["flops_per_launch"] / max(dom["bytes_per_launch"], 1) > FP64_PEAK_TFLOPS * 1e3 / hbm:
-        ach = dom["flops_per_launch"] / (dom["ms_per_launch"] / 1e3) / 1e12
-        roof = {"kernel": dom["name"], "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "fp64 DMMA/DFMA peak measured with scripts/probe_fp64.cu (MEASURED_PEAKS has no fp64)"}
-    else:
-        ach = dom["bytes_per_launch"] / (dom["ms_per_launch"] / 1e3) / 1e9
-        roof = {"kernel": dom["name"], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+    # Rooflines.  The headline object is the fine-grid residual/update pass (north-star kernels 1
+    # and 4, the HBM-bound pass the >= 60 % target is stated for); every component gets its own
+    # entry in roofline_components, and the dominant kernel of the step is named with its bound
+    # (kernels that move < 1 MB per launch and do no GEMM work are latency bound: no roofline).
+    def roof_of(c):
+        if c["flops_per_launch"] > 0 and c["flops_per_launch"] / max(c["bytes_per_launch"], 1) > FP64_PEAK_TFLOPS * 1e3 / hbm:
+            ach = c["flops_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e12
+            return {"kernel": c["name"], "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                    "peak_source": "fp64 DMMA/DFMA peak measured with scripts/probe_fp64.cu (MEASURED_PEAKS has no fp64)"}
+        if c["bytes_per_launch"] < 1e6:
+            return {"kernel": c["name"], "bound": "latency", "achieved": None, "peak": None, "unit": None,
+                    "frac": None, "traffic": None,
+                    "note": "under 1 MB per launch on a handful of SMs: dependency-chain latency, not bandwidth"}
+        ach = c["bytes_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e9
+        return {"kernel": c["name"], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    roof["share_of_step"] = dom["ms_per_launch"] * dom["launches_per_solve"] / ms
+
+    cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
+    upd = next((c for c in comps if c["name"] == "update_residual"), cand[0])
+    roof = roof_of(upd)
+    roof["share_of_step"] = upd["ms_per_launch"] * upd["launches_per_solve"] / ms
+    dom = max(cand, key=lambda c: c["ms_per_launch"] * c["launches_per_solve"])
+    roof_dom = roof_of(dom)
+    roof_dom["share_of_step"] = dom["ms_per_launch"] * dom["launches_per_solve"] / ms
+    roof_all = []
+    for c in cand:
+        r = roof_of(c)
+        roof_all.append({"kernel": c["name"], "bound": r["bound"], "achieved": r["achieved"], "unit": r["unit"],
+                         "frac": r["frac"], "share_of_step": c["ms_per_launch"] * c["launches_per_solve"] / ms})
 
     # ---- e2e through the C-ABI with pinned host buffers
     b = ctx.bundle
@@ -338,6 +354,8 @@ def main():
                    "parallelism": f"replicas x{world}" if world > 1 else "1gpu"},
         "e2e": e2e,
         "roofline": roof,
+        "roofline_dominant": roof_dom,
+        "roofline_components": roof_all,
         "cpu_baseline": cpu,
         "gpu_launches": launches,
         "clocks": clocks,

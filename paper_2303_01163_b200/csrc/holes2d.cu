@@ -346,6 +346,85 @@ __device__ __forceinline__ void fused_gemm_eo(double (&ae)[4][2][2], double (&ao
   }
 }
 
+// Smooth-mode forward transform of a hole's rows on the DMMA pipe, in place in the mode tile:
+// sY holds h+ (columns [0, kh)) and h- ([kh, 2 kh)) of every row; the modes are
+// E(j, kappa) = sum_i h+(j, i) SH[i][kappa] -> column kappa (k = 2 kappa) and
+// O(j, kappa) = sum_i h-(j, i) SH[i][kh + kappa] -> column kh + kappa (k = 2 kappa + 1).
+// Accumulators stay in registers until every warp is done reading, then overwrite sY.
+template <int NA, int NB>
+__device__ __forceinline__ void fused_fwd_tiles(double (&ae)[4][2][2], double (&ao)[4][2][2], const double* pa,
+                                                const double* hcol, int kh) {
+  constexpr int S = kHole2DFusedStride;
+  for (int kk = 0; kk < kh; kk += 4) {
+    double fe[NA], fo[NA], ge[NB], go[NB];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      fe[a] = pa[a * 32 * S + kk];
+      fo[a] = pa[a * 32 * S + kh + kk];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {  // B(k = i, n = kappa) = SH[i][kappa]: column reads of the table
+      ge[b] = hcol[kk * S + b * 32];
+      go[b] = hcol[kk * S + kh + b * 32];
+    }
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        dmma_f64(ae[a][b], fe[a], ge[b]);
+        dmma_f64(ao[a][b], fo[a], go[b]);
+      }
+  }
+}
+
+__device__ __forceinline__ void fused_forward_eo(double* sY, const double* sH, int m0, int m1, int kh, int mh,
+                                                 int tid) {
+  constexpr int S = kHole2DFusedStride;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int jg = warp >> 2, ig = (warp + jg) & 3;
+  const int JP = (m1 + 7) & ~7;
+  const int jt = JP >> 3, it = (kh + 7) >> 3;
+  double ae[4][2][2], ao[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) ae[a][b][0] = ae[a][b][1] = ao[a][b][0] = ao[a][b][1] = 0.0;
+  const int r8 = lane >> 2, c4 = lane & 3;
+  const double* pa = sY + (jg * 8 + r8) * S + c4;
+  const double* hcol = sH + c4 * S + ig * 8 + r8;  // + kk * S (k = i row) + tile * 32 (n = kappa)
+  const int na = min(4, max(0, (jt - jg + 3) >> 2));
+  const int nb = min(2, max(0, (it - ig + 3) >> 2));
+  switch (na * 3 + nb) {
+#define ASDSM_FWD_CASE(NA, NB) \
+  case NA * 3 + NB:            \
+    fused_fwd_tiles<NA, NB>(ae, ao, pa, hcol, kh); \
+    break;
+    ASDSM_FWD_CASE(1, 1) ASDSM_FWD_CASE(1, 2) ASDSM_FWD_CASE(2, 1) ASDSM_FWD_CASE(2, 2)
+    ASDSM_FWD_CASE(3, 1) ASDSM_FWD_CASE(3, 2) ASDSM_FWD_CASE(4, 1) ASDSM_FWD_CASE(4, 2)
+#undef ASDSM_FWD_CASE
+    default:
+      break;
+  }
+  __syncthreads();  // every warp has read its h tiles
+  const int me = (m0 + 1) >> 1, mo = m0 >> 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int j = (jg + 4 * a) * 8 + r8;
+    if (a >= na || j >= m1) continue;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (b >= nb) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kap = (ig + 4 * b) * 8 + 2 * c4 + h;
+        if (kap < me) sY[j * S + kap] = ae[a][b][h];
+        if (kap < mo) sY[j * S + kh + kap] = ao[a][b][h];
+      }
+    }
+  }
+  (void)mh;
+}
+
 // Error-mode hole fill, one CTA per hole (holes up to 108 x 128):
 //   P0  pivots -> shared (cp.async) ; ring rhs from the skeleton
 //   P1  full forward transforms of the first / last ring rows, W = c S D^-1 applied through
@@ -356,8 +435,9 @@ __device__ __forceinline__ void fused_gemm_eo(double (&ae)[4][2][2], double (&ao
 //   P5  back transform on the DMMA pipe, even/odd split: E = X_even S_e^T, O = X_odd S_o^T
 //       over ceil(m0/2) rows -- half the MMAs of a dense V, and out(i) = sc_i (E + O),
 //       out(m0-1-i) = sc_{m0-1-i} (E - O) written straight into the fine array
+template <bool SMOOTH>
 __global__ void __launch_bounds__(kFusedThreads, 1)
-    hole2d_fused_kernel(double* __restrict__ e, Hole2DArgs A, const DevState* state) {
+    hole2d_fused_kernel(double* __restrict__ e, Hole2DArgs A, const double* __restrict__ bvec, const DevState* state) {
   if (!state->active || !state->have_e) return;
 #ifdef ASDSM_FUSED_TRACE  // per-phase clock64 stamps of CTAs 0 and 55, printed at the end
   long long T[8] = {clock64(), 0, 0, 0, 0, 0, 0, 0};
@@ -394,16 +474,27 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   stage_table(sP, A.ipiv, NP, m0, m0, S, tid);
   stage_table(sH, SH, hr, 2 * kh, 2 * kh, S, tid);
   asm volatile("cp.async.commit_group;\n" ::: "memory");
-  {  // zero the k padding of the mode tile (even / odd mode counts me / mo)
+  auto zero_kpad = [&]() {  // zero the k padding of the mode tile (even / odd mode counts me / mo)
     const int me = (m0 + 1) >> 1, mo = m0 >> 1;
     const int pe = kh - me, po = kh - mo;
     for (int t = tid; t < JP * (pe + po); t += kFusedThreads) {
       const int r = t / (pe + po), c = t % (pe + po);
       sY[r * S + (c < pe ? me + c : kh + mo + (c - pe))] = 0.0;
     }
-  }
+  };
+  if (!SMOOTH) zero_kpad();
   if (tid >= 128 && tid - 128 < m0) scs[tid - 128] = __ldg(sc + tid - 128);
-  if (tid < m1) {
+  const i64 Nxg = A.nf0;
+  if (SMOOTH) {
+    // smooth mode: rhs = b - A_hs skeleton on every hole row (hole_rhs_kernel's arithmetic),
+    // pre-scaled by c D^-1 for the forward transform: g(j, i) in natural columns
+    for (int t = tid; t < m1 * m0; t += kFusedThreads) {
+      const int j = t / m0, i = t - j * m0;
+      double f = __ldg(bvec + static_cast<i64>(oy + j) * Nxg + ox + i);
+      if (i == 0 || i == m0 - 1 || j == 0 || j == m1 - 1) f = __dadd_rn(f, ring_rhs(e, A, ox, oy, i, j));
+      sY[j * S + i] = f * __ldg(ci + i);
+    }
+  } else if (tid < m1) {
     fL[tid] = ring_rhs(e, A, ox, oy, 0, tid);
     fR[tid] = ring_rhs(e, A, ox, oy, m0 - 1, tid);
   } else if (tid >= 256 && tid - 256 < m0) {
@@ -420,7 +511,35 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const bool sweeper = side < 2 && k < m0;
   const int colk = (k & 1) ? kh + (k >> 1) : (k >> 1);
   double w0 = 0.0, wm = 0.0;
-  if (tid < mh) {  // pair sums of the pre-scaled ring rows: h+ (even k) and h- (odd k)
+  if (SMOOTH) {
+    // h+ / h- of every row into columns [0, kh) / [kh, 2 kh) in place (values read before the
+    // barrier, written after), K padding zeroed; then modes = h S^T on the DMMA pipe
+    constexpr int kPer = 14;  // >= ceil(128 * 54 / 512)
+    double hp[kPer], hm[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = tid + u * kFusedThreads, j = t / kh, i = t - j * kh;
+      hp[u] = hm[u] = 0.0;
+      if (j < m1 && i < mh) {
+        const double gi = sY[j * S + i], gm = sY[j * S + m0 - 1 - i];
+        const bool mid = (m0 - 1 - i) == i;
+        hp[u] = mid ? gi : gi + gm;
+        hm[u] = mid ? gi : gi - gm;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = tid + u * kFusedThreads, j = t / kh, i = t - j * kh;
+      if (j < JP) {
+        sY[j * S + i] = hp[u];
+        sY[j * S + kh + i] = hm[u];
+      }
+    }
+    __syncthreads();
+    fused_forward_eo(sY, sH, m0, m1, kh, mh, tid);
+    zero_kpad();
+  } else if (tid < mh) {  // pair sums of the pre-scaled ring rows: h+ (even k) and h- (odd k)
     const int i = tid, im = m0 - 1 - tid;
     hv[i] = im == i ? fB[i] : fB[i] + fB[im];
     hv[64 + i] = im == i ? fB[i] : fB[i] - fB[im];
@@ -428,7 +547,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     hv[192 + i] = im == i ? fT[i] : fT[i] - fT[im];
   }
   __syncthreads();
-  if (k < m0) {
+  if (!SMOOTH && k < m0) {
     const int g = tid >> 7;
     const int q = (mh + 3) >> 2;
     const int i0 = g * q, i1 = min(mh, i0 + q);
@@ -461,56 +580,56 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int n1 = side ? m1 - 1 - p : p + 1;  // rows this side eliminates
   const double* pv = sP + k;                 // pivot t of this mode: pv[t * S]
   if (sweeper) {
-    const double fb = ((part[k] + part[256 + k]) + part[512 + k]) + part[768 + k];
-    const double ft = ((part[128 + k] + part[384 + k]) + part[640 + k]) + part[896 + k];
+    // error mode: the mode-space rhs of interior rows is w0 fL + wm fR (ring-only rhs), the two
+    // boundary rows the full transforms fb / ft; smooth mode: read from the mode tile
+    const double fb = SMOOTH ? 0.0 : ((part[k] + part[256 + k]) + part[512 + k]) + part[768 + k];
+    const double ft = SMOOTH ? 0.0 : ((part[128 + k] + part[384 + k]) + part[640 + k]) + part[896 + k];
     const double cf = side ? rr : l, cb = side ? l : rr;
     double y;
     if (side == 0) {  // rows 0 .. p
       double* yv = sY + colk;
-      y = fb * pv[0];
+      y = (SMOOTH ? yv[0] : fb) * pv[0];
       yv[0] = y;
       int t = 1;
       for (; t + 8 <= n1; t += 8) {
-        double pq[8], lq[8], rq[8];
+        double pq[8], fq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           pq[q] = pv[(t + q) * S];
-          lq[q] = fL[t + q];
-          rq[q] = fR[t + q];
+          fq[q] = SMOOTH ? yv[(t + q) * S] : fma(wm, fR[t + q], w0 * fL[t + q]);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          y = (fma(wm, rq[q], w0 * lq[q]) - cf * y) * pq[q];
+          y = (fq[q] - cf * y) * pq[q];
           yv[(t + q) * S] = y;
         }
       }
       for (; t < n1; ++t) {
-        y = (fma(wm, fR[t], w0 * fL[t]) - cf * y) * pv[t * S];
+        y = ((SMOOTH ? yv[t * S] : fma(wm, fR[t], w0 * fL[t])) - cf * y) * pv[t * S];
         yv[t * S] = y;
       }
     } else {  // rows m1-1 .. p+1
       double* yv = sY + (m1 - 1) * S + colk;  // row m1-1-t at yv[-t * S]
       const double* fl = fL + (m1 - 1);
       const double* fr = fR + (m1 - 1);
-      y = ft * pv[0];
+      y = (SMOOTH ? yv[0] : ft) * pv[0];
       yv[0] = y;
       int t = 1;
       for (; t + 8 <= n1; t += 8) {
-        double pq[8], lq[8], rq[8];
+        double pq[8], fq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           pq[q] = pv[(t + q) * S];
-          lq[q] = fl[-(t + q)];
-          rq[q] = fr[-(t + q)];
+          fq[q] = SMOOTH ? yv[-(t + q) * S] : fma(wm, fr[-(t + q)], w0 * fl[-(t + q)]);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          y = (fma(wm, rq[q], w0 * lq[q]) - cf * y) * pq[q];
+          y = (fq[q] - cf * y) * pq[q];
           yv[-(t + q) * S] = y;
         }
       }
       for (; t < n1; ++t) {
-        y = (fma(wm, fr[-t], w0 * fl[-t]) - cf * y) * pv[t * S];
+        y = ((SMOOTH ? yv[-t * S] : fma(wm, fr[-t], w0 * fl[-t])) - cf * y) * pv[t * S];
         yv[-t * S] = y;
       }
     }
@@ -684,9 +803,11 @@ bool hole2d_fused_fits(int m0, int m1) {
          hole2d_fused_smem_bytes(m0, m1) <= kHole2DFusedMaxSmem;
 }
 
-void launch_hole2d_fused(double* e, const Hole2DArgs& A, DevState* state, cudaStream_t s) {
+void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevState* state, cudaStream_t s) {
   const size_t smem = hole2d_fused_smem_bytes(A.m0, A.m1);
-  hole2d_fused_kernel<<<static_cast<unsigned>(A.nbox0 * A.nbox1), kFusedThreads, smem, s>>>(e, A, state);
+  const unsigned grid = static_cast<unsigned>(A.nbox0 * A.nbox1);
+  if (b) hole2d_fused_kernel<true><<<grid, kFusedThreads, smem, s>>>(e, A, b, state);
+  else hole2d_fused_kernel<false><<<grid, kFusedThreads, smem, s>>>(e, A, nullptr, state);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }
@@ -699,7 +820,9 @@ void hole2d_prepare(size_t smem) {
                                         static_cast<int>(smem)));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fwd_thomas_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kHole2DFusedMaxSmem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kHole2DFusedMaxSmem)));
 }
 

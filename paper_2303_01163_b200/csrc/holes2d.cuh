@@ -27,7 +27,8 @@ constexpr size_t kHole2DFusedMaxSmem = 220 * 1024;
 constexpr int kHole2DFusedStride = 108;
 size_t hole2d_fused_smem_bytes(int m0, int m1);
 bool hole2d_fused_fits(int m0, int m1);
-void launch_hole2d_fused(double* e, const Hole2DArgs& A, DevState* state, cudaStream_t s);
+// b == nullptr: error mode (ring-only rhs); else smooth mode, rhs = b - A_hs skeleton
+void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevState* state, cudaStream_t s);
 size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem = false);
 void hole2d_prepare(size_t smem);
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);

@@ -361,9 +361,10 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
   }
   static const bool generic = std::getenv("ASDSM_GENERIC_FILL") != nullptr;
   const SepSolver& H = sep_hole_;
-  if (!generic && mesh_.dim == 2 && b == nullptr && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
-    // Error mode: ring rhs + analytic forward transform + Thomas (one kernel), then the DMMA
-    // back transform straight into the hole positions of the fine array.
+  if (!generic && mesh_.dim == 2 && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
+    // One fused kernel per hole (holes2d.cu) in both modes; for larger holes in error mode: ring
+    // rhs + analytic forward transform + Thomas (one kernel), then the DMMA back transform
+    // straight into the hole positions of the fine array.
     Hole2DArgs A{};
     A.m0 = H.ext[0];
     A.m1 = H.ext[1];
@@ -396,9 +397,38 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.line_right = H.line_right;
     static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
     if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
-      launch_hole2d_fused(e, A, state_, s);
+      launch_hole2d_fused(e, A, b, state_, s);
       return;
     }
+  }
+  if (!generic && mesh_.dim == 2 && b == nullptr && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
+    Hole2DArgs A{};
+    A.m0 = H.ext[0];
+    A.m1 = H.ext[1];
+    A.n0 = mesh_.n[0];
+    A.n1 = mesh_.n[1];
+    A.nf0 = mesh_.nf[0];
+    A.nf1 = mesh_.nf[1];
+    A.nbox0 = mesh_.nc[0] + 1;
+    A.nbox1 = mesh_.nc[1] + 1;
+    static const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
+    A.kb = 32;
+    A.tables_in_smem = (staged && hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 113 * 1024) ? 1 : 0;
+    if (!A.tables_in_smem) {
+      A.kb = 64;
+      A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
+      if (!A.y_in_smem && hole2d_smem_bytes(A.m0, A.m1, 32, true) <= 48 * 1024) {
+        A.kb = 32;  // narrower CTAs so the forward sweep stays in shared memory
+        A.y_in_smem = 1;
+      }
+    }
+    A.st = st_fine_;
+    A.Wt = H.Wt[0];
+    A.half = H.half[0];
+    A.ipiv = H.th_ipiv;
+    A.cp = H.th_cp;
+    A.line_left = H.line_left;
+    A.line_right = H.line_right;
     double* modes = static_cast<double*>(scratch0_);
     launch_hole2d_fwd_thomas(e, modes, A, state_, s);
     GemmLines G{};
@@ -928,7 +958,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
       // one kernel: ring rhs, sweeps, DMMA back transform (writes the hole interior once)
       timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
-            [&] { launch_hole2d_fused(e_, A, state_, s); });
+            [&] { launch_hole2d_fused(e_, A, nullptr, state_, s); });
     } else {
     timed("hole2d_fwd_thomas", 8.0 * NH * (A.y_in_smem ? 1.0 : 3.0), 0.0, iters,
           [&] { launch_hole2d_fwd_thomas(e_, static_cast<double*>(scratch0_), A, state_, s); });
