@@ -619,6 +619,57 @@ void launch_skel2d_write_fast(const Skel2DArgs& a, DevState* state, cudaStream_t
 
 // zero_clamped_spline + CubicSpline ctor (spline.cpp:9-37, 58-76): the knot-only terms, in
 // the reference's operation order (host compiled with -ffp-contract=off).
+// The skeleton correction along one axis is linear in the cross-point corrections: value at
+// fine index i = sum_I B[i][I] y_I for the zero-clamped natural spline through (0, 0), the
+// stations (y_I) and (1, 0) (spline.cpp).  B, evaluated exactly like spline_axis_table +
+// skel_seg_eval but in long double, turns the per-iteration spline phase into a small GEMM.
+std::vector<double> spline_basis_table(int nc, int n, double h, int nf) {
+  using ld = long double;
+  const int np = nc + 2, ni = nc;
+  std::vector<ld> x(static_cast<size_t>(np));
+  x[0] = 0.0L;
+  for (int c = 1; c <= nc; ++c) x[static_cast<size_t>(c)] = static_cast<ld>(static_cast<double>(static_cast<long long>(c) * n) * h);
+  x[static_cast<size_t>(np - 1)] = 1.0L;
+  std::vector<double> B(static_cast<size_t>(nf) * nc, 0.0);
+  for (int I = 0; I < nc; ++I) {
+    std::vector<ld> y(static_cast<size_t>(np), 0.0L), m(static_cast<size_t>(np), 0.0L);
+    y[static_cast<size_t>(I + 1)] = 1.0L;
+    // (hl/6) m_i + ((hl + hr)/3) m_{i+1} + (hr/6) m_{i+2} = rhs_i, m_0 = m_{np-1} = 0
+    std::vector<ld> a(static_cast<size_t>(ni)), d(static_cast<size_t>(ni)), c(static_cast<size_t>(ni)), r(static_cast<size_t>(ni));
+    for (int i = 0; i < ni; ++i) {
+      const ld hl = x[static_cast<size_t>(i + 1)] - x[static_cast<size_t>(i)];
+      const ld hr = x[static_cast<size_t>(i + 2)] - x[static_cast<size_t>(i + 1)];
+      a[static_cast<size_t>(i)] = hl / 6.0L;
+      d[static_cast<size_t>(i)] = (hl + hr) / 3.0L;
+      c[static_cast<size_t>(i)] = hr / 6.0L;
+      r[static_cast<size_t>(i)] = (y[static_cast<size_t>(i + 2)] - y[static_cast<size_t>(i + 1)]) / hr -
+                                  (y[static_cast<size_t>(i + 1)] - y[static_cast<size_t>(i)]) / hl;
+    }
+    for (int i = 1; i < ni; ++i) {
+      const ld wi = a[static_cast<size_t>(i)] / d[static_cast<size_t>(i - 1)];
+      d[static_cast<size_t>(i)] -= wi * c[static_cast<size_t>(i - 1)];
+      r[static_cast<size_t>(i)] -= wi * r[static_cast<size_t>(i - 1)];
+    }
+    for (int i = ni - 1; i >= 0; --i)
+      m[static_cast<size_t>(i + 1)] = (r[static_cast<size_t>(i)] - (i + 1 < ni ? c[static_cast<size_t>(i)] * m[static_cast<size_t>(i + 2)] : 0.0L)) /
+                                      d[static_cast<size_t>(i)];
+    for (int i = 0; i < nf; ++i) {
+      const int fi = i + 1;
+      int cs = fi / n;
+      if (cs > nc) cs = nc;
+      const ld hs = x[static_cast<size_t>(cs + 1)] - x[static_cast<size_t>(cs)];
+      const ld c1 = (y[static_cast<size_t>(cs + 1)] - y[static_cast<size_t>(cs)]) / hs -
+                    hs * (2.0L * m[static_cast<size_t>(cs)] + m[static_cast<size_t>(cs + 1)]) / 6.0L;
+      const ld c2 = m[static_cast<size_t>(cs)] / 2.0L;
+      const ld c3 = (m[static_cast<size_t>(cs + 1)] - m[static_cast<size_t>(cs)]) / (6.0L * hs);
+      const ld t = static_cast<ld>(static_cast<double>(fi) * h) - x[static_cast<size_t>(cs)];
+      const ld v = y[static_cast<size_t>(cs)] + t * (c1 + t * (c2 + t * c3));
+      B[static_cast<size_t>(i) * nc + I] = static_cast<double>(v);
+    }
+  }
+  return B;
+}
+
 std::vector<double> spline_axis_table(int nc, int n, double h) {
   const int np = nc + 2, ni = nc;
   std::vector<double> x(static_cast<size_t>(np));

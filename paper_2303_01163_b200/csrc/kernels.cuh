@@ -121,6 +121,8 @@ void launch_skel2d_ccspline_fast(const Skel2DArgs& a, DevState* state, cudaStrea
 void launch_skel2d_write_fast(const Skel2DArgs& a, DevState* state, cudaStream_t s);
 // host: the data-independent spline terms of one axis (bitwise the reference's values)
 std::vector<double> spline_axis_table(int nc, int n, double h);
+// host: skeleton-correction basis of one axis, B[i][I] (nf x nc) -- see kernels.cu
+std::vector<double> spline_basis_table(int nc, int n, double h, int nf);
 
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
                      DevState* state, cudaStream_t s);

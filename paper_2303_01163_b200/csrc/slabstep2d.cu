@@ -6,7 +6,8 @@
 // scatters the skeleton into the fine array.  Here a cluster of two CTAs does all of it in one
 // launch, CTA a owning slab a (coarse along axis a):
 //   P1  the residual on the slab's stations (compact copy kept by the residual passes), the
-//       eigenvector blocks and the line-solve tables -> shared memory
+//       eigenvector blocks and the line-solve tables -> shared memory; every CTA of a slab
+//       takes a quarter of the fine points (a cluster of 8 CTAs, four per slab)
 //   P2  transform along the coarse axis on the DMMA pipe: nc mode lines of nf fine points
 //   P3  one warp per mode line: partitioned tridiagonal solve -- every lane a Thomas sweep over
 //       its SEG-row segment (in registers), a shuffle-PCR over the separators, the segment
@@ -19,7 +20,6 @@
 // Divisions by mesh constants and by the slab norms are reciprocal multiplies here (the
 // reference divides): values agree to an ulp, far inside the 1e-10 parity tolerance.
 #include "slabstep2d.cuh"
-#include "skel2d.cuh"
 
 #include <cooperative_groups.h>
 
@@ -29,20 +29,26 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int kStepThreads = 320;  // 10 warps: one mode line per warp for nc <= 10
+constexpr int kStepThreads = 256;
 constexpr int kStepWarps = kStepThreads / 32;
 constexpr int kStepMaxNc = 24;
-constexpr int kRecip = 5 * kStepMaxNc;  // per spline family: 1/hl, 1/hr, 1/dg (nc), 1/h, 1/(6h) (nc+1)
+constexpr int kSlabCtas = 4;                 // CTAs per slab; the cluster is both slabs
+constexpr int kClusterCtas = 2 * kSlabCtas;
+constexpr int kOwnMax = (kStepMaxNc + kSlabCtas - 1) / kSlabCtas;  // mode lines one CTA solves
 
 struct StepLayout {
-  int NC, NF, PS;
-  int st, md, wv, pt, cr1, cr2, nrm, ce1, ce2, stab, rcp, srhs, smm, sg1, sg2, red, total;
+  int NC, XR, NF, PS;
+  int st, md, ml, wv, pt, cr1, cr2, nrm, ce1, ce2, bas, red, total;
 };
+
+// x-range of part c of a line of n points
+__host__ __device__ inline int xr_begin(int n, int c) { return (n * c) / kSlabCtas; }
 
 __host__ __device__ inline StepLayout step_layout(const MeshDev& m, int pstride) {
   StepLayout L{};
   L.NC = m.nc[0] > m.nc[1] ? m.nc[0] : m.nc[1];
   L.NF = m.nf[0] > m.nf[1] ? m.nf[0] : m.nf[1];
+  L.XR = (L.NF + kSlabCtas - 1) / kSlabCtas + 1;
   L.PS = pstride;
   const int ncc = m.nc[0] * m.nc[1];
   int o = 0;
@@ -51,21 +57,17 @@ __host__ __device__ inline StepLayout step_layout(const MeshDev& m, int pstride)
     o += (n + 1) & ~1;  // keep 16-byte alignment of every region
     return r;
   };
-  L.st = take(L.NC * L.NF);
-  L.md = take(L.NC * L.NF);
+  L.st = take(L.NC * L.XR);          // stations of this x-range, then the slab solution there
+  L.md = take(L.NC * L.XR);          // modes of this x-range
+  L.ml = take(kOwnMax * L.NF);       // full mode lines this CTA solves
   L.wv = take(2 * L.NC * L.NC);
-  L.pt = take(L.NC * pstride);
+  L.pt = take(kOwnMax * pstride);
   L.cr1 = take(ncc);
   L.cr2 = take(ncc);
-  L.nrm = take(2);
+  L.nrm = take(kClusterCtas);
   L.ce1 = take(ncc);
   L.ce2 = take(ncc);
-  L.stab = take(2 * kSkelTabMax);
-  L.rcp = take(2 * kRecip);
-  L.srhs = take((m.nc[0] + m.nc[1]) * kStepMaxNc);
-  L.smm = take((m.nc[0] + m.nc[1]) * (kStepMaxNc + 2));
-  L.sg1 = take(m.nc[1] * 4 * (m.nc[0] + 1));
-  L.sg2 = take(m.nc[0] * 4 * (m.nc[1] + 1));
+  L.bas = take(L.XR * L.NC);        // this x-range's rows of the skeleton-correction basis
   L.red = take(32);
   L.total = o;
   return L;
@@ -77,11 +79,11 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// C[nc][nf] = Amat[nc][nc] * B[nc][nf] (B, C in shared memory; MT = ceil(nc/8) row tiles,
-// KS = ceil(nc/4) k steps of m8n8k4), warps over the 8-column tiles; returns the warp's sum of
-// squares of C when kNorm.
+// C[nc][ld] = Amat[nc][nc] * B[nc][ld] over the first nx columns (B, C in shared memory;
+// MT = ceil(nc/8) row tiles, KS = ceil(nc/4) k steps of m8n8k4), warps over 8-column tiles;
+// returns the warp's sum of squares of C when kNorm.
 template <int MT, int KS, bool kNorm>
-__device__ __forceinline__ double small_gemm(const double* Amat, const double* B, double* C, int nc, int nf) {
+__device__ __forceinline__ double small_gemm(const double* Amat, const double* B, double* C, int nc, int nx, int ld) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r8 = lane >> 2, c4 = lane & 3;
   double a[MT][KS];
 #pragma unroll
@@ -92,14 +94,14 @@ __device__ __forceinline__ double small_gemm(const double* Amat, const double* B
       a[mt][ks] = (row < nc && k < nc) ? Amat[row * nc + k] : 0.0;
     }
   double ss = 0.0;
-  const int ntiles = (nf + 7) >> 3;
+  const int ntiles = (nx + 7) >> 3;
   for (int nt = warp; nt < ntiles; nt += kStepWarps) {
     const int n0 = nt * 8;
     double b[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = ks * 4 + c4;
-      b[ks] = (k < nc && n0 + r8 < nf) ? B[k * nf + n0 + r8] : 0.0;
+      b[ks] = (k < nc && n0 + r8 < nx) ? B[k * ld + n0 + r8] : 0.0;
     }
     double acc[MT][2];
 #pragma unroll
@@ -114,8 +116,8 @@ __device__ __forceinline__ double small_gemm(const double* Amat, const double* B
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + 2 * c4 + h;
-        if (row < nc && col < nf) {
-          C[row * nf + col] = acc[mt][h];
+        if (row < nc && col < nx) {
+          C[row * ld + col] = acc[mt][h];
           if (kNorm) ss += acc[mt][h] * acc[mt][h];
         }
       }
@@ -125,13 +127,13 @@ __device__ __forceinline__ double small_gemm(const double* Amat, const double* B
 }
 
 template <bool kNorm>
-__device__ __forceinline__ double gemm_dispatch(const double* Amat, const double* B, double* C, int nc, int nf) {
-  if (nc <= 4) return small_gemm<1, 1, kNorm>(Amat, B, C, nc, nf);
-  if (nc <= 8) return small_gemm<1, 2, kNorm>(Amat, B, C, nc, nf);
-  if (nc <= 12) return small_gemm<2, 3, kNorm>(Amat, B, C, nc, nf);
-  if (nc <= 16) return small_gemm<2, 4, kNorm>(Amat, B, C, nc, nf);
-  if (nc <= 20) return small_gemm<3, 5, kNorm>(Amat, B, C, nc, nf);
-  return small_gemm<3, 6, kNorm>(Amat, B, C, nc, nf);
+__device__ __forceinline__ double gemm_dispatch(const double* Amat, const double* B, double* C, int nc, int nx, int ld) {
+  if (nc <= 4) return small_gemm<1, 1, kNorm>(Amat, B, C, nc, nx, ld);
+  if (nc <= 8) return small_gemm<1, 2, kNorm>(Amat, B, C, nc, nx, ld);
+  if (nc <= 12) return small_gemm<2, 3, kNorm>(Amat, B, C, nc, nx, ld);
+  if (nc <= 16) return small_gemm<2, 4, kNorm>(Amat, B, C, nc, nx, ld);
+  if (nc <= 20) return small_gemm<3, 5, kNorm>(Amat, B, C, nc, nx, ld);
+  return small_gemm<3, 6, kNorm>(Amat, B, C, nc, nx, ld);
 }
 
 // One line of mode space (length n, in shared memory, in place) by one warp; T = this mode's
@@ -199,40 +201,15 @@ __device__ __forceinline__ void part_solve_line(double* line, const double* T, i
   if (q < R) line[base + M - 1] = xs;
 }
 
-__device__ __forceinline__ void solve_dispatch(int seg, double* line, const double* T, int n, int P, int last, double l, double r) {
-  switch (seg) {
-#define ASDSM_SEG(S_) \
-  case S_:            \
-    part_solve_line<S_>(line, T, n, P, last, l, r); \
-    break;
-    ASDSM_SEG(2) ASDSM_SEG(4) ASDSM_SEG(8) ASDSM_SEG(12) ASDSM_SEG(16) ASDSM_SEG(20) ASDSM_SEG(24) ASDSM_SEG(28)
-    ASDSM_SEG(32)
-#undef ASDSM_SEG
-    default:
-      break;
-  }
-}
-
-// segment index of fine index fi (1-based) on an axis with factor n: fi / n clamped to nc,
-// without an integer division
-__device__ __forceinline__ int seg_of(int fi, int n, float invn, int nc) {
-  int c = __float2int_rd(__int2float_rn(fi) * invn);
-  if ((c + 1) * n <= fi) ++c;
-  else if (c * n > fi) --c;
-  return c > nc ? nc : c;
-}
-
-__device__ __forceinline__ double seg_eval(const double* tab, const double* seg, int c, double x) {
-  const double t = __dsub_rn(x, tab[c]);
-  const double* s = seg + 4 * c;
-  return __dadd_rn(s[0], __dmul_rn(t, __dadd_rn(s[1], __dmul_rn(t, __dadd_rn(s[2], __dmul_rn(t, s[3]))))));
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kStepThreads, 1)
+// Cluster of 2 x kSlabCtas CTAs: CTA (a, c) owns slab a's fine x-range c (stations, transforms,
+// solution, skeleton write) and the mode lines k = c, c + kSlabCtas, ... (line solves); the
+// mode lines move between the two ownerships through distributed shared memory.
+template <int SEG>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThreads, 1)
     slabstep2d_kernel(SlabStep2DArgs A, DevState* S) {
-  if (!S->active) return;  // same decision in both CTAs of the cluster
+  if (!S->active) return;  // same decision in every CTA of the cluster
 #ifdef ASDSM_STEP_TRACE
-  long long T_[10] = {clock64(), 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long T_[12] = {clock64(), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #define STEP_STAMP(i) T_[i] = clock64()
 #else
 #define STEP_STAMP(i)
@@ -242,98 +219,108 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kStepThreads, 1)
   const MeshDev& m = A.m;
   const int PS = A.pstride[0] > A.pstride[1] ? A.pstride[0] : A.pstride[1];
   const StepLayout Lo = step_layout(m, PS);
-  const int a = static_cast<int>(cluster.block_rank()), f = 1 - a;
-  const int nc = m.nc[a], nf = m.nf[f];
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int a = rank / kSlabCtas, c = rank % kSlabCtas;
+  const int nc = m.nc[a], nf = m.nf[1 - a];
+  const int x0 = xr_begin(nf, c), nx = xr_begin(nf, c + 1) - x0, XR = Lo.XR;
   const int nc0 = m.nc[0], nc1 = m.nc[1], ncc = nc0 * nc1;
+  const int nown = (nc - c + kSlabCtas - 1) / kSlabCtas;  // modes c, c + C, ... < nc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* st = sm + Lo.st;
   double* md = sm + Lo.md;
+  double* ml = sm + Lo.ml;
   double* sW = sm + Lo.wv;
   double* sV = sW + nc * nc;
   double* pt = sm + Lo.pt;
-  double* stab = sm + Lo.stab;
-  double* rcp = sm + Lo.rcp;
-  // P1
+  // P1: this x-range of the stations, the eigenvector blocks, the owned modes' line tables
   const double* rs = (S->cur ? A.sta1 : A.sta0) + (a == 0 ? 0 : static_cast<i64>(nc0) * m.nf[1]);
-  // bulk loads: cp.async keeps every request in flight (a load -> shared store loop would
-  // wait one L2 round trip per element)
-  for (int i = tid; i < nc * nf; i += kStepThreads) cp_async8(st + i, rs + i);
+  for (int i = tid; i < nc * nx; i += kStepThreads) {
+    const int j = i / nx, x = i - j * nx;
+    cp_async8(st + j * XR + x, rs + static_cast<i64>(j) * nf + x0 + x);
+  }
   for (int i = tid; i < nc * nc; i += kStepThreads) {
     cp_async8(sW + i, A.W[a] + i);
     cp_async8(sV + i, A.V[a] + i);
   }
-  for (int i = tid; i < nc * A.pstride[a]; i += kStepThreads) cp_async8(pt + i, A.part[a] + i);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  for (int fam = 0; fam < 2; ++fam) {  // spline tables and the reciprocals of their widths
-    const int ncf = m.nc[fam], tl = (ncf + 2) + 5 * ncf;
-    const double* src = A.sp_tab[fam];
-    double* dt = stab + fam * kSkelTabMax;
-    double* dr = rcp + fam * kRecip;
-    for (int q = tid; q < tl; q += kStepThreads) cp_async8(dt + q, src + q);
-    for (int q = tid; q < 5 * kStepMaxNc; q += kStepThreads) {
-      const int kind = q / kStepMaxNc, i = q % kStepMaxNc;
-      double v = 0.0;
-      if (kind == 0 && i < ncf) v = 1.0 / __ldg(src + ncf + 2 + i);               // 1 / hl
-      else if (kind == 1 && i < ncf) v = 1.0 / __ldg(src + 2 * ncf + 2 + i);      // 1 / hr
-      else if (kind == 2 && i < ncf) v = 1.0 / __ldg(src + 4 * ncf + 2 + i);      // 1 / diag
-      else if (kind >= 3 && i <= ncf) {
-        const double h = __dsub_rn(__ldg(src + i + 1), __ldg(src + i));
-        v = kind == 3 ? 1.0 / h : 1.0 / __dmul_rn(6.0, h);
-      }
-      dr[q] = v;
-    }
+  for (int i = tid; i < nown * A.pstride[a]; i += kStepThreads) {
+    const int u = i / A.pstride[a], o = i - u * A.pstride[a];
+    cp_async8(pt + u * PS + o, A.part[a] + static_cast<i64>(c + u * kSlabCtas) * A.pstride[a] + o);
   }
+  // skeleton-correction basis of this slab's fine axis (1 - a), rows x0 .. x0 + nx
+  const int ncb = m.nc[1 - a];
+  double* bas = sm + Lo.bas;
+  for (int i = tid; i < nx * ncb; i += kStepThreads) cp_async8(bas + i, A.basis[1 - a] + static_cast<i64>(x0) * ncb + i);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   STEP_STAMP(1);
-  // P2: md = W st
-  gemm_dispatch<false>(sW, st, md, nc, nf);
+  // P2: md = W st on this x-range, then every mode row to its owner's full line (DSMEM)
+  gemm_dispatch<false>(sW, st, md, nc, nx, XR);
   __syncthreads();
+  for (int i = tid; i < nc * nx; i += kStepThreads) {
+    const int k = i / nx, x = i - k * nx;
+    double* dst = cluster.map_shared_rank(ml, a * kSlabCtas + k % kSlabCtas);
+    dst[(k / kSlabCtas) * Lo.NF + x0 + x] = md[k * XR + x];
+  }
+  cluster.sync();
   STEP_STAMP(2);
-  // P3
-  for (int k = warp; k < nc; k += kStepWarps)
-    solve_dispatch(A.pseg[a], md + k * nf, pt + k * A.pstride[a], nf, A.pP[a], A.plast[a], A.line_l[a], A.line_r[a]);
-  __syncthreads();
+  // P3: one warp per owned mode line
+  if (warp < nown) {
+    const int k = c + warp * kSlabCtas;
+    (void)k;
+    part_solve_line<SEG>(ml + warp * Lo.NF, pt + warp * PS, nf, A.pP[a], A.plast[a], A.line_l[a], A.line_r[a]);
+  }
+  STEP_STAMP(10);
+  cluster.sync();
   STEP_STAMP(3);
-  // P4: sol = V md -> st, squared norm
-  double ss = gemm_dispatch<true>(sV, md, st, nc, nf);
+  // P4: pull this x-range of every mode line back, sol = V md, squared norm
+  for (int i = tid; i < nc * nx; i += kStepThreads) {
+    const int k = i / nx, x = i - k * nx;
+    const double* src = cluster.map_shared_rank(ml, a * kSlabCtas + k % kSlabCtas);
+    md[k * XR + x] = src[(k / kSlabCtas) * Lo.NF + x0 + x];
+  }
+  __syncthreads();
+  double ss = gemm_dispatch<true>(sV, md, st, nc, nx, XR);
   double* red = sm + Lo.red;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
   if (lane == 0) red[warp] = ss;
   __syncthreads();
   STEP_STAMP(4);
-  // P5: exchange the norm and the cross values with the peer CTA
+  // P5: norms (per-CTA partials to every CTA, summed in rank order) and cross values
   double* nrm = sm + Lo.nrm;
   double* cr1 = sm + Lo.cr1;  // u_fc at the cross points (slab 1)
   double* cr2 = sm + Lo.cr2;  // u_cf at the cross points (slab 0)
-  double* peer_nrm = cluster.map_shared_rank(nrm, 1 - a);
-  double* peer_cr = cluster.map_shared_rank(a == 1 ? cr1 : cr2, 1 - a);
-  if (tid == 0) {
+  if (tid < kClusterCtas) {
     double t = 0.0;
     for (int w = 0; w < kStepWarps; ++w) t += red[w];
-    nrm[a] = t;
-    peer_nrm[a] = t;
+    cluster.map_shared_rank(nrm, tid)[rank] = t;
   }
-  for (int t = tid; t < ncc; t += kStepThreads) {
-    const int I = t % nc0, J = t / nc0;
-    double v;
-    if (a == 1) v = st[J * nf + (I + 1) * m.n[0] - 1];  // u_fc(x = station I, J)
-    else v = st[I * nf + (J + 1) * m.n[1] - 1];         // u_cf(I, y = station J)
-    (a == 1 ? cr1 : cr2)[t] = v;
-    peer_cr[t] = v;
+  for (int t = tid; t < ncc * kClusterCtas; t += kStepThreads) {
+    const int dst = t / ncc, q = t - dst * ncc;
+    const int I = q % nc0, J = q / nc0;
+    const int x = a == 1 ? (I + 1) * m.n[0] - 1 : (J + 1) * m.n[1] - 1;  // along this slab's fine axis
+    if (x < x0 || x >= x0 + nx) continue;
+    const double v = a == 1 ? st[J * XR + x - x0] : st[I * XR + x - x0];
+    cluster.map_shared_rank(a == 1 ? cr1 : cr2, dst)[q] = v;
   }
   cluster.sync();
   STEP_STAMP(5);
-  const double ncf = sqrt(nrm[0]), nfc = sqrt(nrm[1]);
-  if (a == 0 && tid == 0) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int r = 0; r < kSlabCtas; ++r) {
+    s0 += nrm[r];
+    s1 += nrm[kSlabCtas + r];
+  }
+  const double ncf = sqrt(s0), nfc = sqrt(s1);
+  if (rank == 0 && tid == 0) {
     S->slab_norm[0] = ncf;
     S->slab_norm[1] = nfc;
     if (!(ncf > 0.0) || !(nfc > 0.0)) S->have_e = 0;
   }
   if (!(ncf > 0.0) || !(nfc > 0.0)) return;  // ZeroNormSolution: no correction this step
   const double ifc = 1.0 / nfc, icf = 1.0 / ncf;
-  // P6: corrections at the cross points (error mode: the coin picks the slab), spline segments
+  STEP_STAMP(9);
+  // P6: corrections at the cross points (error mode: the coin picks the slab)
   double* ce1 = sm + Lo.ce1;
   double* ce2 = sm + Lo.ce2;
   const bool take_fc = A.coin[0] != 0;
@@ -344,115 +331,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kStepThreads, 1)
     ce2[t] = __dsub_rn(uh, u2);
   }
   __syncthreads();
-  double* srhs = sm + Lo.srhs;  // [line][i], lines: nc1 along x then nc0 along y
-  double* smm = sm + Lo.smm;    // [line][c]
-  double* sg1 = sm + Lo.sg1;
-  double* sg2 = sm + Lo.sg2;
-  const int nlines = nc0 + nc1;
-  auto yval = [&](int line, int c) -> double {
-    if (line < nc1) return (c == 0 || c == nc0 + 1) ? 0.0 : ce1[(c - 1) + nc0 * line];
-    const int I = line - nc1;
-    return (c == 0 || c == nc1 + 1) ? 0.0 : ce2[I + nc0 * (c - 1)];
-  };
-  for (int t = tid; t < 2 * ncc; t += kStepThreads) {
-    const int line = t < ncc ? t / nc0 : nc1 + (t - ncc) / nc1;
-    const int i = t < ncc ? t % nc0 : (t - ncc) % nc1;
-    const double* rr = rcp + (line < nc1 ? 0 : kRecip);
-    srhs[line * kStepMaxNc + i] = __dsub_rn(__dmul_rn(__dsub_rn(yval(line, i + 2), yval(line, i + 1)), rr[kStepMaxNc + i]),
-                                            __dmul_rn(__dsub_rn(yval(line, i + 1), yval(line, i)), rr[i]));
-  }
-  __syncthreads();
-  for (int line = tid; line < nlines; line += kStepThreads) {
-    const int ni = line < nc1 ? nc0 : nc1, n = ni + 2;
-    const double* tab = stab + (line < nc1 ? 0 : kSkelTabMax);
-    const double* rr = rcp + (line < nc1 ? 0 : kRecip);
-    const double* w = tab + n + 2 * ni;
-    const double* up = w + 2 * ni;
-    double* rhs = srhs + line * kStepMaxNc;
-    double* mm = smm + line * (kStepMaxNc + 2);
-    for (int i = 1; i < ni; ++i) rhs[i] = __dsub_rn(rhs[i], __dmul_rn(w[i], rhs[i - 1]));
-    mm[0] = 0.0;
-    mm[n - 1] = 0.0;
-    if (ni > 0) {
-      mm[ni] = __dmul_rn(rhs[ni - 1], rr[2 * kStepMaxNc + ni - 1]);
-      for (int i = ni - 1; i >= 1; --i)
-        mm[i] = __dmul_rn(__dsub_rn(rhs[i - 1], __dmul_rn(up[i - 1], mm[i + 1])), rr[2 * kStepMaxNc + i - 1]);
-    }
-  }
-  __syncthreads();
-  for (int t = tid; t < nc1 * (nc0 + 1) + nc0 * (nc1 + 1); t += kStepThreads) {
-    int line, c;
-    if (t < nc1 * (nc0 + 1)) {
-      line = t / (nc0 + 1);
-      c = t % (nc0 + 1);
-    } else {
-      line = nc1 + (t - nc1 * (nc0 + 1)) / (nc1 + 1);
-      c = (t - nc1 * (nc0 + 1)) % (nc1 + 1);
-    }
-    const double* x = stab + (line < nc1 ? 0 : kSkelTabMax);
-    const double* rr = rcp + (line < nc1 ? 0 : kRecip);
-    const double* mm = smm + line * (kStepMaxNc + 2);
-    const double y0 = yval(line, c), y1 = yval(line, c + 1);
-    const double h = __dsub_rn(x[c + 1], x[c]);
-    double* seg = line < nc1 ? sg1 + line * 4 * (nc0 + 1) + 4 * c : sg2 + (line - nc1) * 4 * (nc1 + 1) + 4 * c;
-    seg[0] = y0;
-    seg[1] = __dsub_rn(__dmul_rn(__dsub_rn(y1, y0), rr[3 * kStepMaxNc + c]),
-                       __dmul_rn(__dmul_rn(h, __dadd_rn(__dmul_rn(2.0, mm[c]), mm[c + 1])), 1.0 / 6.0));
-    seg[2] = __dmul_rn(mm[c], 0.5);
-    seg[3] = __dmul_rn(__dsub_rn(mm[c + 1], mm[c]), rr[4 * kStepMaxNc + c]);
-  }
-  __syncthreads();
+  STEP_STAMP(8);
   STEP_STAMP(6);
-  // P7: skeleton write (skel2d_write_fast_kernel's arithmetic)
+  // P7: skeleton write on this x-range: slab value / norm + the spline of the corrections,
+  // which is linear in them (B = spline_basis_table): sum_I B[x][I] E[I].  At the knots B is
+  // the identity, so the cross-point rounding of the reference's merge, (av + bv) - bv, keeps
+  // bv = P(u_cf) / ncf + E2 exactly.
   const i64 Nx = m.nf[0];
-  const double* tab0 = stab;
-  const double* tab1 = stab + kSkelTabMax;
-  const float invn0 = 1.0f / static_cast<float>(m.n[0]), invn1 = 1.0f / static_cast<float>(m.n[1]);
-  if (a == 1) {  // lines along x at the y-stations: u_fc / nfc + spline, cross points (av + bv) - bv
-    for (int J = 0; J < nc1; ++J) {
-      const int j = (J + 1) * m.n[1] - 1;
-      const int cj = seg_of(j + 1, m.n[1], invn1, nc1);
-      const double xj = static_cast<double>(j + 1) * m.h[1];
-      const double* s1 = sg1 + J * 4 * (nc0 + 1);
-      const double* srow = st + J * nf;
-      double* orow = A.out + Nx * j;
-#pragma unroll 4
-      for (int i = tid; i < m.nf[0]; i += kStepThreads) {
-        const int fi = i + 1;
-        const int c = seg_of(fi, m.n[0], invn0, nc0);
-        const double ufc = srow[i] * ifc;
-        const double av = __dadd_rn(ufc, seg_eval(tab0, s1, c, static_cast<double>(fi) * m.h[0]));
-        double val = av;
-        if (c * m.n[0] == fi && c >= 1) {  // an x-station: cross point
-          const int I = c - 1;
-          const double ucf = cr2[I + nc0 * J] * icf;
-          const double bv = __dadd_rn(ucf, seg_eval(tab1, sg2 + I * 4 * (nc1 + 1), cj, xj));
-          val = __dadd_rn(__dadd_rn(av, bv), -bv);
+  if (a == 1) {  // lines along x at the y-stations: one fine x per thread, every line J
+    for (int xl = tid; xl < nx; xl += kStepThreads) {
+      const int i = x0 + xl;
+      double br[kStepMaxNc];
+#pragma unroll
+      for (int I = 0; I < kStepMaxNc; ++I) br[I] = I < nc0 ? bas[xl * nc0 + I] : 0.0;
+      const bool cross = (i + 1) % m.n[0] == 0;
+      const int Ic = (i + 1) / m.n[0] - 1;
+      for (int J = 0; J < nc1; ++J) {
+        const double* e1 = ce1 + nc0 * J;
+        double sp = 0.0;
+#pragma unroll
+        for (int I = 0; I < kStepMaxNc; ++I)
+          if (I < nc0) sp = fma(br[I], e1[I], sp);
+        double val = __dadd_rn(st[J * XR + xl] * ifc, sp);
+        if (cross) {
+          const double bv = __dadd_rn(cr2[Ic + nc0 * J] * icf, ce2[Ic + nc0 * J]);
+          val = __dadd_rn(__dadd_rn(val, bv), -bv);
         }
-        orow[i] = val;
+        A.out[i + Nx * ((J + 1) * m.n[1] - 1)] = val;
       }
     }
-  } else {  // lines along y at the x-stations (cross points are written by CTA 1)
-    for (int I = 0; I < nc0; ++I) {
-      const int i = (I + 1) * m.n[0] - 1;
-      const double* s2 = sg2 + I * 4 * (nc1 + 1);
-      const double* scol = st + I * nf;
-#pragma unroll 4
-      for (int j = tid; j < m.nf[1]; j += kStepThreads) {
-        const int fj = j + 1;
-        const int c = seg_of(fj, m.n[1], invn1, nc1);
-        if (c * m.n[1] == fj && c >= 1 && c <= nc1) continue;  // a y-station: cross point
-        const double ucf = scol[j] * icf;
-        A.out[i + Nx * j] = __dadd_rn(ucf, seg_eval(tab1, s2, c, static_cast<double>(fj) * m.h[1]));
+  } else {  // lines along y at the x-stations (cross points are written by the slab-1 CTAs)
+    for (int jl = tid; jl < nx; jl += kStepThreads) {
+      const int j = x0 + jl;
+      if ((j + 1) % m.n[1] == 0) continue;  // a y-station: cross point
+      double br[kStepMaxNc];
+#pragma unroll
+      for (int J = 0; J < kStepMaxNc; ++J) br[J] = J < nc1 ? bas[jl * nc1 + J] : 0.0;
+      for (int I = 0; I < nc0; ++I) {
+        double sp = 0.0;
+#pragma unroll
+        for (int J = 0; J < kStepMaxNc; ++J)
+          if (J < nc1) sp = fma(br[J], ce2[I + nc0 * J], sp);
+        A.out[(I + 1) * m.n[0] - 1 + Nx * j] = __dadd_rn(st[I * XR + jl] * icf, sp);
       }
     }
   }
 #ifdef ASDSM_STEP_TRACE
   __syncthreads();
   STEP_STAMP(7);
-  if (tid == 0)
-    printf("STEPDBG cta %d load %lld tf %lld solve %lld back %lld xchg %lld ccspline %lld write %lld\n", a,
-           T_[1] - T_[0], T_[2] - T_[1], T_[3] - T_[2], T_[4] - T_[3], T_[5] - T_[4], T_[6] - T_[5], T_[7] - T_[6]);
+  if (tid == 0 && (rank == 0 || rank == kSlabCtas))
+    printf("STEPDBG cta %d load %lld tf+scatter %lld solve %lld (own %lld) back %lld xchg %lld norm %lld corr %lld write %lld\n",
+           rank, T_[1] - T_[0], T_[2] - T_[1], T_[3] - T_[2], T_[10] - T_[2], T_[4] - T_[3], T_[5] - T_[4], T_[9] - T_[5],
+           T_[8] - T_[9], T_[7] - T_[6]);
 #endif
 #undef STEP_STAMP
 }
@@ -463,6 +393,7 @@ bool slabstep2d_supported(const MeshDev& m, const SepSolver* slab) {
   if (m.dim != 2 || m.nc[0] > kStepMaxNc - 2 || m.nc[1] > kStepMaxNc - 2) return false;
   for (int a = 0; a < 2; ++a)
     if (slab[a].part == nullptr || slab[a].complex_modes) return false;
+  if (slab[0].part_seg != slab[1].part_seg) return false;
   const int ps = std::max(slab[0].part_stride, slab[1].part_stride);
   return sizeof(double) * static_cast<size_t>(step_layout(m, ps).total) <= 220 * 1024;
 }
@@ -471,12 +402,31 @@ size_t slabstep2d_smem_bytes(const SlabStep2DArgs& A) {
   return sizeof(double) * static_cast<size_t>(step_layout(A.m, std::max(A.pstride[0], A.pstride[1])).total);
 }
 
+// one kernel per segment length: a single solve body per kernel keeps the code small enough
+// to stay resident (measured: with every length behind one switch the line solve ran 5x slower)
+#define ASDSM_FOR_SEGS(X) X(2) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+
 void slabstep2d_prepare() {
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(slabstep2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+#define ASDSM_SEG_ATTR(S_)                                                                                 \
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(slabstep2d_kernel<S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        220 * 1024));
+  ASDSM_FOR_SEGS(ASDSM_SEG_ATTR)
+#undef ASDSM_SEG_ATTR
 }
 
 void launch_slabstep2d(const SlabStep2DArgs& A, DevState* st, cudaStream_t s) {
-  slabstep2d_kernel<<<2, kStepThreads, slabstep2d_smem_bytes(A), s>>>(A, st);
+  if (A.pseg[0] != A.pseg[1]) throw AsdsmError(kUnsupported, "slab step: slabs with different segment lengths");
+  const size_t smem = slabstep2d_smem_bytes(A);
+  switch (A.pseg[0]) {
+#define ASDSM_SEG_LAUNCH(S_) \
+  case S_:                   \
+    slabstep2d_kernel<S_><<<kClusterCtas, kStepThreads, smem, s>>>(A, st); \
+    break;
+    ASDSM_FOR_SEGS(ASDSM_SEG_LAUNCH)
+#undef ASDSM_SEG_LAUNCH
+    default:
+      throw AsdsmError(kUnsupported, "slab step: unsupported segment length");
+  }
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

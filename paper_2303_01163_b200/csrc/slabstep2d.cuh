@@ -17,7 +17,7 @@ struct SlabStep2DArgs {
   double line_l[2], line_r[2];  // line-axis stencil coefficients of slab a
   const double* sta0;     // station copies of the residual buffers (MarchArgs::sta0/sta1)
   const double* sta1;
-  const double* sp_tab[2];
+  const double* basis[2];  // spline_basis_table of axis 0 / 1: [fine index][station]
   const int* coin;        // coin[0] == 0 -> take P(u_cf) at cross points, else P(u_fc)
   double* out;            // fine array: skeleton points written
 };

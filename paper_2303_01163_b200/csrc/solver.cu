@@ -199,6 +199,9 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
         const std::vector<double> tab = spline_axis_table(m.nc[a], m.n[a], m.h[a]);
         sp_tab_[a] = dev_.alloc<double>(tab.size());
         ASDSM_CUDA_CHECK(cudaMemcpy(sp_tab_[a], tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+        const std::vector<double> bas = spline_basis_table(m.nc[a], m.n[a], m.h[a], m.nf[a]);
+        sp_basis_[a] = dev_.alloc<double>(bas.size());
+        ASDSM_CUDA_CHECK(cudaMemcpy(sp_basis_[a], bas.data(), bas.size() * sizeof(double), cudaMemcpyHostToDevice));
       }
       for (int b = 0; b < 2; ++b)  // residual on the slab stations, one copy per residual buffer
         stations_[b] = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * m.nf[1] + static_cast<size_t>(m.nc[1]) * m.nf[0]);
@@ -295,7 +298,7 @@ SlabStep2DArgs Solver::slabstep2d_args(const int* coin, double* out) const {
     A.pstride[a] = S.part_stride;
     A.line_l[a] = S.line_left;
     A.line_r[a] = S.line_right;
-    A.sp_tab[a] = sp_tab_[a];
+    A.basis[a] = sp_basis_[a];
   }
   A.sta0 = stations_[0];
   A.sta1 = stations_[1];

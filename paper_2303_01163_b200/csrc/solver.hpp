@@ -125,6 +125,7 @@ class Solver {
   bool fast2d_ = false;          // fused 2D slab/skeleton/hole path
   double* slab_modes_[2] = {nullptr, nullptr};
   double* stations_[2] = {nullptr, nullptr};  // residual on the slab stations (per residual buffer)
+  double* sp_basis_[2] = {nullptr, nullptr};    // skeleton-correction basis per axis (nf x nc)
   bool step2d_ = false;                          // one-launch slab step (slabstep2d.cu) eligible
   double* sp_tab_[2] = {nullptr, nullptr};
   double* seg1_ = nullptr;
