@@ -76,12 +76,38 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+// Programmatic dependent launch: a kernel lets the next one in the stream start as soon as all of
+// its CTAs are resident (launch_dependents), and the next one runs its data-independent prologue
+// (table staging) before waiting for this grid's completion and memory (wait).  Both are no-ops
+// for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 #endif
 
 constexpr int kMaxDim = 3;
+
+#ifdef __CUDACC__
+// Launch with the programmatic-stream-serialization attribute (PDL; captured into the graph as a
+// programmatic dependency) when ASDSM_PDL=1, plainly otherwise.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  ASDSM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+#endif
 
 // Host-side count of kernels this library launched (reported as gpu_launches by bench.py).
 extern long long g_kernel_launches;

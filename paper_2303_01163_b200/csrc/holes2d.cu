@@ -438,7 +438,7 @@ __device__ __forceinline__ void fused_forward_eo(double* sY, const double* sH, i
 template <bool SMOOTH>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     hole2d_fused_kernel(double* __restrict__ e, Hole2DArgs A, const double* __restrict__ bvec, const DevState* state) {
-  if (!state->active || !state->have_e) return;
+  pdl_launch_dependents();
 #ifdef ASDSM_FUSED_TRACE  // per-phase clock64 stamps of CTAs 0 and 55, printed at the end
   long long T[8] = {clock64(), 0, 0, 0, 0, 0, 0, 0};
 #define FUSED_STAMP(i) T[i] = clock64()
@@ -470,10 +470,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int hole = blockIdx.x;
   const int hx = hole % A.nbox0, hy = hole / A.nbox0;
   const int ox = hx * A.n0, oy = hy * A.n1;
-  // P0
+  // P0 (the tables are constant: staged while the previous kernel drains)
   stage_table(sP, A.ipiv, NP, m0, m0, S, tid);
   stage_table(sH, SH, hr, 2 * kh, 2 * kh, S, tid);
   asm volatile("cp.async.commit_group;\n" ::: "memory");
+  pdl_wait();
+  if (!state->active || !state->have_e) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    return;
+  }
   auto zero_kpad = [&]() {  // zero the k padding of the mode tile (even / odd mode counts me / mo)
     const int me = (m0 + 1) >> 1, mo = m0 >> 1;
     const int pe = kh - me, po = kh - mo;
@@ -806,8 +811,9 @@ bool hole2d_fused_fits(int m0, int m1) {
 void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevState* state, cudaStream_t s) {
   const size_t smem = hole2d_fused_smem_bytes(A.m0, A.m1);
   const unsigned grid = static_cast<unsigned>(A.nbox0 * A.nbox1);
-  if (b) hole2d_fused_kernel<true><<<grid, kFusedThreads, smem, s>>>(e, A, b, state);
-  else hole2d_fused_kernel<false><<<grid, kFusedThreads, smem, s>>>(e, A, nullptr, state);
+  if (b) launch_pdl(hole2d_fused_kernel<true>, grid, kFusedThreads, smem, s, e, A, b, static_cast<const DevState*>(state));
+  else launch_pdl(hole2d_fused_kernel<false>, grid, kFusedThreads, smem, s, e, A, static_cast<const double*>(nullptr),
+                  static_cast<const DevState*>(state));
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
 // loads -- the right shape when the arrays sit in L2 (config 1) and at HBM scale alike.
 template <int MODE, bool VAR, int YC>
 __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
+  pdl_launch_dependents();
+  pdl_wait();
   DevState* S = A.state;
   if (!S->active) return;
   const int cur = S->cur;
@@ -381,13 +383,13 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
 #define ASDSM_YC_DISPATCH(YCV)                                                                              \
   do {                                                                                                      \
     if (var) {                                                                                              \
-      if (mode == kMarchResidual) stencil2d_yc_kernel<kMarchResidual, true, YCV><<<nb2, 256, 0, s>>>(A);    \
-      else if (mode == kMarchUpdate) stencil2d_yc_kernel<kMarchUpdate, true, YCV><<<nb2, 256, 0, s>>>(A);   \
-      else stencil2d_yc_kernel<kMarchDots, true, YCV><<<nb2, 256, 0, s>>>(A);                              \
+      if (mode == kMarchResidual) launch_pdl(stencil2d_yc_kernel<kMarchResidual, true, YCV>, nb2, 256, 0, s, A); \
+      else if (mode == kMarchUpdate) launch_pdl(stencil2d_yc_kernel<kMarchUpdate, true, YCV>, nb2, 256, 0, s, A); \
+      else launch_pdl(stencil2d_yc_kernel<kMarchDots, true, YCV>, nb2, 256, 0, s, A);                      \
     } else {                                                                                                \
-      if (mode == kMarchResidual) stencil2d_yc_kernel<kMarchResidual, false, YCV><<<nb2, 256, 0, s>>>(A);   \
-      else if (mode == kMarchUpdate) stencil2d_yc_kernel<kMarchUpdate, false, YCV><<<nb2, 256, 0, s>>>(A);  \
-      else stencil2d_yc_kernel<kMarchDots, false, YCV><<<nb2, 256, 0, s>>>(A);                             \
+      if (mode == kMarchResidual) launch_pdl(stencil2d_yc_kernel<kMarchResidual, false, YCV>, nb2, 256, 0, s, A); \
+      else if (mode == kMarchUpdate) launch_pdl(stencil2d_yc_kernel<kMarchUpdate, false, YCV>, nb2, 256, 0, s, A); \
+      else launch_pdl(stencil2d_yc_kernel<kMarchDots, false, YCV>, nb2, 256, 0, s, A);                     \
     }                                                                                                       \
   } while (0)
     ASDSM_YC_DISPATCH(kYc);

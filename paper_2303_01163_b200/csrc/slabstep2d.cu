@@ -207,7 +207,7 @@ __device__ __forceinline__ void part_solve_line(double* line, const double* T, i
 template <int SEG>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThreads, 1)
     slabstep2d_kernel(SlabStep2DArgs A, DevState* S) {
-  if (!S->active) return;  // same decision in every CTA of the cluster
+  pdl_launch_dependents();
 #ifdef ASDSM_STEP_TRACE
   long long T_[12] = {clock64(), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #define STEP_STAMP(i) T_[i] = clock64()
@@ -232,12 +232,8 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThre
   double* sW = sm + Lo.wv;
   double* sV = sW + nc * nc;
   double* pt = sm + Lo.pt;
-  // P1: this x-range of the stations, the eigenvector blocks, the owned modes' line tables
-  const double* rs = (S->cur ? A.sta1 : A.sta0) + (a == 0 ? 0 : static_cast<i64>(nc0) * m.nf[1]);
-  for (int i = tid; i < nc * nx; i += kStepThreads) {
-    const int j = i / nx, x = i - j * nx;
-    cp_async8(st + j * XR + x, rs + static_cast<i64>(j) * nf + x0 + x);
-  }
+  // P1: the eigenvector blocks, the owned modes' line tables and the spline basis (constant:
+  // staged while the previous kernel drains), then this x-range of the stations
   for (int i = tid; i < nc * nc; i += kStepThreads) {
     cp_async8(sW + i, A.W[a] + i);
     cp_async8(sV + i, A.V[a] + i);
@@ -250,6 +246,16 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThre
   const int ncb = m.nc[1 - a];
   double* bas = sm + Lo.bas;
   for (int i = tid; i < nx * ncb; i += kStepThreads) cp_async8(bas + i, A.basis[1 - a] + static_cast<i64>(x0) * ncb + i);
+  pdl_wait();
+  if (!S->active) {  // same decision in every CTA of the cluster
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    return;
+  }
+  const double* rs = (S->cur ? A.sta1 : A.sta0) + (a == 0 ? 0 : static_cast<i64>(nc0) * m.nf[1]);
+  for (int i = tid; i < nc * nx; i += kStepThreads) {
+    const int j = i / nx, x = i - j * nx;
+    cp_async8(st + j * XR + x, rs + static_cast<i64>(j) * nf + x0 + x);
+  }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
@@ -420,7 +426,7 @@ void launch_slabstep2d(const SlabStep2DArgs& A, DevState* st, cudaStream_t s) {
   switch (A.pseg[0]) {
 #define ASDSM_SEG_LAUNCH(S_) \
   case S_:                   \
-    slabstep2d_kernel<S_><<<kClusterCtas, kStepThreads, smem, s>>>(A, st); \
+    launch_pdl(slabstep2d_kernel<S_>, kClusterCtas, kStepThreads, smem, s, A, st); \
     break;
     ASDSM_FOR_SEGS(ASDSM_SEG_LAUNCH)
 #undef ASDSM_SEG_LAUNCH
