@@ -247,6 +247,51 @@ __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+// DOTS restricted to the skeleton rows of a 2D mesh (rows at the y-stations, columns at the
+// x-stations, each point once): same per-point arithmetic as the full pass.
+template <bool VAR>
+__global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const bool work = S->have_e != 0;
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1];
+  const i64 sy = A.g.stride[1];
+  const Stencil& st = A.st;
+  const double* __restrict__ ee = A.e;
+  const double* __restrict__ rcur = S->cur ? A.r1 : A.r0;
+  const int nc0 = A.nc[0], nc1 = A.nc[1], n0 = A.n[0], n1 = A.n[1];
+  const i64 nrow = static_cast<i64>(nc1) * Nx, ncol = static_cast<i64>(nc0) * Ny;
+  double a0 = 0.0, a2 = 0.0;
+  for (i64 t = work ? static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x : nrow + ncol; t < nrow + ncol;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    int x, y;
+    if (t < nrow) {
+      const int J = static_cast<int>(t / Nx);
+      x = static_cast<int>(t - static_cast<i64>(J) * Nx);
+      y = (J + 1) * n1 - 1;
+    } else {
+      const i64 tc = t - nrow;
+      const int I = static_cast<int>(tc / Ny);
+      y = static_cast<int>(tc - static_cast<i64>(I) * Ny);
+      if ((y + 1) % n1 == 0) continue;  // cross point: counted with the rows
+      x = (I + 1) * n0 - 1;
+    }
+    const i64 p = x + y * sy;
+    const i64 N = A.g.size;
+    auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
+    double acc = 0.0;
+    if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[1]), __ldg(ee + p - sy)));
+    if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[0]), __ldg(ee + p - 1)));
+    acc = __dadd_rn(acc, __dmul_rn(C(2, st.diag), __ldg(ee + p)));
+    if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(3, st.right[0]), __ldg(ee + p + 1)));
+    if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[1]), __ldg(ee + p + sy)));
+    a0 += __ldg(rcur + p) * acc;
+    a2 += acc * acc;
+  }
+  block_reduce4_march(a0, 0.0, a2, 0.0, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
 // Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
@@ -374,7 +419,10 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
     }                                                                                   \
   } while (0)
-  if (A.g.dim == 2) {
+  if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {
+    if (var) skel2d_dots_kernel<true><<<kNumSms, 128, 0, s>>>(A);
+    else skel2d_dots_kernel<false><<<kNumSms, 128, 0, s>>>(A);
+  } else if (A.g.dim == 2) {
     // measured (configs 1-2): 8-row segments, a persistent grid of 4 CTAs per SM (more CTAs
     // pay in the completion count and block scheduling, fewer leave HBM latency exposed)
     constexpr int kYc = 8;

@@ -338,6 +338,12 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
 
 void Solver::march_launch(int mode, MarchArgs A, cudaStream_t s) {
   A.coef = coef_fine_;
+  if (A.skel_only) {
+    for (int a = 0; a < 2; ++a) {
+      A.nc[a] = mesh_.nc[a];
+      A.n[a] = mesh_.n[a];
+    }
+  }
   A.sta0 = A.sta1 = nullptr;
   if (fast2d_ && mode != kMarchDots && A.ro0 == r_[0] && A.ro1 == r_[1]) {
     A.sta0 = stations_[0];
@@ -746,8 +752,10 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
                             st_fine_, partials_, state_, history_, s, coef_fine_);
     c.op = kCtrlStep;
     c.k = k;
-    march_launch(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
-                                        st_fine_, partials_, state_, c, history_), s);
+    MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
+                                partials_, state_, c, history_);
+    dots.skel_only = (mesh_.dim == 2 && skel_dots_) ? 1 : 0;
+    march_launch(kMarchDots, dots, s);
     c.op = kCtrlAccept;
     MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_, partials_, state_,
                               c, history_);
@@ -886,8 +894,10 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   auto set_step = [&]() {
     CtrlArgs c{};
     c.op = kCtrlStep;
-    march_launch(kMarchDots, march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
-                                        st_fine_, partials_, state_, c, history_), s);
+    MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
+                                partials_, state_, c, history_);
+    dots.skel_only = (mesh_.dim == 2 && skel_dots_) ? 1 : 0;
+    march_launch(kMarchDots, dots, s);
   };
   const double ex = has_exact_ ? 1.0 : 0.0;
   timed("update_residual", 8.0 * N * (5.0 + ex), 0.0, iters, [&] {
@@ -911,7 +921,14 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   });
   out[0].ms -= out[1].ms;
   out.pop_back();
-  timed("step_dots", 8.0 * N * 2.0, 0.0, iters, [&] { set_step(); });
+  {
+    // skeleton-row dots move 2 doubles per skeleton point (+ the stencil's e neighbours, cached)
+    i64 nskel_pts = N;
+    if (mesh_.dim == 2 && skel_dots_)
+      nskel_pts = static_cast<i64>(mesh_.nc[1]) * mesh_.nf[0] + static_cast<i64>(mesh_.nc[0]) * mesh_.nf[1];
+    timed(mesh_.dim == 2 && skel_dots_ ? "step_dots_skeleton" : "step_dots", 8.0 * nskel_pts * 2.0, 0.0, iters,
+          [&] { set_step(); });
+  }
   const SepSolver& H = sep_hole_;
   i64 slab_pts = 0;
   for (int a = 0; a < mesh_.dim; ++a) slab_pts += g_slab_[a].size;

@@ -2,6 +2,7 @@
 // SolverContext + asdsm_iterate (proj/include/asdsm/solver.hpp:114-163).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -126,7 +127,9 @@ class Solver {
   double* slab_modes_[2] = {nullptr, nullptr};
   double* stations_[2] = {nullptr, nullptr};  // residual on the slab stations (per residual buffer)
   double* sp_basis_[2] = {nullptr, nullptr};    // skeleton-correction basis per axis (nf x nc)
-  bool step2d_ = false;                          // one-launch slab step (slabstep2d.cu) eligible
+  bool step2d_ = false;
+  // optimal-step dot products over the skeleton rows only (2D; ASDSM_FULL_DOTS=1: every row)
+  bool skel_dots_ = std::getenv("ASDSM_FULL_DOTS") == nullptr;                          // one-launch slab step (slabstep2d.cu) eligible
   double* sp_tab_[2] = {nullptr, nullptr};
   double* seg1_ = nullptr;
   double* seg2_ = nullptr;
