@@ -292,6 +292,65 @@ __global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+// 3D counterpart: the union of the station planes (x-planes, then y-planes off the x-stations,
+// then z-planes off both), each point once, same per-point arithmetic as march3d's DOTS.
+template <bool VAR>
+__global__ void __launch_bounds__(256) skel3d_dots_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const bool work = S->have_e != 0;
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
+  const i64 sy = A.g.stride[1], sz = A.g.stride[2];
+  const Stencil& st = A.st;
+  const double* __restrict__ ee = A.e;
+  const double* __restrict__ rcur = S->cur ? A.r1 : A.r0;
+  const int n0 = A.n[0], n1 = A.n[1], n2 = A.n[2];
+  const i64 px = static_cast<i64>(A.nc[0]) * Ny * Nz;  // x-planes: (I, y, z), y fastest
+  const i64 py = static_cast<i64>(A.nc[1]) * Nx * Nz;  // y-planes: (J, x, z), x fastest
+  const i64 pz = static_cast<i64>(A.nc[2]) * Nx * Ny;  // z-planes: (K, x, y), x fastest
+  double a0 = 0.0, a2 = 0.0;
+  for (i64 t = work ? static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x : px + py + pz; t < px + py + pz;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    int x, y, z;
+    if (t < px) {
+      const i64 q = t / Ny;
+      y = static_cast<int>(t - q * Ny);
+      const int I = static_cast<int>(q / Nz);
+      z = static_cast<int>(q - static_cast<i64>(I) * Nz);
+      x = (I + 1) * n0 - 1;
+    } else if (t < px + py) {
+      const i64 u = t - px, q = u / Nx;
+      x = static_cast<int>(u - q * Nx);
+      if ((x + 1) % n0 == 0) continue;
+      const int J = static_cast<int>(q / Nz);
+      z = static_cast<int>(q - static_cast<i64>(J) * Nz);
+      y = (J + 1) * n1 - 1;
+    } else {
+      const i64 u = t - px - py, q = u / Nx;
+      x = static_cast<int>(u - q * Nx);
+      const int K = static_cast<int>(q / Ny);
+      y = static_cast<int>(q - static_cast<i64>(K) * Ny);
+      if ((x + 1) % n0 == 0 || (y + 1) % n1 == 0) continue;
+      z = (K + 1) * n2 - 1;
+    }
+    const i64 p = x + y * sy + z * sz;
+    const i64 N = A.g.size;
+    auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
+    double acc = 0.0;
+    if (z > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[2]), __ldg(ee + p - sz)));
+    if (y > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[1]), __ldg(ee + p - sy)));
+    if (x > 0) acc = __dadd_rn(acc, __dmul_rn(C(2, st.left[0]), __ldg(ee + p - 1)));
+    acc = __dadd_rn(acc, __dmul_rn(C(3, st.diag), __ldg(ee + p)));
+    if (x < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[0]), __ldg(ee + p + 1)));
+    if (y < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(5, st.right[1]), __ldg(ee + p + sy)));
+    if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(C(6, st.right[2]), __ldg(ee + p + sz)));
+    a0 += __ldg(rcur + p) * acc;
+    a2 += acc * acc;
+  }
+  block_reduce4_march(a0, 0.0, a2, 0.0, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
 // Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
@@ -419,7 +478,10 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
     }                                                                                   \
   } while (0)
-  if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {
+  if (A.g.dim == 3 && mode == kMarchDots && A.skel_only) {
+    if (var) skel3d_dots_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
+    else skel3d_dots_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
+  } else if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {
     if (var) skel2d_dots_kernel<true><<<kNumSms, 128, 0, s>>>(A);
     else skel2d_dots_kernel<false><<<kNumSms, 128, 0, s>>>(A);
   } else if (A.g.dim == 2) {

@@ -33,8 +33,8 @@ struct MarchArgs {
   // (y = (j+1) n1 - 1) -- written by RESIDUAL / UPDATE so the slab gather reads them coalesced
   double* sta0;
   double* sta1;
-  int nc[2];
-  // DOTS on the skeleton rows only (2D): on hole rows A e is the hole fill's own residual
+  int nc[3];
+  // DOTS on the skeleton rows only: on hole rows A e is the hole fill's own residual
   // (rounding level) -- the reference's subsampled path samples skeleton rows for that reason
   // (solver.cpp:463-465); here the full sum drops those rounding-level terms as well
   int skel_only;

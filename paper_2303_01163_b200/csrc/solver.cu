@@ -339,7 +339,7 @@ void Solver::skeleton(const double* const* sol, const double* u_cc, const int* c
 void Solver::march_launch(int mode, MarchArgs A, cudaStream_t s) {
   A.coef = coef_fine_;
   if (A.skel_only) {
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < mesh_.dim; ++a) {
       A.nc[a] = mesh_.nc[a];
       A.n[a] = mesh_.n[a];
     }
@@ -754,7 +754,7 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
     c.k = k;
     MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
                                 partials_, state_, c, history_);
-    dots.skel_only = (mesh_.dim == 2 && skel_dots_) ? 1 : 0;
+    dots.skel_only = skel_dots_ ? 1 : 0;
     march_launch(kMarchDots, dots, s);
     c.op = kCtrlAccept;
     MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_, partials_, state_,
@@ -896,7 +896,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     c.op = kCtrlStep;
     MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
                                 partials_, state_, c, history_);
-    dots.skel_only = (mesh_.dim == 2 && skel_dots_) ? 1 : 0;
+    dots.skel_only = skel_dots_ ? 1 : 0;
     march_launch(kMarchDots, dots, s);
   };
   const double ex = has_exact_ ? 1.0 : 0.0;
@@ -924,10 +924,16 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   {
     // skeleton-row dots move 2 doubles per skeleton point (+ the stencil's e neighbours, cached)
     i64 nskel_pts = N;
-    if (mesh_.dim == 2 && skel_dots_)
-      nskel_pts = static_cast<i64>(mesh_.nc[1]) * mesh_.nf[0] + static_cast<i64>(mesh_.nc[0]) * mesh_.nf[1];
-    timed(mesh_.dim == 2 && skel_dots_ ? "step_dots_skeleton" : "step_dots", 8.0 * nskel_pts * 2.0, 0.0, iters,
-          [&] { set_step(); });
+    if (skel_dots_) {
+      nskel_pts = 0;
+      for (int a = 0; a < mesh_.dim; ++a) {
+        i64 plane = mesh_.nc[a];
+        for (int b = 0; b < mesh_.dim; ++b)
+          if (b != a) plane *= mesh_.nf[b];
+        nskel_pts += plane;  // (cross points counted per plane: an upper bound)
+      }
+    }
+    timed(skel_dots_ ? "step_dots_skeleton" : "step_dots", 8.0 * nskel_pts * 2.0, 0.0, iters, [&] { set_step(); });
   }
   const SepSolver& H = sep_hole_;
   i64 slab_pts = 0;
