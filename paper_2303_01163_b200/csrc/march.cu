@@ -356,13 +356,13 @@ __global__ void __launch_bounds__(256) skel3d_dots_kernel(MarchArgs A) {
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
 constexpr int ZC = 8;
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
+__global__ void __launch_bounds__(256, 4) stencil3d_zc_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
   const int cur = S->cur;
   double s = 0.0;
   bool work = true;
-  if (MODE == kMarchUpdate) {
+  if (MODE == kMarchUpdate || MODE == kMarchCand) {
     s = S->s;
     work = s != 0.0 && (!A.retry_pass || S->retry);
   }
@@ -370,11 +370,12 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
   const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
   const i64 sy = A.g.stride[1], sz = A.g.stride[2];
   const Stencil& st = A.st;
-  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  const double* __restrict__ uu = MODE == kMarchCand ? (cur ? A.uo0 : A.uo1) : (cur ? A.u1 : A.u0);
   Src<MODE> V{uu, A.e, s};
   const double* __restrict__ rcur = cur ? A.r1 : A.r0;
   double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
-  double* __restrict__ ro = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
+  double* __restrict__ ro =
+      (MODE == kMarchUpdate || MODE == kMarchCand) ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
   const int ntx = (Nx + 31) / 32, nty = (Ny + 7) / 8, ntz = (Nz + ZC - 1) / ZC;
   const long long ntiles = static_cast<long long>(ntx) * nty * ntz;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -414,8 +415,8 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
         a2 += acc * acc;
       } else {
         double r = __dsub_rn(__ldg(A.b + p), acc);
-        if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0 &&
-            (z + 1) % A.n[2] != 0)
+        if ((MODE == kMarchUpdate || MODE == kMarchCand) && A.sparse && (x + 1) % A.n[0] != 0 &&
+            (y + 1) % A.n[1] != 0 && (z + 1) % A.n[2] != 0)
           r = 0.0;
         ro[p] = r;
         if (MODE == kMarchUpdate) uo[p] = vc;
@@ -433,6 +434,28 @@ __global__ void __launch_bounds__(256) stencil3d_zc_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+
+// The 3D update's first pass: u' = u + s e into the non-current buffer (vectorized stream);
+// the residual of u' follows as kMarchCand (measured: two passes stream faster than the fused
+// 3D update, whose neighbour values each cost two loads).
+__global__ void __launch_bounds__(256) axpy_update_kernel(MarchArgs A) {
+  const DevState* S = A.state;
+  if (!S->active) return;
+  const double s = S->s;
+  if (!(s != 0.0 && (!A.retry_pass || S->retry))) return;
+  const int cur = S->cur;
+  const double* __restrict__ u = cur ? A.u1 : A.u0;
+  const double* __restrict__ e = A.e;
+  double* __restrict__ uo = cur ? A.uo0 : A.uo1;
+  const i64 n = A.g.size, n2 = n / 2;
+  const i64 stride = static_cast<i64>(gridDim.x) * blockDim.x;
+  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 uv = __ldg(reinterpret_cast<const double2*>(u) + i);
+    const double2 ev = __ldg(reinterpret_cast<const double2*>(e) + i);
+    reinterpret_cast<double2*>(uo)[i] = make_double2(__dadd_rn(uv.x, __dmul_rn(s, ev.x)), __dadd_rn(uv.y, __dmul_rn(s, ev.y)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) uo[n - 1] = __dadd_rn(u[n - 1], __dmul_rn(s, e[n - 1]));
+}
 }  // namespace
 
 int march_strip(const FineGeom& g) {
@@ -504,6 +527,14 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   } while (0)
     ASDSM_YC_DISPATCH(kYc);
 #undef ASDSM_YC_DISPATCH
+  } else if (mode == kMarchUpdate && std::getenv("ASDSM_MARCH3D") == nullptr) {
+    // measured (configs 3/4): axpy + candidate residual beats the fused 3D update
+    axpy_update_kernel<<<8 * kNumSms, 256, 0, s>>>(A);
+    ASDSM_CUDA_CHECK(cudaGetLastError());
+    ++g_kernel_launches;
+    const unsigned nbz = 8 * kNumSms;
+    if (var) stencil3d_zc_kernel<kMarchCand, true><<<nbz, 256, 0, s>>>(A);
+    else stencil3d_zc_kernel<kMarchCand, false><<<nbz, 256, 0, s>>>(A);
   } else if (std::getenv("ASDSM_MARCH3D") == nullptr && mode != kMarchUpdate) {
     // measured (config 3/4): the barrier-free z-coarsened pass streams the residual and the
     // dot-product passes faster; the smem-plane march is faster for the 5-array update pass

@@ -3,7 +3,9 @@
 
 namespace asdsm_b200 {
 
-enum { kMarchResidual = 0, kMarchUpdate = 1, kMarchDots = 2 };
+// kMarchCand: the residual of the update's candidate iterate (already written to the
+// non-current buffer by an axpy pass) -- the 3D update runs as axpy + kMarchCand
+enum { kMarchResidual = 0, kMarchUpdate = 1, kMarchDots = 2, kMarchCand = 3 };
 
 struct MarchArgs {
   const double* u0;  // current iterate buffers (state->cur selects); DOTS: unused
