@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   double* part = fT + m0;     // [4][2][128] partial sums of the full row transforms
   double* xch = part + 1024;  // [2 sides][2][128] values exchanged at the meeting rows
   double* scs = xch + 512;    // [m0] scale_i
-  double* hv = scs + 128;     // [4][64] ring-row pair sums h+ / h- of fB and fT
+  double* hv = scs + 128;     // [4][64] ring-row pair sums h+ / h- of fB and fT (P0: [4][128] ring sides)
   const int tid = threadIdx.x;
   const int hole = blockIdx.x;
   const int hx = hole % A.nbox0, hy = hole / A.nbox0;
@@ -498,6 +498,74 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       double f = __ldg(bvec + static_cast<i64>(oy + j) * Nxg + ox + i);
       if (i == 0 || i == m0 - 1 || j == 0 || j == m1 - 1) f = __dadd_rn(f, ring_rhs(e, A, ox, oy, i, j));
       sY[j * S + i] = f * __ldg(ci + i);
+    }
+  } else if (A.skel_line0 != nullptr) {
+    // the four skeleton sides of this hole: line value / norm + sum_k B[pos][k] E[k] (the same
+    // arithmetic the skeleton write used), into the ring arrays' spare room (hv: 4 x 128)
+    double* sB = hv;        // bottom row (y-station hy-1), x = ox + i
+    double* sT = hv + 128;  // top row (y-station hy)
+    double* sL = hv + 256;  // left column (x-station hx-1), y = oy + j
+    double* sR = hv + 384;  // right column (x-station hx)
+    const int nc0 = A.nc0, nc1 = A.nc1, ncc = nc0 * nc1;
+    const double* E1 = A.corr;
+    const double* E2 = A.corr + ncc;
+    for (int t = tid; t < 2 * m0 + 2 * m1; t += kFusedThreads) {
+      int side, q;
+      if (t < m0) { side = 0; q = t; }
+      else if (t < 2 * m0) { side = 1; q = t - m0; }
+      else if (t < 2 * m0 + m1) { side = 2; q = t - 2 * m0; }
+      else { side = 3; q = t - 2 * m0 - m1; }
+      double v = 0.0;
+      if (side < 2) {  // rows: J = hy - 1 / hy, x = ox + q
+        const int J = hy - 1 + side;
+        if (J >= 0 && J < nc1) {
+          const int x = ox + q;
+          const double* b0 = A.basis0 + static_cast<i64>(x) * nc0;
+          double sp = 0.0;
+          for (int I = 0; I < nc0; ++I) sp = fma(__ldg(b0 + I), __ldg(E1 + I + nc0 * J), sp);
+          v = __dadd_rn(__ldg(A.skel_line1 + static_cast<i64>(J) * A.nf0 + x), sp);
+          if (side == 0) e[static_cast<i64>(oy - 1) * Nxg + x] = v;  // owned: the bottom row
+        }
+        (side == 0 ? sB : sT)[q] = v;
+      } else {  // columns: I = hx - 1 / hx, y = oy + q
+        const int I = hx - 1 + (side - 2);
+        if (I >= 0 && I < nc0) {
+          const int y = oy + q;
+          const double* b1 = A.basis1 + static_cast<i64>(y) * nc1;
+          double sp = 0.0;
+          for (int J = 0; J < nc1; ++J) sp = fma(__ldg(b1 + J), __ldg(E2 + I + nc0 * J), sp);
+          v = __dadd_rn(__ldg(A.skel_line0 + static_cast<i64>(I) * A.nf1 + y), sp);
+          if (side == 2) e[static_cast<i64>(y) * Nxg + ox - 1] = v;  // owned: the left column
+        }
+        (side == 2 ? sL : sR)[q] = v;
+      }
+    }
+    __syncthreads();
+    const Stencil& st = A.st;
+    auto ring = [&](int i, int j) -> double {  // ring_rhs's terms and order on the computed sides
+      double acc = 0.0;
+      if (j == 0 && oy > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[1], sB[i]));
+      if (i == 0 && ox > 0) acc = __dadd_rn(acc, __dmul_rn(st.left[0], sL[j]));
+      if (i == m0 - 1 && ox + m0 < A.nf0 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(st.right[0], sR[j]));
+      if (j == m1 - 1 && oy + m1 < A.nf1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(st.right[1], sT[i]));
+      return __dsub_rn(0.0, acc);
+    };
+    double rl = 0.0, rr = 0.0, rb = 0.0, rt = 0.0;  // read before the arrays are overwritten
+    if (tid < m1) {
+      rl = ring(0, tid);
+      rr = ring(m0 - 1, tid);
+    } else if (tid >= 256 && tid - 256 < m0) {
+      rb = ring(tid - 256, 0);
+      rt = ring(tid - 256, m1 - 1);
+    }
+    __syncthreads();
+    if (tid < m1) {
+      fL[tid] = rl;
+      fR[tid] = rr;
+    } else if (tid >= 256 && tid - 256 < m0) {
+      const double c = __ldg(ci + tid - 256);
+      fB[tid - 256] = rb * c;
+      fT[tid - 256] = rt * c;
     }
   } else if (tid < m1) {
     fL[tid] = ring_rhs(e, A, ox, oy, 0, tid);
@@ -800,7 +868,7 @@ size_t hole2d_fused_smem_bytes(int m0, int m1) {
   const size_t S = kHole2DFusedStride;
   const size_t jp = (m1 + 7) & ~7;
   const size_t np = m1 - ((m1 - 1) >> 1);
-  return sizeof(double) * ((jp + half_sine_rows(m0) + np) * S + 2 * static_cast<size_t>(m0 + m1) + 15 * 128);
+  return sizeof(double) * ((jp + half_sine_rows(m0) + np) * S + 2 * static_cast<size_t>(m0 + m1) + 17 * 128);
 }
 
 bool hole2d_fused_fits(int m0, int m1) {

@@ -12,6 +12,15 @@ struct Hole2DArgs {
   Stencil st;        // fine stencil
   const double* Wt;  // forward eigenvectors along x, transposed: Wt[i*m0 + k] = W[k][i]
   const double* half;  // even/odd half sine table + row scalings along x (SepSolver::half)
+  // error mode after the one-launch slab step: the ring is evaluated here from the normalized
+  // station-line values + the spline of the cross-point corrections (else read from the fine
+  // array), and the hole writes the skeleton lines it owns (its left column and bottom row)
+  const double* skel_line0;  // [nc0][nf1]
+  const double* skel_line1;  // [nc1][nf0]
+  const double* corr;        // E1 then E2 (nc0*nc1 each)
+  const double* basis0;      // spline_basis_table of axis 0 [nf0][nc0]
+  const double* basis1;      // [nf1][nc1]
+  int nc0, nc1;
   const double* ipiv;  // Thomas pivots [j][k]
   const double* cp;    // Thomas upper factors [j][k]
   double line_left, line_right;

@@ -38,7 +38,7 @@ constexpr int kOwnMax = (kStepMaxNc + kSlabCtas - 1) / kSlabCtas;  // mode lines
 
 struct StepLayout {
   int NC, XR, NF, PS;
-  int st, md, ml, wv, pt, cr1, cr2, nrm, ce1, ce2, bas, red, total;
+  int st, md, ml, wv, pt, cr1, cr2, nrm, ce1, ce2, red, total;
 };
 
 // x-range of part c of a line of n points
@@ -67,7 +67,6 @@ __host__ __device__ inline StepLayout step_layout(const MeshDev& m, int pstride)
   L.nrm = take(kClusterCtas);
   L.ce1 = take(ncc);
   L.ce2 = take(ncc);
-  L.bas = take(L.XR * L.NC);        // this x-range's rows of the skeleton-correction basis
   L.red = take(32);
   L.total = o;
   return L;
@@ -242,10 +241,6 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThre
     const int u = i / A.pstride[a], o = i - u * A.pstride[a];
     cp_async8(pt + u * PS + o, A.part[a] + static_cast<i64>(c + u * kSlabCtas) * A.pstride[a] + o);
   }
-  // skeleton-correction basis of this slab's fine axis (1 - a), rows x0 .. x0 + nx
-  const int ncb = m.nc[1 - a];
-  double* bas = sm + Lo.bas;
-  for (int i = tid; i < nx * ncb; i += kStepThreads) cp_async8(bas + i, A.basis[1 - a] + static_cast<i64>(x0) * ncb + i);
   pdl_wait();
   if (!S->active) {  // same decision in every CTA of the cluster
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
@@ -339,46 +334,26 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kStepThre
   __syncthreads();
   STEP_STAMP(8);
   STEP_STAMP(6);
-  // P7: skeleton write on this x-range: slab value / norm + the spline of the corrections,
-  // which is linear in them (B = spline_basis_table): sum_I B[x][I] E[I].  At the knots B is
-  // the identity, so the cross-point rounding of the reference's merge, (av + bv) - bv, keeps
-  // bv = P(u_cf) / ncf + E2 exactly.
-  const i64 Nx = m.nf[0];
-  if (a == 1) {  // lines along x at the y-stations: one fine x per thread, every line J
-    for (int xl = tid; xl < nx; xl += kStepThreads) {
-      const int i = x0 + xl;
-      double br[kStepMaxNc];
-#pragma unroll
-      for (int I = 0; I < kStepMaxNc; ++I) br[I] = I < nc0 ? bas[xl * nc0 + I] : 0.0;
-      const bool cross = (i + 1) % m.n[0] == 0;
-      const int Ic = (i + 1) / m.n[0] - 1;
-      for (int J = 0; J < nc1; ++J) {
-        const double* e1 = ce1 + nc0 * J;
-        double sp = 0.0;
-#pragma unroll
-        for (int I = 0; I < kStepMaxNc; ++I)
-          if (I < nc0) sp = fma(br[I], e1[I], sp);
-        double val = __dadd_rn(st[J * XR + xl] * ifc, sp);
-        if (cross) {
-          const double bv = __dadd_rn(cr2[Ic + nc0 * J] * icf, ce2[Ic + nc0 * J]);
-          val = __dadd_rn(__dadd_rn(val, bv), -bv);
-        }
-        A.out[i + Nx * ((J + 1) * m.n[1] - 1)] = val;
-      }
-    }
-  } else {  // lines along y at the x-stations (cross points are written by the slab-1 CTAs)
-    for (int jl = tid; jl < nx; jl += kStepThreads) {
-      const int j = x0 + jl;
-      if ((j + 1) % m.n[1] == 0) continue;  // a y-station: cross point
-      double br[kStepMaxNc];
-#pragma unroll
-      for (int J = 0; J < kStepMaxNc; ++J) br[J] = J < nc1 ? bas[jl * nc1 + J] : 0.0;
-      for (int I = 0; I < nc0; ++I) {
-        double sp = 0.0;
-#pragma unroll
-        for (int J = 0; J < kStepMaxNc; ++J)
-          if (J < nc1) sp = fma(br[J], ce2[I + nc0 * J], sp);
-        A.out[(I + 1) * m.n[0] - 1 + Nx * j] = __dadd_rn(st[I * XR + jl] * icf, sp);
+  // P7: publish what the skeleton is made of -- the normalized slab values on this x-range of
+  // every station line, the cross-point corrections and the cross points themselves.  The hole
+  // kernel evaluates its ring from these (value / norm + spline of the corrections) and writes
+  // the skeleton lines it owns, so the line values are computed by 100 CTAs instead of 8.
+  {
+    const double inv = a == 1 ? ifc : icf;
+    double* dst = (a == 1 ? A.skel_line1 : A.skel_line0) + x0;
+    for (int j = 0; j < nc; ++j)
+      for (int x = tid; x < nx; x += kStepThreads) dst[static_cast<i64>(j) * nf + x] = st[j * XR + x] * inv;
+    if (rank == 0) {
+      const i64 Nx = m.nf[0];
+      for (int t = tid; t < ncc; t += kStepThreads) {
+        A.corr[t] = ce1[t];
+        A.corr[ncc + t] = ce2[t];
+        // cross point (reference merge order: lines along x, then the y-line value added and
+        // removed): av = P(u_fc)/nfc + E1 (B is the identity at knots), bv = P(u_cf)/ncf + E2
+        const int I = t % nc0, J = t / nc0;
+        const double av = __dadd_rn(cr1[t] * ifc, ce1[t]);
+        const double bv = __dadd_rn(cr2[t] * icf, ce2[t]);
+        A.out[(I + 1) * m.n[0] - 1 + Nx * ((J + 1) * m.n[1] - 1)] = __dadd_rn(__dadd_rn(av, bv), -bv);
       }
     }
   }

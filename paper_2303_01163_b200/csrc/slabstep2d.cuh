@@ -17,9 +17,11 @@ struct SlabStep2DArgs {
   double line_l[2], line_r[2];  // line-axis stencil coefficients of slab a
   const double* sta0;     // station copies of the residual buffers (MarchArgs::sta0/sta1)
   const double* sta1;
-  const double* basis[2];  // spline_basis_table of axis 0 / 1: [fine index][station]
+  double* skel_line0;     // out: u_cf / ||u_cf|| on the x-stations' lines [nc0][nf1]
+  double* skel_line1;     // out: u_fc / ||u_fc|| on the y-stations' lines [nc1][nf0]
+  double* corr;           // out: cross-point corrections E1 then E2 (nc0*nc1 each)
   const int* coin;        // coin[0] == 0 -> take P(u_cf) at cross points, else P(u_fc)
-  double* out;            // fine array: skeleton points written
+  double* out;            // fine array: the cross points (the rest of the skeleton: holes2d)
 };
 
 bool slabstep2d_supported(const MeshDev& m, const SepSolver* slab);

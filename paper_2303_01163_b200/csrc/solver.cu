@@ -206,7 +206,12 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
       for (int b = 0; b < 2; ++b)  // residual on the slab stations, one copy per residual buffer
         stations_[b] = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * m.nf[1] + static_cast<size_t>(m.nc[1]) * m.nf[0]);
       seg1_ = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * 4 * (m.nc[0] + 1));
-      step2d_ = std::getenv("ASDSM_NO_SLABSTEP") == nullptr && slabstep2d_supported(md_, sep_slab_);
+      step2d_ = std::getenv("ASDSM_NO_SLABSTEP") == nullptr && std::getenv("ASDSM_HOLE_UNFUSED") == nullptr &&
+                slabstep2d_supported(md_, sep_slab_) && !sep_hole_.complex_modes && sep_hole_.nd == 1 &&
+                sep_hole_.L == 1 && !sep_hole_.use_pcr && hole2d_fused_fits(sep_hole_.ext[0], sep_hole_.ext[1]);
+      skel_line_[0] = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * m.nf[1]);
+      skel_line_[1] = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * m.nf[0]);
+      skel_corr_ = dev_.alloc<double>(2 * static_cast<size_t>(m.nc[0]) * m.nc[1]);
       if (step2d_) slabstep2d_prepare();
       seg2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * 4 * (m.nc[1] + 1));
     }
@@ -298,12 +303,14 @@ SlabStep2DArgs Solver::slabstep2d_args(const int* coin, double* out) const {
     A.pstride[a] = S.part_stride;
     A.line_l[a] = S.line_left;
     A.line_r[a] = S.line_right;
-    A.basis[a] = sp_basis_[a];
   }
   A.sta0 = stations_[0];
   A.sta1 = stations_[1];
   A.coin = coin;
   A.out = out;
+  A.skel_line0 = skel_line_[0];
+  A.skel_line1 = skel_line_[1];
+  A.corr = skel_corr_;
   return A;
 }
 
@@ -405,10 +412,20 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.line_left = H.line_left;
     A.line_right = H.line_right;
     static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
+    if (ring_from_lines_) {  // the slab step left the skeleton to the holes (fused kernel only)
+      A.skel_line0 = skel_line_[0];
+      A.skel_line1 = skel_line_[1];
+      A.corr = skel_corr_;
+      A.basis0 = sp_basis_[0];
+      A.basis1 = sp_basis_[1];
+      A.nc0 = mesh_.nc[0];
+      A.nc1 = mesh_.nc[1];
+    }
     if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
       launch_hole2d_fused(e, A, b, state_, s);
       return;
     }
+    if (ring_from_lines_) throw AsdsmError(kUnsupported, "slab step without the fused hole kernel");
   }
   if (!generic && mesh_.dim == 2 && b == nullptr && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
     Hole2DArgs A{};
@@ -578,9 +595,11 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
     if (r0 == r_[0] && r1 == r_[1]) {  // the station copies the residual passes keep
       A.sta0 = stations_[0];
       A.sta1 = stations_[1];
-      if (step2d_) {  // slab solves + normalization + cc/spline + skeleton write, one launch
-        launch_slabstep2d(slabstep2d_args(coins_ + 4 * k, out), state_, s);
+      if (step2d_) {  // slab solves + normalization + cc/spline in one launch; the holes
+        launch_slabstep2d(slabstep2d_args(coins_ + 4 * k, out), state_, s);  // write the skeleton
+        ring_from_lines_ = true;
         fill(out, nullptr, s);
+        ring_from_lines_ = false;
         return;
       }
     }

@@ -128,6 +128,9 @@ class Solver {
   double* stations_[2] = {nullptr, nullptr};  // residual on the slab stations (per residual buffer)
   double* sp_basis_[2] = {nullptr, nullptr};    // skeleton-correction basis per axis (nf x nc)
   bool step2d_ = false;
+  double* skel_line_[2] = {nullptr, nullptr};   // slab step outputs: normalized station lines
+  double* skel_corr_ = nullptr;                 //   and the cross-point corrections
+  bool ring_from_lines_ = false;                // fill(): holes evaluate + write the skeleton
   // optimal-step dot products over the skeleton rows only (ASDSM_FULL_DOTS=1: every row)
   bool skel_dots_ = std::getenv("ASDSM_FULL_DOTS") == nullptr;                          // one-launch slab step (slabstep2d.cu) eligible
   double* sp_tab_[2] = {nullptr, nullptr};
