@@ -515,30 +515,35 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       else if (t < 2 * m0) { side = 1; q = t - m0; }
       else if (t < 2 * m0 + m1) { side = 2; q = t - 2 * m0; }
       else { side = 3; q = t - 2 * m0 - m1; }
+      // row sides: station J = hy - 1 / hy at x = ox + q, basis of axis 0, E1 row J;
+      // column sides: station I = hx - 1 / hx at y = oy + q, basis of axis 1, E2 column I
+      const bool row = side < 2;
+      const int stn = row ? hy - 1 + side : hx - 1 + (side - 2);
+      const int nk = row ? nc0 : nc1;
+      const int pos = row ? ox + q : oy + q;
       double v = 0.0;
-      if (side < 2) {  // rows: J = hy - 1 / hy, x = ox + q
-        const int J = hy - 1 + side;
-        if (J >= 0 && J < nc1) {
-          const int x = ox + q;
-          const double* b0 = A.basis0 + static_cast<i64>(x) * nc0;
-          double sp = 0.0;
-          for (int I = 0; I < nc0; ++I) sp = fma(__ldg(b0 + I), __ldg(E1 + I + nc0 * J), sp);
-          v = __dadd_rn(__ldg(A.skel_line1 + static_cast<i64>(J) * A.nf0 + x), sp);
-          if (side == 0) e[static_cast<i64>(oy - 1) * Nxg + x] = v;  // owned: the bottom row
+      if (stn >= 0 && stn < (row ? nc1 : nc0)) {
+        const double* bb = (row ? A.basis0 : A.basis1) + static_cast<i64>(pos) * nk;
+        const double* ee = row ? E1 + nc0 * stn : E2 + stn;
+        const int es = row ? 1 : nc0;
+        const double lv = __ldg((row ? A.skel_line1 + static_cast<i64>(stn) * A.nf0 : A.skel_line0 + static_cast<i64>(stn) * A.nf1) + pos);
+        constexpr int kU = 12;  // every load of the dot product in flight at once
+        double bq[kU], eq[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          bq[k] = k < nk ? __ldg(bb + k) : 0.0;
+          eq[k] = k < nk ? __ldg(ee + k * es) : 0.0;
         }
-        (side == 0 ? sB : sT)[q] = v;
-      } else {  // columns: I = hx - 1 / hx, y = oy + q
-        const int I = hx - 1 + (side - 2);
-        if (I >= 0 && I < nc0) {
-          const int y = oy + q;
-          const double* b1 = A.basis1 + static_cast<i64>(y) * nc1;
-          double sp = 0.0;
-          for (int J = 0; J < nc1; ++J) sp = fma(__ldg(b1 + J), __ldg(E2 + I + nc0 * J), sp);
-          v = __dadd_rn(__ldg(A.skel_line0 + static_cast<i64>(I) * A.nf1 + y), sp);
-          if (side == 2) e[static_cast<i64>(y) * Nxg + ox - 1] = v;  // owned: the left column
-        }
-        (side == 2 ? sL : sR)[q] = v;
+        double sp = 0.0;
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+          if (k < nk) sp = fma(bq[k], eq[k], sp);
+        for (int k = kU; k < nk; ++k) sp = fma(__ldg(bb + k), __ldg(ee + k * es), sp);
+        v = __dadd_rn(lv, sp);
+        if (side == 0) e[static_cast<i64>(oy - 1) * Nxg + pos] = v;  // owned: the bottom row
+        if (side == 2) e[static_cast<i64>(pos) * Nxg + ox - 1] = v;  // owned: the left column
       }
+      (side == 0 ? sB : side == 1 ? sT : side == 2 ? sL : sR)[q] = v;
     }
     __syncthreads();
     const Stencil& st = A.st;
