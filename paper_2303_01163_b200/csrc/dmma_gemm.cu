@@ -124,10 +124,238 @@ __global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __res
   }
 }
 
+
+// Even/odd-split transforms (plan.cpp half_sine_tables): V = D S and W = c S D^-1 with S the
+// DST-I matrix, whose row m-1-i is (-1)^k times row i.  Both directions need only the
+// ceil(m/2) x m half table SH (even columns first, then odd) and half the MMAs of the dense
+// GEMM:
+//   back:    E_q = sum_kappa x_{2 kappa} SH[q][kappa],  O_q = sum_kappa x_{2 kappa+1} SH[q][kh+kappa]
+//            out(q) = sc_q (E_q + O_q),  out(m-1-q) = sc_{m-1-q} (E_q - O_q)      (q < ceil(m/2))
+//   forward: g_j = ci_j in(j),  h+-_j = g_j +- g_{m-1-j}  (j < ceil(m/2); h = g_j at j = m-1-j)
+//            out(2 kappa) = sum_j h+_j SH[j][kappa],  out(2 kappa+1) = sum_j h-_j SH[j][kh+kappa]
+// Warp-specialized: warps 0-3 accumulate E, warps 4-7 O over the same 64 x 64 tile (each warp
+// 32 x 32, the dense kernel's register budget); the back transform combines them through shared
+// memory in the epilogue.
+constexpr int EP = 64, EQ = 64, EK = 16, ELD2 = EK + 4, ENT2 = 256;
+constexpr size_t kEo2Smem = sizeof(double) * 4 * EP * ELD2 + 2 * EP * sizeof(i64);
+
+template <bool kBack, bool kContigIn>
+__global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                           const double* __restrict__ SH, const double* __restrict__ sc,
+                                                           int m, int kh, i64 in_es, i64 out_es, GemmLines L) {
+  extern __shared__ __align__(16) double esm[];
+  double(*AE)[ELD2] = reinterpret_cast<double(*)[ELD2]>(esm);
+  double(*AO)[ELD2] = reinterpret_cast<double(*)[ELD2]>(esm + EP * ELD2);
+  double(*BE)[ELD2] = reinterpret_cast<double(*)[ELD2]>(esm + 2 * EP * ELD2);
+  double(*BO)[ELD2] = reinterpret_cast<double(*)[ELD2]>(esm + 3 * EP * ELD2);
+  i64* s_ib = reinterpret_cast<i64*>(esm + 4 * EP * ELD2);
+  i64* s_ob = s_ib + EP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp >> 2, wl = warp & 3;  // grp 0: E, 1: O
+  const int wp = (wl >> 1) * 32, wq = (wl & 1) * 32;
+  const int mh = (m + 1) >> 1;
+  const i64 p0 = static_cast<i64>(blockIdx.y) * EP;
+  const int q0 = blockIdx.x * EQ;
+  const double* __restrict__ ci = sc + m;
+  for (int t = tid; t < EP; t += ENT2) {
+    i64 ib = 0, ob = 0;
+    if (p0 + t < L.nlines) line_base(L, p0 + t, ib, ob);
+    s_ib[t] = ib;
+    s_ob[t] = ob;
+  }
+  __syncthreads();
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int K = kBack ? kh : mh;
+  constexpr int PA = (EP * 2 * EK) / ENT2;  // 8
+  constexpr int PB = (EQ * 2 * EK) / ENT2;  // 8
+  double ra[PA], rb[PB];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int e = tid + r * ENT2;
+      int pl, c;  // c in [0, 2 EK): back: mode 2 k0 + c; forward: (j = k0 + c/2, parity = mirror)
+      if (kContigIn) {
+        pl = e / (2 * EK);
+        c = e % (2 * EK);
+      } else {
+        pl = e % EP;
+        c = e / EP;
+      }
+      double v = 0.0;
+      if (p0 + pl < L.nlines) {
+        if (kBack) {
+          const int k = 2 * k0 + c;
+          if (k < m) v = __ldg(in + s_ib[pl] + static_cast<i64>(k) * in_es);
+        } else {
+          const int j = k0 + (c >> 1);
+          const int jj = (c & 1) ? m - 1 - j : j;
+          if (j < mh) v = __ldg(in + s_ib[pl] + static_cast<i64>(jj) * in_es) * __ldg(ci + jj);
+        }
+      }
+      ra[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < PB; ++r) {
+      const int e = tid + r * ENT2;
+      double v = 0.0;
+      if (kBack) {  // B(n = q, k = kappa): SH[q][half kh + kappa], kappa contiguous
+        const int ql = e / (2 * EK), c = e % (2 * EK), half = c / EK, kl = c % EK;
+        if (q0 + ql < mh && k0 + kl < kh) v = __ldg(SH + static_cast<i64>(q0 + ql) * 2 * kh + half * kh + k0 + kl);
+      } else {  // B(n = kappa, k = j): SH[j][half kh + kappa], kappa contiguous
+        const int nl = e % EQ, c = e / EQ, half = c / EK, jl = c % EK;
+        if (q0 + nl < kh && k0 + jl < mh) v = __ldg(SH + static_cast<i64>(k0 + jl) * 2 * kh + half * kh + q0 + nl);
+      }
+      rb[r] = v;
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int r = 0; r < PA; ++r) {
+      const int e = tid + r * ENT2;
+      int pl, c;
+      if (kContigIn) {
+        pl = e / (2 * EK);
+        c = e % (2 * EK);
+      } else {
+        pl = e % EP;
+        c = e / EP;
+      }
+      if (c & 1) AO[pl][c >> 1] = ra[r];
+      else AE[pl][c >> 1] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < PB; ++r) {
+      const int e = tid + r * ENT2;
+      if (kBack) {
+        const int ql = e / (2 * EK), c = e % (2 * EK);
+        if (c < EK) BE[ql][c] = rb[r];
+        else BO[ql][c - EK] = rb[r];
+      } else {
+        const int nl = e % EQ, c = e / EQ;
+        if (c < EK) BE[nl][c] = rb[r];
+        else BO[nl][c - EK] = rb[r];
+      }
+    }
+  };
+  const int r8 = lane >> 2, c4 = lane & 3;
+  double(*As)[ELD2] = grp ? AO : AE;
+  double(*Bs)[ELD2] = grp ? BO : BE;
+  load(0);
+  for (int k0 = 0; k0 < K; k0 += EK) {
+    store();
+    __syncthreads();
+    if (!kBack) {
+      // forward: AE/AO hold g_j / g_{m-1-j}; make them h+ / h- (g_j alone at the middle row)
+      for (int t = tid; t < EP * EK; t += ENT2) {
+        const int pl = t / EK, jl = t % EK, j = k0 + jl;
+        const double g = AE[pl][jl], gm = AO[pl][jl];
+        const bool mid = (m - 1 - j) == j;
+        AE[pl][jl] = mid ? g : g + gm;
+        AO[pl][jl] = mid ? g : g - gm;
+      }
+      __syncthreads();
+    }
+    if (k0 + EK < K) load(k0 + EK);
+#pragma unroll
+    for (int kk = 0; kk < EK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) fa[a] = As[wp + a * 8 + r8][kk + c4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = Bs[wq + b * 8 + r8][kk + c4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b], fa[a], fb[b]);
+    }
+    __syncthreads();
+  }
+  if (kBack) {
+    // E -> shared (over the A tiles), then the O warps combine: out(q), out(m-1-q)
+    double(*Ex)[EQ + 4] = reinterpret_cast<double(*)[EQ + 4]>(esm);
+    if (grp == 0) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          Ex[wp + a * 8 + r8][wq + b * 8 + 2 * c4] = acc[a][b][0];
+          Ex[wp + a * 8 + r8][wq + b * 8 + 2 * c4 + 1] = acc[a][b][1];
+        }
+    }
+    __syncthreads();
+    if (grp == 1) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int pl = wp + a * 8 + r8;
+        if (p0 + pl >= L.nlines) continue;
+        const i64 ob = s_ob[pl];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ql = wq + b * 8 + 2 * c4 + h, q = q0 + ql;
+            if (q >= mh) continue;
+            const double E = Ex[pl][ql], O = acc[a][b][h];
+            out[ob + static_cast<i64>(q) * out_es] = __ldg(sc + q) * (E + O);
+            const int qm = m - 1 - q;
+            if (qm != q) out[ob + static_cast<i64>(qm) * out_es] = __ldg(sc + qm) * (E - O);
+          }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int pl = wp + a * 8 + r8;
+      if (p0 + pl >= L.nlines) continue;
+      const i64 ob = s_ob[pl];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kap = q0 + wq + b * 8 + 2 * c4 + h;
+          const int k = 2 * kap + grp;  // E -> even modes, O -> odd
+          if (kap < kh && k < m) out[ob + static_cast<i64>(k) * out_es] = acc[a][b][h];
+        }
+    }
+  }
+}
+
 }  // namespace
 
-void dmma_prepare() {}  // the register-staged kernel needs no attributes (a 3-stage cp.async
-                        // variant measured slower on both m=102 and m=409 and was dropped)
+void dmma_prepare() {  // (a 3-stage cp.async variant of the dense kernel measured slower on both
+                       // m=102 and m=409 and was dropped)
+  static bool done = false;
+  if (done) return;
+  done = true;
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+}
+
+void launch_dmma_eo_transform(bool back, const double* in, double* out, const double* half, int m, i64 in_es,
+                              i64 out_es, const GemmLines& L, cudaStream_t s) {
+  const int kh = half_sine_kh(m), hr = half_sine_rows(m), mh = (m + 1) / 2;
+  const double* sc = half + static_cast<i64>(hr) * 2 * kh;
+  const i64 pb = (L.nlines + EP - 1) / EP;
+  if (pb > 65535) throw AsdsmError(kUnsupported, "transform batch too large for the grid");
+  const int nq = back ? mh : kh;
+  dim3 grid(static_cast<unsigned>((nq + EQ - 1) / EQ), static_cast<unsigned>(pb));
+  const bool ci = in_es == 1;
+  if (back) {
+    if (ci) dmma_eo2_kernel<true, true><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+    else dmma_eo2_kernel<true, false><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+  } else {
+    if (ci) dmma_eo2_kernel<false, true><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+    else dmma_eo2_kernel<false, false><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+  }
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
 
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s) {

@@ -6,6 +6,10 @@
 
 namespace asdsm_b200 {
 
+// the even/odd kernel is used for axes of at least this many modes (below, the dense kernel's
+// rounding is kept: the split's savings do not matter there)
+constexpr int kEoMinModes = 64;
+
 struct GemmLines {
   int o_ext[2];
   i64 o_in[2], o_out[2];
@@ -16,6 +20,10 @@ struct GemmLines {
 
 // in_es / out_es: element stride along the transform axis for input / output.
 void dmma_prepare();  // kernel attributes (call before any stream capture)
+// Even/odd-split transform with the half sine table of SepSolver::half (back: V, forward: W);
+// half the MMAs of launch_dmma_transform.
+void launch_dmma_eo_transform(bool back, const double* in, double* out, const double* half, int m, i64 in_es,
+                              i64 out_es, const GemmLines& L, cudaStream_t s);
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s);
 

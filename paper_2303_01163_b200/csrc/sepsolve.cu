@@ -255,9 +255,11 @@ BoxArray compact_layout(const SepSolver& S, const BoxArray& like, void* ptr) {
   return b;
 }
 
+// eo: 1 back transform (mat = V), 2 forward (mat = W): long axes with a half sine table run the
+// even/odd-split DMMA kernel (half the MMAs); 0 or short axes the dense one
 template <typename TIn, typename TMat, typename TOut>
 void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const BoxArray& out, const TMat* mat,
-                      cudaStream_t st) {
+                      cudaStream_t st, int eo = 0) {
   LineMap M{};
   int no = 0;
   for (int a = 0; a < 3; ++a) {
@@ -295,6 +297,11 @@ void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const Bo
         G.out_bs[a] = M.out_bs[a];
       }
       G.nlines = M.nlines;
+      static const bool dense = std::getenv("ASDSM_DENSE_GEMM") != nullptr;
+      if (eo != 0 && S.half[axis] != nullptr && m >= kEoMinModes && !dense) {
+        launch_dmma_eo_transform(eo == 1, ip, op, S.half[axis], m, in.stride[axis], out.stride[axis], G, st);
+        return;
+      }
       launch_dmma_transform(ip, op, mat, m, in.stride[axis], out.stride[axis], G, st);
       return;
     }
@@ -363,12 +370,12 @@ void sep_back_transform(const SepSolver& S, void* modes, const BoxArray& out, vo
   if (S.complex_modes) throw AsdsmError(kUnsupported, "sep_back_transform: complex modes");
   const BoxArray c0 = compact_layout(S, out, modes);
   if (S.nd == 1) {
-    launch_transform<double, double, double>(S, S.dax[0], c0, out, S.V[S.dax[0]], st);
+    launch_transform<double, double, double>(S, S.dax[0], c0, out, S.V[S.dax[0]], st, 1);
     return;
   }
   const BoxArray c1 = compact_layout(S, out, scratch);
-  launch_transform<double, double, double>(S, S.dax[1], c0, c1, S.V[S.dax[1]], st);
-  launch_transform<double, double, double>(S, S.dax[0], c1, out, S.V[S.dax[0]], st);
+  launch_transform<double, double, double>(S, S.dax[1], c0, c1, S.V[S.dax[1]], st, 1);
+  launch_transform<double, double, double>(S, S.dax[0], c1, out, S.V[S.dax[0]], st, 1);
 }
 
 void sep_prepare() {
@@ -397,17 +404,17 @@ void sep_solve(const SepSolver& S, const BoxArray& in, const BoxArray& out, void
   }
   if (S.nd == 1) {
     const int a = S.dax[0];
-    launch_transform<double, double, double>(S, a, in, c0, S.W[a], st);
+    launch_transform<double, double, double>(S, a, in, c0, S.W[a], st, 2);
     launch_line_solve<double>(S, c0, st);
-    launch_transform<double, double, double>(S, a, c0, out, S.V[a], st);
+    launch_transform<double, double, double>(S, a, c0, out, S.V[a], st, 1);
     return;
   }
   const int a0 = S.dax[0], a1 = S.dax[1];
-  launch_transform<double, double, double>(S, a0, in, c0, S.W[a0], st);
-  launch_transform<double, double, double>(S, a1, c0, c1, S.W[a1], st);
+  launch_transform<double, double, double>(S, a0, in, c0, S.W[a0], st, 2);
+  launch_transform<double, double, double>(S, a1, c0, c1, S.W[a1], st, 2);
   launch_line_solve<double>(S, c1, st);
-  launch_transform<double, double, double>(S, a1, c1, c0, S.V[a1], st);
-  launch_transform<double, double, double>(S, a0, c0, out, S.V[a0], st);
+  launch_transform<double, double, double>(S, a1, c1, c0, S.V[a1], st, 1);
+  launch_transform<double, double, double>(S, a0, c0, out, S.V[a0], st, 1);
 }
 
 }  // namespace asdsm_b200

@@ -470,7 +470,8 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     G.out_bs[0] = A.n0;
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
-    launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
+    if (A.m0 >= kEoMinModes) launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, 1, 1, G, s);
+    else launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
     return;
   }
   if (!generic && mesh_.dim == 3 && b == nullptr && !H.complex_modes && H.nd == 2 && H.L == 2 && H.dax[0] == 0 &&
@@ -1021,7 +1022,12 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     G.out_bs[1] = static_cast<i64>(mesh_.n[1]) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(H.ext[1]) * G.nbox[0] * G.nbox[1];
     timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
-          [&] { launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s); });
+          [&] {
+            if (H.ext[0] >= kEoMinModes)
+              launch_dmma_eo_transform(true, static_cast<const double*>(scratch0_), e_, H.half[0], H.ext[0], 1, 1, G, s);
+            else
+              launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s);
+          });
     }
   } else {
     double hflops = 0;
