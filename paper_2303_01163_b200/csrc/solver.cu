@@ -470,7 +470,8 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     G.out_bs[0] = A.n0;
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
-    if (A.m0 >= kEoMinModes) launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, 1, 1, G, s);
+    if (A.m0 >= kEoMinModes && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
+      launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, 1, 1, G, s);
     else launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
     return;
   }

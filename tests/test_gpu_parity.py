@@ -182,3 +182,23 @@ def test_slab_step_kernels_agree(spec, nf, nc, iters, monkeypatch):
     k = np.arange(len(b))
     assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
     assert np.max(np.abs(st_new.u - st_old.u)) <= 1e-8 * np.max(np.abs(st_old.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 6), ("cfg:4:1", 99, 4, 5), ("ex:1:1", 399, 4, 10)])
+def test_even_odd_transforms_agree(spec, nf, nc, iters, monkeypatch):
+    """The even/odd-split DMMA transforms (half sine table, dmma_gemm.cu) against the dense
+    eigenvector GEMMs on meshes with axes of 64+ modes (the reference-parity tests above run
+    coarser meshes).  The two round differently and the iteration amplifies last-bit
+    differences (3D: ~1e-12 at k = 0 growing to ~1e-9), so the bound only has to catch a wrong
+    transform, which would be off at O(1)."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=1)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_eo = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_DENSE_GEMM", "1")
+    ctx_d, _, _ = _ctx(spec, nf, nc)
+    st_d = ctx_d.iterate(opts)
+    a = np.array([h.res_l2 for h in st_eo.history])
+    b = np.array([h.res_l2 for h in st_d.history])
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= 1e-6 * b)
+    assert np.max(np.abs(st_eo.u - st_d.u)) <= 1e-6 * np.max(np.abs(st_d.u))
