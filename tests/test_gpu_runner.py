@@ -81,3 +81,21 @@ def test_sparse_residual_zero_on_holes():
     # test_solver.cpp "skeleton-row residual evaluation tracks the full residual": 1e-6
     for a, b in zip(full.history, sp.history):
         assert abs(a.res_l2 - b.res_l2) <= 1e-6 * a.res_l2
+
+
+def test_cxx_dropin_header_matches_python_api(tmp_path):
+    """The C++ mirror of the reference API (include/asdsm_b200.hpp) drives the same device path:
+    its history equals the Python binding's bit for bit."""
+    from cxx_tools import build_example, run_example
+    exe = build_example(tmp_path)
+    rc, out = run_example(exe, 1, 1, 99, 9, 8, 2)
+    assert rc == 0, out
+    rows = [line.split(",") for line in out.strip().splitlines()]
+    assert rows[-1] == ["stop", "max_iter"]
+    got = np.array([[float(x) for x in r] for r in rows[:-1]])
+    mesh = pb.asdsm.example_mesh(1, 1, 99, 9)
+    ctx = pb.SolverContext(mesh, pb.make_problem(1, 1))
+    st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=8, stagnation_window=0, rng_seed=2))
+    want = np.array([[h.k, h.res_l2, h.res_inf, h.err_max, h.err_l2, h.s_hat] for h in st.history])
+    assert got.shape == want.shape
+    np.testing.assert_array_equal(got[:, :3], want[:, :3])

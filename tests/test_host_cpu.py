@@ -113,3 +113,16 @@ def test_bench_max_over_ranks_gloo():
         p.join(120)
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: 2.5, 1: 2.5}
+
+
+def test_cxx_dropin_header_builds_and_fails_loudly_without_gpu(tmp_path):
+    """include/asdsm_b200.hpp (the reference's asdsm::asdsm_iterate / SolverContext / errors
+    mirrored over the C-ABI) compiles with plain g++, links the in-tree library, and without a GPU
+    the solve throws the CudaFailure class -- no CPU fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by tests/test_gpu_runner.py")
+    from cxx_tools import build_example, run_example
+    exe = build_example(tmp_path)
+    rc, out = run_example(exe, 1, 1, 99, 9, 3)
+    assert rc == 3 and out.startswith("error,CudaFailure"), out
