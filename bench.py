@@ -49,6 +49,20 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(cid, kernel):
+    """DRAM bytes per launch (read + write) of `kernel` at config `cid` from the committed ncu
+    --set full capture (profiles/r*_traffic.json, newest round first), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            k = json.load(open(path))["kernels"].get(f"{cid}/{kernel}")
+        except Exception:
+            continue
+        if k:
+            return float(k["dram_read_bytes"] + k["dram_write_bytes"])
+    return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -270,7 +284,7 @@ def main():
                     "note": "under 1 MB per launch on a handful of SMs: dependency-chain latency, not bandwidth"}
         ach = c["bytes_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e9
         return {"kernel": c["name"], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+                "frac": ach / hbm, "traffic": ncu_traffic(cid, c["name"]), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
     cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
     upd = next((c for c in comps if c["name"] == "update_residual"), cand[0])
