@@ -181,6 +181,36 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     for (int a = 0; a < 3; ++a) A.m[a] = m.n[a] - 1;
     faces3d_ = dev_.alloc<double>(static_cast<size_t>(nholes) * hole3d_face_doubles(A));
     hole3d_prepare(A);
+    // one-kernel fill: padded copies of the hole solver's eigenvector tables
+    const SepSolver& H = sep_hole_;
+    if (!H.complex_modes && H.nd == 2 && H.L == 2 && H.dax[0] == 0 && H.dax[1] == 1 && !H.use_pcr) {
+      Hole3DFusedArgs F{};
+      for (int a = 0; a < 3; ++a) {
+        F.m[a] = H.ext[a];
+        F.n[a] = m.n[a];
+        F.nf[a] = m.nf[a];
+        F.nbox[a] = m.nc[a] + 1;
+      }
+      h3f_causal_ = H.line_right == 0.0;
+      if (hole3d_fused_plan(F, h3f_causal_)) {
+        for (int a = 0; a < 2; ++a) {
+          const int mm = F.m[a];
+          std::vector<double> half(static_cast<size_t>(half_sine_rows(mm)) * 2 * half_sine_kh(mm) + 2 * mm);
+          ASDSM_CUDA_CHECK(cudaMemcpy(half.data(), H.half[a], half.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          const std::vector<double> t = hole3d_half_table(a == 0 ? F.ax : F.ay, half);
+          double* d = dev_.alloc<double>(t.size());
+          ASDSM_CUDA_CHECK(cudaMemcpy(d, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
+          (a == 0 ? F.Hx : F.Hy) = d;
+        }
+        F.st = st_fine_;
+        F.ipiv = H.th_ipiv;
+        F.cp = H.th_cp;
+        F.line_left = H.line_left;
+        hole3d_fused_prepare();
+        h3f_ = F;
+        h3f_ok_ = true;
+      }
+    }
   }
   state_ = dev_.alloc<DevState>(1);
   sep_prepare();
@@ -492,6 +522,10 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.cp = H.th_cp;
     A.line_left = H.line_left;
     A.faces = faces3d_;
+    if (h3f_ok_ && std::getenv("ASDSM_HOLE3D_UNFUSED") == nullptr) {  // (read at capture time)
+      launch_hole3d_fused(e, h3f_, h3f_causal_, state_, s);
+      return;
+    }
     launch_hole3d_faces(e, A, state_, s);
     launch_hole3d_thomas(static_cast<double*>(scratch0_), A, state_, s);
     sep_back_transform(H, scratch0_, hole_array(e), scratch1_, s);

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "holes3d.cuh"
 #include "kernels.cuh"
 #include "merge3d.cuh"
 #include "march.cuh"
@@ -137,6 +138,9 @@ class Solver {
   double* seg1_ = nullptr;
   double* seg2_ = nullptr;
   double* faces3d_ = nullptr;  // 3D fused fill: transformed hole faces
+  Hole3DFusedArgs h3f_{};      // 3D one-kernel fill (holes3d_fused.cu), when the hole fits
+  bool h3f_ok_ = false;
+  bool h3f_causal_ = false;
   std::vector<long long> skel_rows_;  // ascending skeleton rows (subsample > 0), built lazily
   long long* sub_rows_ = nullptr;     // per-iteration sorted subsets, [k][m]
   size_t sub_cap_ = 0;

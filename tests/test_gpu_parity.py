@@ -202,3 +202,29 @@ def test_even_odd_transforms_agree(spec, nf, nc, iters, monkeypatch):
     assert len(a) == len(b)
     assert np.all(np.abs(a - b) <= 1e-6 * b)
     assert np.max(np.abs(st_eo.u - st_d.u)) <= 1e-6 * np.max(np.abs(st_d.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 6), ("cfg:3:0", 29, 4, 6), ("cfg:3:0", 79, 4, 4),
+                                              ("cfg:4:1", 99, 4, 5), ("cfg:4:1", 254, 4, 3), ("cfg:4:3", 29, 4, 6)])
+def test_fused_hole3d_fill_agrees(spec, nf, nc, iters, monkeypatch):
+    """The one-kernel 3D hole fill (holes3d_fused.cu: faces, line solves and both DMMA back
+    transforms per hole in shared memory; SYM schedule for the steady configs, CAUSAL plane
+    streaming for the space-time ones, m = 5 ... 50) against the four-launch path (faces kernel,
+    Thomas kernel, two dense transform GEMMs).  One error guess must agree to rounding; the
+    iteration amplifies last-bit differences, so its bound only has to catch a wrong fill."""
+    ctx, _, _ = _ctx(spec, nf, nc)
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal(ctx.fine_size())
+    e_new = ctx.error_guess(r, 7)
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=1)
+    st_new = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_HOLE3D_UNFUSED", "1")
+    ctx_o, _, _ = _ctx(spec, nf, nc)
+    e_old = ctx_o.error_guess(r, 7)
+    st_old = ctx_o.iterate(opts)
+    assert np.max(np.abs(e_new - e_old)) <= 1e-12 * np.max(np.abs(e_old))
+    a = np.array([h.res_l2 for h in st_new.history])
+    b = np.array([h.res_l2 for h in st_old.history])
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= 1e-6 * b)
+    assert np.max(np.abs(st_new.u - st_old.u)) <= 1e-6 * np.max(np.abs(st_old.u))
