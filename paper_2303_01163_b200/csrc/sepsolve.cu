@@ -7,6 +7,7 @@
 //                      precomputed elimination factors, line held in shared memory
 #include "sepsolve.cuh"
 #include "dmma_gemm.cuh"
+#include "partsolve.cuh"
 
 #include <cstdlib>
 #include <type_traits>
@@ -240,6 +241,85 @@ __global__ void pcr_kernel(PcrArgs<T> A) {
   for (int i = threadIdx.x; i < A.m; i += blockDim.x) d[static_cast<i64>(i) * A.stride_L] = x0[i] * IB[i];
 }
 
+// Lines solved by one warp each with the partition method (SepSolver::part): 8 lines per CTA,
+// the lines and their tables staged in shared memory (consecutive lines are neighbours along the
+// fastest combo axis, so the staging reads 8 adjacent values per line position).
+constexpr int kPartWarps = 8;
+struct PartArgs {
+  double* data;
+  i64 stride_L;
+  int m, ncombo, cext0;
+  i64 cstride0, cstride1;
+  int nbox[3];
+  i64 box_stride[3];
+  i64 nlines;
+  const double* part;
+  int pstride, P, last;
+  double l, r;
+  int line_major;  // stride_L == 1: stage along the line
+};
+
+template <int SEG>
+__global__ void __launch_bounds__(32 * kPartWarps) part_line_kernel(PartArgs A) {
+  extern __shared__ __align__(16) double psm[];
+  double* lines = psm;                        // [kPartWarps][m]
+  double* tabs = psm + kPartWarps * A.m;      // [kPartWarps][pstride]
+  const int warp = threadIdx.x >> 5;
+  const i64 line0 = static_cast<i64>(blockIdx.x) * kPartWarps;
+  auto base_of = [&](i64 line) -> double* {
+    const int combo = static_cast<int>(line % A.ncombo);
+    i64 t = line / A.ncombo;
+    const i64 h0 = t % A.nbox[0];
+    t /= A.nbox[0];
+    const i64 h1 = t % A.nbox[1];
+    const i64 h2 = t / A.nbox[1];
+    const int c0 = combo % A.cext0, c1 = combo / A.cext0;
+    return A.data + h0 * A.box_stride[0] + h1 * A.box_stride[1] + h2 * A.box_stride[2] + c0 * A.cstride0 +
+           c1 * A.cstride1;
+  };
+  __shared__ double* bases[kPartWarps];
+  if (threadIdx.x < kPartWarps) {
+    const i64 line = line0 + threadIdx.x;
+    bases[threadIdx.x] = line < A.nlines ? base_of(line) : nullptr;
+  }
+  for (int q = threadIdx.x; q < kPartWarps * A.pstride; q += blockDim.x) {
+    const int w = q / A.pstride, o = q - w * A.pstride;
+    const i64 line = line0 + w;
+    if (line < A.nlines) cp_async8(tabs + q, A.part + static_cast<i64>(line % A.ncombo) * A.pstride + o);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  __syncthreads();
+  const int n = kPartWarps * A.m;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    int w, p;
+    if (A.line_major) {
+      w = q / A.m;
+      p = q - w * A.m;
+    } else {
+      p = q / kPartWarps;
+      w = q - p * kPartWarps;
+    }
+    const double* b = bases[w];
+    lines[w * A.m + p] = b ? b[static_cast<i64>(p) * A.stride_L] : 0.0;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  if (bases[warp]) part_solve_line<SEG>(lines + warp * A.m, tabs + warp * A.pstride, A.m, A.P, A.last, A.l, A.r);
+  __syncthreads();
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    int w, p;
+    if (A.line_major) {
+      w = q / A.m;
+      p = q - w * A.m;
+    } else {
+      p = q / kPartWarps;
+      w = q - p * kPartWarps;
+    }
+    double* b = bases[w];
+    if (b) b[static_cast<i64>(p) * A.stride_L] = lines[w * A.m + p];
+  }
+}
+
 // Compact mode layout of a batch: element strides (1, e0, e0*e1), boxes back to back.
 BoxArray compact_layout(const SepSolver& S, const BoxArray& like, void* ptr) {
   BoxArray b;
@@ -339,6 +419,42 @@ void launch_line_solve(const SepSolver& S, const BoxArray& buf, cudaStream_t st)
     A.left = S.line_left;
     const int bs = 128;
     thomas_kernel<T><<<static_cast<unsigned>((A.nlines + bs - 1) / bs), bs, 0, st>>>(A);
+  } else if (std::is_same<T, double>::value && S.part != nullptr && !S.complex_modes &&
+             std::getenv("ASDSM_PCR_LINES") == nullptr) {  // (read at capture time)
+    PartArgs A{};
+    A.data = reinterpret_cast<double*>(buf.ptr);
+    A.stride_L = buf.stride[S.L];
+    A.m = S.ext[S.L];
+    A.ncombo = S.ncombo;
+    A.cext0 = cax[0] >= 0 ? S.ext[cax[0]] : 1;
+    A.cstride0 = cax[0] >= 0 ? buf.stride[cax[0]] : 0;
+    A.cstride1 = cax[1] >= 0 ? buf.stride[cax[1]] : 0;
+    for (int a = 0; a < 3; ++a) {
+      A.nbox[a] = buf.nbox[a];
+      A.box_stride[a] = buf.box_stride[a];
+    }
+    A.nlines = nb * S.ncombo;
+    A.part = S.part;
+    A.pstride = S.part_stride;
+    A.P = S.part_P;
+    A.last = S.part_last;
+    A.l = S.line_left;
+    A.r = S.line_right;
+    A.line_major = A.stride_L == 1 ? 1 : 0;
+    const size_t smem = sizeof(double) * kPartWarps * (static_cast<size_t>(A.m) + A.pstride);
+    if (smem > kPcrMaxSmem) throw AsdsmError(kUnsupported, "partitioned line solve exceeds shared memory");
+    const unsigned grid = static_cast<unsigned>((A.nlines + kPartWarps - 1) / kPartWarps);
+    switch (S.part_seg) {
+      case 2: part_line_kernel<2><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 4: part_line_kernel<4><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 8: part_line_kernel<8><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 12: part_line_kernel<12><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 16: part_line_kernel<16><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 20: part_line_kernel<20><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 24: part_line_kernel<24><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      case 28: part_line_kernel<28><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+      default: part_line_kernel<32><<<grid, 32 * kPartWarps, smem, st>>>(A); break;
+    }
   } else {
     PcrArgs<T> A{};
     A.data = reinterpret_cast<T*>(buf.ptr);
@@ -383,6 +499,15 @@ void sep_prepare() {
   if (done) return;
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(pcr_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(pcr_kernel<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(part_line_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPcrMaxSmem));
   done = true;
 }
 

@@ -228,3 +228,24 @@ def test_fused_hole3d_fill_agrees(spec, nf, nc, iters, monkeypatch):
     assert len(a) == len(b)
     assert np.all(np.abs(a - b) <= 1e-6 * b)
     assert np.max(np.abs(st_new.u - st_old.u)) <= 1e-6 * np.max(np.abs(st_old.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 4, 5), ("cfg:3:0", 29, 4, 6)])
+def test_partitioned_slab_lines_agree(spec, nf, nc, iters, monkeypatch):
+    """Slab line solves by the warp partition method (sepsolve.cu part_line_kernel: segment
+    Thomas in registers + shuffle PCR over the separators) against the cyclic-reduction CTA per
+    line (pcr_kernel).  Both are exact tridiagonal solvers; one error guess agrees to rounding."""
+    ctx, _, _ = _ctx(spec, nf, nc)
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(ctx.fine_size())
+    e_new = ctx.error_guess(r, 3)
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=2)
+    st_new = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_PCR_LINES", "1")
+    ctx_o, _, _ = _ctx(spec, nf, nc)
+    e_old = ctx_o.error_guess(r, 3)
+    st_old = ctx_o.iterate(opts)
+    assert np.max(np.abs(e_new - e_old)) <= 1e-11 * np.max(np.abs(e_old))
+    a = np.array([h.res_l2 for h in st_new.history])
+    b = np.array([h.res_l2 for h in st_old.history])
+    assert np.all(np.abs(a - b) <= 1e-6 * b)
