@@ -88,7 +88,8 @@ _lib = None
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "libasdsm_b200.so")
+    # ASDSM_LIB: an instrumented build of the same library (profiling only)
+    return os.environ.get("ASDSM_LIB") or os.path.join(_HERE, "libasdsm_b200.so")
 
 
 class _Options(ctypes.Structure):
