@@ -9,6 +9,7 @@
 #include "dmma_gemm.cuh"
 #include "partsolve.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -57,6 +58,45 @@ __device__ __forceinline__ void line_bases(const LineMap& M, i64 p, i64& ib, i64
   const i64 h2 = t / M.nbox[1];
   ib = h0 * M.in_bs[0] + h1 * M.in_bs[1] + h2 * M.in_bs[2] + o0 * M.o_in[0] + o1 * M.o_in[1];
   ob = h0 * M.out_bs[0] + h1 * M.out_bs[1] + h2 * M.out_bs[2] + o0 * M.o_out[0] + o1 * M.o_out[1];
+}
+
+// Short axes (m <= kSmallModes, e.g. the coarse axis of a slab): one thread per line, the m
+// inputs in registers, the m x m matrix in shared memory -- the pass is a pure stream (the tiled
+// GEMMs spend a 64-wide output tile on m outputs).  32-bit line decomposition.
+constexpr int kSmallModes = 16;
+__global__ void __launch_bounds__(256) small_transform_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                              const double* __restrict__ mat, int m, i64 in_es,
+                                                              i64 out_es, LineMap M) {
+  __shared__ double sm[kSmallModes * kSmallModes];
+  for (int q = threadIdx.x; q < m * m; q += blockDim.x) sm[q] = mat[q];
+  __syncthreads();
+  const int n = static_cast<int>(M.nlines);
+  const int e0 = M.o_ext[0], e1 = M.o_ext[1], b0 = M.nbox[0], b1 = M.nbox[1];
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    int t = p;
+    const int o0 = t % e0;
+    t /= e0;
+    const int o1 = t % e1;
+    t /= e1;
+    const int h0 = t % b0;
+    t /= b0;
+    const int h1 = t % b1;
+    const int h2 = t / b1;
+    const i64 ib = h0 * M.in_bs[0] + h1 * M.in_bs[1] + h2 * M.in_bs[2] + o0 * M.o_in[0] + o1 * M.o_in[1];
+    const i64 ob = h0 * M.out_bs[0] + h1 * M.out_bs[1] + h2 * M.out_bs[2] + o0 * M.o_out[0] + o1 * M.o_out[1];
+    double x[kSmallModes];
+#pragma unroll
+    for (int k = 0; k < kSmallModes; ++k) x[k] = k < m ? __ldg(in + ib + k * in_es) : 0.0;
+#pragma unroll
+    for (int q = 0; q < kSmallModes; ++q) {
+      if (q >= m) break;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kSmallModes; ++k)
+        if (k < m) acc = fma(x[k], sm[q * m + k], acc);
+      out[ob + q * out_es] = acc;
+    }
+  }
 }
 
 // out(line, q) = sum_k in(line, k) * Mat[q][k]
@@ -364,6 +404,13 @@ void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const Bo
   if constexpr (std::is_same<TIn, double>::value && std::is_same<TMat, double>::value &&
                 std::is_same<TOut, double>::value) {
     static const bool scalar = std::getenv("ASDSM_SCALAR_GEMM") != nullptr;
+    if (m <= kSmallModes && M.nlines < (1LL << 31) && std::getenv("ASDSM_NO_SMALL_TRANSFORM") == nullptr) {
+      const i64 nb = std::min<i64>((M.nlines + 255) / 256, 16LL * kNumSms);
+      small_transform_kernel<<<static_cast<unsigned>(nb), 256, 0, st>>>(ip, op, mat, m, in.stride[axis], out.stride[axis], M);
+      ASDSM_CUDA_CHECK(cudaGetLastError());
+      ++g_kernel_launches;
+      return;
+    }
     if (!scalar) {
       GemmLines G{};
       for (int i = 0; i < 2; ++i) {

@@ -249,3 +249,23 @@ def test_partitioned_slab_lines_agree(spec, nf, nc, iters, monkeypatch):
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
     assert np.all(np.abs(a - b) <= 1e-6 * b)
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:1:1", 399, 9, 6)])
+def test_small_axis_transform_agrees(spec, nf, nc, iters, monkeypatch):
+    """Short-axis eigenvector transforms as a thread-per-line stream (sepsolve.cu
+    small_transform_kernel, m <= 16: the coarse axis of every slab) against the tiled DMMA GEMM."""
+    ctx, _, _ = _ctx(spec, nf, nc)
+    rng = np.random.default_rng(13)
+    r = rng.standard_normal(ctx.fine_size())
+    e_new = ctx.error_guess(r, 5)
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=6)
+    st_new = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_NO_SMALL_TRANSFORM", "1")
+    ctx_o, _, _ = _ctx(spec, nf, nc)
+    e_old = ctx_o.error_guess(r, 5)
+    st_old = ctx_o.iterate(opts)
+    assert np.max(np.abs(e_new - e_old)) <= 1e-11 * np.max(np.abs(e_old))
+    a = np.array([h.res_l2 for h in st_new.history])
+    b = np.array([h.res_l2 for h in st_old.history])
+    assert np.all(np.abs(a - b) <= 1e-6 * b)
