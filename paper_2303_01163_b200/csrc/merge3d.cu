@@ -220,6 +220,7 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int a, int stage, const DevState
   const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2], nf1 = m.nf[c.f1], nf2 = m.nf[c.f2];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   double y[kMaxKnots], dg[kMaxKnots], up[kMaxKnots], rh[kMaxKnots];
+  auto yl = [&](int q) { return y[q]; };
   if (stage == 0) {
     const int n1 = ncA * nf2, n2 = ncA * nf1, n3 = ncA * nc2;
     if (t < n1) {
@@ -227,21 +228,27 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int a, int stage, const DevState
       y[0] = 0.0;
       y[nc1 + 1] = 0.0;
       for (int C = 0; C < nc1; ++C) y[C + 1] = fam1_y(m, c, I, k2, C);
-      spline_second_derivs(m, c.f1, y, A.mF1[a] + static_cast<i64>(t) * (nc1 + 2), dg, up, rh);
+      double* mm = A.mF1[a] + static_cast<i64>(t) * (nc1 + 2);
+      spline_second_derivs(m, c.f1, y, mm, dg, up, rh);
+      spline_segments(m, c.f1, yl, mm, A.sF1[a] + static_cast<i64>(t) * 4 * (nc1 + 1));
     } else if (t < n1 + n2) {
       const int l = t - n1;
       const int I = l % ncA, k1 = l / ncA;
       y[0] = 0.0;
       y[nc2 + 1] = 0.0;
       for (int C = 0; C < nc2; ++C) y[C + 1] = fam2_y(m, c, I, k1, C);
-      spline_second_derivs(m, c.f2, y, A.mF2[a] + static_cast<i64>(l) * (nc2 + 2), dg, up, rh);
+      double* mm = A.mF2[a] + static_cast<i64>(l) * (nc2 + 2);
+      spline_second_derivs(m, c.f2, y, mm, dg, up, rh);
+      spline_segments(m, c.f2, yl, mm, A.sF2[a] + static_cast<i64>(l) * 4 * (nc2 + 1));
     } else if (t < n1 + n2 + n3) {
       const int l = t - n1 - n2;
       const int I = l % ncA, C2 = l / ncA;
       y[0] = 0.0;
       y[nc1 + 1] = 0.0;
       for (int C = 0; C < nc1; ++C) y[C + 1] = fam3_y(A, c, I, C2, C);
-      spline_second_derivs(m, c.f1, y, A.mF3a[a] + static_cast<i64>(l) * (nc1 + 2), dg, up, rh);
+      double* mm = A.mF3a[a] + static_cast<i64>(l) * (nc1 + 2);
+      spline_second_derivs(m, c.f1, y, mm, dg, up, rh);
+      spline_segments(m, c.f1, yl, mm, A.sF3a[a] + static_cast<i64>(l) * 4 * (nc1 + 1));
     }
   } else {
     // fam3b: (I, k1), y = g(I, k1, C2) = fam3a spline (I, C2) at k1
@@ -250,42 +257,35 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int a, int stage, const DevState
     const int I = t % ncA, k1 = t / ncA;
     y[0] = 0.0;
     y[nc2 + 1] = 0.0;
-    for (int C2 = 0; C2 < nc2; ++C2) {
-      const double* mm = A.mF3a[a] + static_cast<i64>(I + ncA * C2) * (nc1 + 2);
-      auto yv = [&](int q) -> double { return (q == 0 || q == nc1 + 1) ? 0.0 : fam3_y(A, c, I, C2, q - 1); };
-      y[C2 + 1] = spline_eval(m, c.f1, yv, mm, k1 + 1);
-    }
-    spline_second_derivs(m, c.f2, y, A.mF3b[a] + static_cast<i64>(t) * (nc2 + 2), dg, up, rh);
-    for (int q = 0; q < nc2 + 2; ++q) A.g3[a][static_cast<i64>(t) * (nc2 + 2) + q] = y[q];
+    for (int C2 = 0; C2 < nc2; ++C2)
+      y[C2 + 1] = spline_eval_seg(m, c.f1, A.sF3a[a] + static_cast<i64>(I + ncA * C2) * 4 * (nc1 + 1), k1 + 1);
+    double* mm = A.mF3b[a] + static_cast<i64>(t) * (nc2 + 2);
+    spline_second_derivs(m, c.f2, y, mm, dg, up, rh);
+    spline_segments(m, c.f2, yl, mm, A.sF3b[a] + static_cast<i64>(t) * 4 * (nc2 + 1));
   }
+  (void)nf2;
 }
 
-// corrected slab a = slab + ((s1 + s2) - s3) at every slab point (solver.cpp:289-292)
+// corrected slab a = slab + ((s1 + s2) - s3) at every slab point (solver.cpp:289-292), each
+// spline from its line's segment table
 __global__ void m3_apply_kernel(Merge3DArgs A, int a, const DevState* st) {
   if (!st->active || !st->have_e) return;
   const MeshDev& m = A.m;
   const PlaneCtx c = plane_ctx(A, a);
-  const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2], nf1 = m.nf[c.f1];
+  const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2];
+  const int e0 = c.se.e[0], e1 = c.se.e[1];
   const i64 total = static_cast<i64>(c.se.e[0]) * c.se.e[1] * c.se.e[2];
   for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += static_cast<i64>(gridDim.x) * blockDim.x) {
     int q[3];
-    q[0] = static_cast<int>(t % c.se.e[0]);
-    q[1] = static_cast<int>((t / c.se.e[0]) % c.se.e[1]);
-    q[2] = static_cast<int>(t / (static_cast<i64>(c.se.e[0]) * c.se.e[1]));
+    const i64 r = t / e0;
+    q[0] = static_cast<int>(t - r * e0);
+    q[1] = static_cast<int>(r % e1);
+    q[2] = static_cast<int>(r / e1);
     const int I = q[a], k1 = q[c.f1], k2 = q[c.f2];
-    const double* m1 = A.mF1[a] + static_cast<i64>(I + ncA * k2) * (nc1 + 2);
-    auto y1 = [&](int C) -> double { return (C == 0 || C == nc1 + 1) ? 0.0 : fam1_y(m, c, I, k2, C - 1); };
-    const double s1 = spline_eval(m, c.f1, y1, m1, k1 + 1);
-    const double* m2 = A.mF2[a] + static_cast<i64>(I + ncA * k1) * (nc2 + 2);
-    auto y2 = [&](int C) -> double { return (C == 0 || C == nc2 + 1) ? 0.0 : fam2_y(m, c, I, k1, C - 1); };
-    const double s2 = spline_eval(m, c.f2, y2, m2, k2 + 1);
-    const i64 l3 = I + static_cast<i64>(ncA) * k1;
-    const double* m3 = A.mF3b[a] + l3 * (nc2 + 2);
-    const double* g = A.g3[a] + l3 * (nc2 + 2);
-    auto y3 = [&](int C) -> double { return g[C]; };
-    const double s3 = spline_eval(m, c.f2, y3, m3, k2 + 1);
-    (void)nf1;
+    const double s1 = spline_eval_seg(m, c.f1, A.sF1[a] + static_cast<i64>(I + ncA * k2) * 4 * (nc1 + 1), k1 + 1);
+    const double s2 = spline_eval_seg(m, c.f2, A.sF2[a] + static_cast<i64>(I + ncA * k1) * 4 * (nc2 + 1), k2 + 1);
+    const double s3 = spline_eval_seg(m, c.f2, A.sF3b[a] + static_cast<i64>(I + ncA * k1) * 4 * (nc2 + 1), k2 + 1);
     A.corrected[a][t] = __dadd_rn(c.slab[t], __dsub_rn(__dadd_rn(s1, s2), s3));
   }
 }

@@ -18,6 +18,10 @@ struct Merge3DArgs {
   double* mF3b[3];         // (nc_a*nf_f1) x (nc_f2+2)
   double* g3[3];           // (nc_a*nf_f1) x (nc_f2+2): knot values of fam3b lines
   double* corrected[3];    // corrected slabs
+  double* sF1[3];          // per-interval spline coefficients (nc+1 x 4) of the fam1, fam2,
+  double* sF2[3];          // fam3a and fam3b lines (spline_segments)
+  double* sF3a[3];
+  double* sF3b[3];
 };
 
 void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_t s);

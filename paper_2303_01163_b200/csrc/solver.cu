@@ -173,6 +173,10 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
       m3_.mF3b[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * (m.nc[f2] + 2));
       m3_.g3[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * (m.nc[f2] + 2));
       m3_.corrected[a] = dev_.alloc<double>(static_cast<size_t>(g_slab_[a].size));
+      m3_.sF1[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f2] * 4 * (m.nc[f1] + 1));
+      m3_.sF2[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * 4 * (m.nc[f2] + 1));
+      m3_.sF3a[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nc[f2] * 4 * (m.nc[f1] + 1));
+      m3_.sF3b[a] = dev_.alloc<double>(static_cast<size_t>(m.nc[a]) * m.nf[f1] * 4 * (m.nc[f2] + 1));
     }
   }
   partials_ = dev_.alloc<double>(4 * static_cast<size_t>(kRedStride));
