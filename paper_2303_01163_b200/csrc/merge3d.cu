@@ -12,6 +12,8 @@
 #include "merge3d.cuh"
 #include "spline.cuh"
 
+#include <algorithm>
+
 namespace asdsm_b200 {
 
 namespace {
@@ -213,8 +215,9 @@ __device__ __forceinline__ double fam3_y(const Merge3DArgs& A, const PlaneCtx& c
 // Line families per slab a (offsets in Merge3DArgs):
 //   fam1: (I, k2) along f1, nc_f1 knots     fam2: (I, k1) along f2, nc_f2 knots
 //   fam3a: (I, C2) along f1                 fam3b: (I, k1) along f2 through g(I, k1, :)
-__global__ void m3_derivs_kernel(Merge3DArgs A, int a, int stage, const DevState* st) {
+__global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
   if (!st->active || !st->have_e) return;
+  const int a = blockIdx.y;  // slab
   const MeshDev& m = A.m;
   const PlaneCtx c = plane_ctx(A, a);
   const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2], nf1 = m.nf[c.f1], nf2 = m.nf[c.f2];
@@ -268,8 +271,9 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int a, int stage, const DevState
 
 // corrected slab a = slab + ((s1 + s2) - s3) at every slab point (solver.cpp:289-292), each
 // spline from its line's segment table
-__global__ void m3_apply_kernel(Merge3DArgs A, int a, const DevState* st) {
+__global__ void m3_apply_kernel(Merge3DArgs A, const DevState* st) {
   if (!st->active || !st->have_e) return;
+  const int a = blockIdx.y;  // slab
   const MeshDev& m = A.m;
   const PlaneCtx c = plane_ctx(A, a);
   const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2];
@@ -376,16 +380,19 @@ void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_
   }
   m2_fill_kernel<<<nblk(npair, 256), 256, 0, s>>>(A, st);
   g_kernel_launches += 3;
+  // the three slabs' corrections are independent: one launch per stage covers all of them
+  int nl = 0, nl3 = 0;
+  i64 ns = 0;
   for (int a = 0; a < 3; ++a) {
     const int f1 = (a == 0) ? 1 : 0, f2 = (a == 2) ? 1 : 2;
-    const int nl = m.nc[a] * (m.nf[f2] + m.nf[f1] + m.nc[f2]);
-    m3_derivs_kernel<<<(nl + 63) / 64, 64, 0, s>>>(A, a, 0, st);
-    const int nl3 = m.nc[a] * m.nf[f1];
-    m3_derivs_kernel<<<(nl3 + 63) / 64, 64, 0, s>>>(A, a, 1, st);
-    const i64 ns = static_cast<i64>(m.nc[a]) * m.nf[f1] * m.nf[f2];
-    m3_apply_kernel<<<nblk(ns, 256), 256, 0, s>>>(A, a, st);
-    g_kernel_launches += 3;
+    nl = std::max(nl, m.nc[a] * (m.nf[f2] + m.nf[f1] + m.nc[f2]));
+    nl3 = std::max(nl3, m.nc[a] * m.nf[f1]);
+    ns = std::max(ns, static_cast<i64>(m.nc[a]) * m.nf[f1] * m.nf[f2]);
   }
+  m3_derivs_kernel<<<dim3((nl + 31) / 32, 3), 32, 0, s>>>(A, 0, st);
+  m3_derivs_kernel<<<dim3((nl3 + 31) / 32, 3), 32, 0, s>>>(A, 1, st);
+  m3_apply_kernel<<<dim3(nblk(ns, 256, 3 * kNumSms), 3), 256, 0, s>>>(A, st);
+  g_kernel_launches += 3;
   const i64 nskel = static_cast<i64>(m.nc[0]) * m.nf[1] * m.nf[2] +
                    static_cast<i64>(m.nf[0] - m.nc[0]) * m.nc[1] * m.nf[2] +
                    static_cast<i64>(m.nf[0] - m.nc[0]) * (m.nf[1] - m.nc[1]) * m.nc[2];
