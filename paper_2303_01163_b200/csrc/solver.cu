@@ -144,6 +144,18 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   if (!variable_) scratch = std::max(scratch, sep_scratch_bytes(sep_coarse_, 1));
   scratch0_ = dev_.alloc<unsigned char>(scratch);
   scratch1_ = dev_.alloc<unsigned char>(scratch);
+  if (m.dim == 3 && !variable_) {
+    // the three slab solves of an iteration are independent: slabs 1 and 2 run on their own
+    // streams (forked / joined with events, captured into the graph as parallel branches),
+    // each with its own mode-space scratch
+    for (int a = 1; a < 3; ++a) {
+      const size_t sa = sep_scratch_bytes(sep_slab_[a], 1);
+      slab_scr_[a][0] = dev_.alloc<unsigned char>(sa);
+      slab_scr_[a][1] = dev_.alloc<unsigned char>(sa);
+      ASDSM_CUDA_CHECK(cudaStreamCreateWithFlags(&aux_[a - 1], cudaStreamNonBlocking));
+    }
+    for (int i = 0; i < 3; ++i) ASDSM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming));
+  }
   b_coarse_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
   u_cc_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
   cc_e1_ = dev_.alloc<double>(static_cast<size_t>(g_coarse_.size));
@@ -289,6 +301,10 @@ void Solver::set_bundle(const double* b_fine, const double* const* b_slab, const
 
 Solver::~Solver() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  for (cudaStream_t& q : aux_)
+    if (q) cudaStreamDestroy(q);
+  for (cudaEvent_t& e : ev_)
+    if (e) cudaEventDestroy(e);
 }
 
 void Solver::reset_state(const RunOptions& o, cudaStream_t s) {
@@ -651,15 +667,28 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
     fill(out, nullptr, s);
     return;
   }
+  const bool fork = aux_[0] != nullptr && std::getenv("ASDSM_SERIAL_SLABS") == nullptr;  // (read at capture time)
+  if (fork) {
+    ASDSM_CUDA_CHECK(cudaEventRecord(ev_[0], s));
+    for (cudaStream_t q : aux_) ASDSM_CUDA_CHECK(cudaStreamWaitEvent(q, ev_[0], 0));
+  }
   for (int a = 0; a < mesh_.dim; ++a) {
     if (variable_) {
       launch_gather(r0, r1, sol_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
       solve_box(a, sol_slab_[a], s);
       continue;
     }
-    launch_gather(r0, r1, rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);
-    sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]), scratch0_,
-              scratch1_, s);
+    const bool own = fork && a > 0;
+    cudaStream_t q = own ? aux_[a - 1] : s;
+    launch_gather(r0, r1, rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, q);
+    sep_solve(sep_slab_[a], kind_array(g_slab_[a], rhs_slab_[a]), kind_array(g_slab_[a], sol_slab_[a]),
+              own ? slab_scr_[a][0] : scratch0_, own ? slab_scr_[a][1] : scratch1_, q);
+  }
+  if (fork) {
+    for (int i = 0; i < 2; ++i) {
+      ASDSM_CUDA_CHECK(cudaEventRecord(ev_[1 + i], aux_[i]));
+      ASDSM_CUDA_CHECK(cudaStreamWaitEvent(s, ev_[1 + i], 0));
+    }
   }
   for (int a = 0; a < mesh_.dim; ++a) {
     CtrlArgs c{};

@@ -149,6 +149,9 @@ class Solver {
   SlabStep2DArgs slabstep2d_args(const int* coin, double* out) const;
   void* scratch0_ = nullptr;
   void* scratch1_ = nullptr;
+  void* slab_scr_[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // 3D: slabs 1, 2
+  cudaStream_t aux_[2] = {nullptr, nullptr};  // 3D: streams of slabs 1 and 2
+  cudaEvent_t ev_[3] = {nullptr, nullptr, nullptr};
   double* partials_ = nullptr;
   DevState* state_ = nullptr;
   double* history_ = nullptr;
