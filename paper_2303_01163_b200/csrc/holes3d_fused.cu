@@ -27,6 +27,7 @@
 #include "holes3d.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace asdsm_b200 {
@@ -131,7 +132,7 @@ __device__ __forceinline__ void fwd_dots(const HalfTab& T, int nv, const double*
 // Back transform of `np` consecutive planes held in X (plane stride rp*skx; row r(l), column
 // c(k); finite everywhere, zero where no mode lives), planes t0.. of the hole.
 __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const HalfTab& Ty, const Hole3DFusedArgs& A,
-                            const Geo& h, double* __restrict__ e) {
+                            const Geo& h, double* __restrict__ e, long long* tr = nullptr) {
   const int mx = A.m[0], my = A.m[1];
   const int skx = A.lay.skx, rp = A.lay.rp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -180,6 +181,7 @@ __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const 
     }
   }
   __syncthreads();
+  if (tr) *tr = clock64();
   // ---- step B: out[t][j][i] = sum_l Vy[j][l] P[t][l][i] (rows of P in even/odd order)
   const i64 sy = A.nf[0], sz = static_cast<i64>(A.nf[0]) * A.nf[1];
   const int nty = (Ty.he + 7) >> 3;
@@ -427,8 +429,7 @@ __global__ void __launch_bounds__(kH3Threads, 1)
   const int TC = L.tc;
   const int nring = 2 * my + 2 * mx;   // per plane: A0[my] A1[my] B0[mx] B1[mx]
   double* CH0 = sm + L.faces;          // [my][mx]
-  double* R = CH0 + my * mx;           // [TC][nring] ring values of the chunk
-  double* V = R + TC * nring;          // [TC][nring] YA+ YA- XB+ XB- of the chunk
+  double* V = CH0 + my * mx;           // [TC][nring] YA+ YA- XB+ XB- of the chunk
   double* HB = V + TC * nring;         // pair sums: [TC][2][2 he_y] then [TC][2][2 he_x]
   double* HBx = HB + TC * 4 * Ty.he;
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -446,49 +447,106 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     yv[u] = 0.0;
     kl[u] = c < ncombo ? (c % mx) | ((c / mx) << 16) : -1;
   }
-  auto ring_of = [&](int q, int t) -> double {
-    if (q < 2 * my) {
-      const int f = q / my, j = q - f * my;
-      return (f == 0 || mx > 1) ? ring_val(e, A, h, f == 0 ? 0 : mx - 1, j, t) : 0.0;
+  // Ring values from raw skeleton values staged through shared memory one chunk ahead
+  // (cp.async: no registers wait on the loads).  Per plane: XL[j] = e(ox-1, oy+j), XR[j] =
+  // e(ox+mx, oy+j), YL[i] = e(ox+i, oy-1), YR[i] = e(ox+i, oy+my); plane 0 also needs the
+  // values below the hole at the face points (RZ, same layout as the ring vectors).  Same
+  // terms and order as ring_val, so the values are bitwise the same.
+  double* RAW = HBx + TC * 4 * Tx.he;  // [2][TC][nring]
+  double* RZ = RAW + 2 * TC * nring;   // [nring]
+  const Stencil& stn = A.st;
+  const i64 esy = A.nf[0], esz = static_cast<i64>(A.nf[0]) * A.nf[1];
+  const bool hxl = h.ox > 0, hxr = h.ox + mx < A.nf[0] && stn.has_right[0];
+  const bool hyl = h.oy > 0, hyr = h.oy + my < A.nf[1] && stn.has_right[1];
+  auto stage_raw = [&](int c) {
+    const int t0c = c * TC;
+    if (t0c < mt) {
+      double* dst = RAW + (c & 1) * TC * nring;
+      const int npc = min(TC, mt - t0c);
+      for (int q = tid; q < npc * nring; q += kH3Threads) {
+        const int tt = q / nring, r = q - tt * nring;
+        const i64 zo = (h.oz + t0c + tt) * esz;
+        bool ok;
+        i64 p;
+        if (r < 2 * my) {
+          const int f = r / my, j = r - f * my;
+          ok = f == 0 ? hxl : hxr;
+          p = (f == 0 ? h.ox - 1 : h.ox + mx) + (h.oy + j) * esy + zo;
+        } else {
+          const int r2 = r - 2 * my, f = r2 / mx, i = r2 - f * mx;
+          ok = f == 0 ? hyl : hyr;
+          p = (h.ox + i) + (f == 0 ? h.oy - 1 : h.oy + my) * esy + zo;
+        }
+        if (ok) cp_async8(dst + q, e + p);
+        else dst[q] = 0.0;
+      }
     }
-    const int r = q - 2 * my, f = r / mx, i = r - f * mx;
-    return ((f == 0 || my > 1) && i > 0 && i < mx - 1) ? ring_val(e, A, h, i, f == 0 ? 0 : my - 1, t) : 0.0;
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  constexpr int kRingPer = 4;  // ring values per thread per chunk (TC * nring <= 2048)
-  double rv[kRingPer];
-  auto fetch = [&](int t0) {
-#pragma unroll
-    for (int u = 0; u < kRingPer; ++u) {
-      const int q = tid + u * kH3Threads;
-      const int tt = q / nring, qq = q - tt * nring;
-      rv[u] = (tt < TC && t0 + tt < mt) ? ring_of(qq, t0 + tt) : 0.0;
+  auto ring_raw = [&](const double* rp, double ez, int i, int j, bool t0) -> double {
+    double acc = 0.0;
+    if (t0 && h.oz > 0) acc = __dadd_rn(acc, __dmul_rn(stn.left[2], ez));
+    if (j == 0 && hyl) acc = __dadd_rn(acc, __dmul_rn(stn.left[1], rp[2 * my + i]));
+    if (i == 0 && hxl) acc = __dadd_rn(acc, __dmul_rn(stn.left[0], rp[j]));
+    if (i == mx - 1 && hxr) acc = __dadd_rn(acc, __dmul_rn(stn.right[0], rp[my + j]));
+    if (j == my - 1 && hyr) acc = __dadd_rn(acc, __dmul_rn(stn.right[1], rp[2 * my + mx + i]));
+    return __dsub_rn(0.0, acc);
+  };
+  // values below the hole at the face points of plane 0 (x faces all j, y faces all i)
+  if (h.oz > 0)
+    for (int r = tid; r < nring; r += kH3Threads) {
+      int i, j;
+      if (r < 2 * my) {
+        const int f = r / my;
+        j = r - f * my;
+        i = f == 0 ? 0 : mx - 1;
+      } else {
+        const int r2 = r - 2 * my, f = r2 / mx;
+        i = r2 - f * mx;
+        j = f == 0 ? 0 : my - 1;
+      }
+      cp_async8(RZ + r, e + (h.ox + i) + (h.oy + j) * esy + (h.oz - 1) * esz);
     }
-  };
-  fetch(0);
+  stage_raw(0);
+  stage_raw(1);
+#ifdef ASDSM_H3_TRACE
+  long long ph[4] = {0, 0, 0, 0}, c0 = clock64(), c1, c2, c3, c4;
+#endif
   for (int t0 = 0; t0 < mt; t0 += TC) {
     const int np = min(TC, mt - t0);
-#pragma unroll
-    for (int u = 0; u < kRingPer; ++u) {
-      const int q = tid + u * kH3Threads;
-      if (q < TC * nring) R[q] = rv[u];
-    }
+    const int ci = t0 / TC;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
-    if (t0 + TC < mt) fetch(t0 + TC);
+    const double* RW = RAW + (ci & 1) * TC * nring;
     // vectors: (plane, sign) -> y transform of cx0 A0 +/- cx1 A1, x transform of cy0 B0 +/- cy1 B1
     fwd_pairs(Ty, 2 * np, [&](int v, int j) {
-      const double* Rp = R + (v >> 1) * nring;
-      const double a0 = cx0 * Rp[j], a1 = cx1 * Rp[my + j];
+      const int tt = v >> 1;
+      const double* rp = RW + tt * nring;
+      const bool z0 = t0 + tt == 0;
+      const double r0 = ring_raw(rp, RZ[j], 0, j, z0);
+      const double r1 = mx > 1 ? ring_raw(rp, RZ[my + j], mx - 1, j, z0) : 0.0;
+      const double a0 = cx0 * r0, a1 = cx1 * r1;
       return (v & 1) ? a0 - a1 : a0 + a1;
     }, HB);
     fwd_pairs(Tx, 2 * np, [&](int v, int i) {
-      const double* Rp = R + (v >> 1) * nring + 2 * my;
-      const double b0 = cy0 * Rp[i], b1 = cy1 * Rp[mx + i];
+      const int tt = v >> 1;
+      const double* rp = RW + tt * nring;
+      const bool z0 = t0 + tt == 0;
+      const bool mid = i > 0 && i < mx - 1;
+      const double r0 = mid ? ring_raw(rp, RZ[2 * my + i], i, 0, z0) : 0.0;
+      const double r1 = (mid && my > 1) ? ring_raw(rp, RZ[2 * my + mx + i], i, my - 1, z0) : 0.0;
+      const double b0 = cy0 * r0, b1 = cy1 * r1;
       return (v & 1) ? b0 - b1 : b0 + b1;
     }, HBx);
     __syncthreads();
+    stage_raw(ci + 2);  // this chunk's raw values are consumed (pair sums formed)
     fwd_dots(Ty, 2 * np, HB, [&](int v, int l, double x) { V[(v >> 1) * nring + (v & 1) * my + l] = x; });
     fwd_dots(Tx, 2 * np, HBx, [&](int v, int k, double x) { V[(v >> 1) * nring + 2 * my + (v & 1) * mx + k] = x; });
     __syncthreads();
+#ifdef ASDSM_H3_TRACE
+    c1 = clock64();
+    ph[0] += c1 - c0;
+#endif
     double iv[kCausalLines];  // bidiagonal: one pivot per line for every t (L1-resident table)
 #pragma unroll
     for (int u = 0; u < kCausalLines; ++u) iv[u] = kl[u] >= 0 ? __ldg(A.ipiv + tid + u * kH3Threads) : 0.0;
@@ -509,9 +567,24 @@ __global__ void __launch_bounds__(kH3Threads, 1)
       }
     }
     __syncthreads();
+#ifdef ASDSM_H3_TRACE
+    c2 = clock64();
+    back_planes(X, np, t0, Tx, Ty, A, h, e, &c3);
+    __syncthreads();
+    c4 = clock64();
+    ph[1] += c2 - c1;
+    ph[2] += c3 - c2;
+    ph[3] += c4 - c3;
+    c0 = c4;
+#else
     back_planes(X, np, t0, Tx, Ty, A, h, e);
     __syncthreads();
+#endif
   }
+#ifdef ASDSM_H3_TRACE
+  if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 500))
+    printf("H3TRACE blk %d fwd %lld thomas %lld stepA %lld stepB %lld\n", blockIdx.x, ph[0], ph[1], ph[2], ph[3]);
+#endif
 }
 
 int stride4mod8(int m) {  // >= round_up(m, 4) and == 4 (mod 8): conflict-free DMMA fragments
@@ -570,9 +643,9 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     const int nring = 2 * (mx + my);
     L.faces = static_cast<int>(off);
     int tc = 0;
-    for (int c = std::min(mt, 8); c >= 1; --c) {
-      if (c * nring > 4 * kH3Threads) continue;
-      size_t o = off + static_cast<size_t>(my) * mx + 2 * static_cast<size_t>(c) * nring +
+    static const int tc_max = std::getenv("ASDSM_H3_TC") ? std::atoi(std::getenv("ASDSM_H3_TC")) : 8;
+    for (int c = std::min(mt, tc_max); c >= 1; --c) {
+      size_t o = off + static_cast<size_t>(my) * mx + 3 * static_cast<size_t>(c) * nring + nring +
                  4 * static_cast<size_t>(c) * (A.ax.he + A.ay.he);
       o = (o + 1) & ~static_cast<size_t>(1);
       size_t xs = static_cast<size_t>(c) * L.rp * L.skx + slack;
@@ -584,7 +657,8 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     }
     if (tc == 0) return false;
     L.tc = tc;
-    off += static_cast<size_t>(my) * mx + 2 * static_cast<size_t>(tc) * nring + 4 * static_cast<size_t>(tc) * (A.ax.he + A.ay.he);
+    off += static_cast<size_t>(my) * mx + 3 * static_cast<size_t>(tc) * nring + nring +
+           4 * static_cast<size_t>(tc) * (A.ax.he + A.ay.he);
     off = (off + 1) & ~static_cast<size_t>(1);
     L.x = static_cast<int>(off);
     size_t xs = static_cast<size_t>(tc) * L.rp * L.skx + slack;
