@@ -416,6 +416,39 @@ __global__ void hole_rhs_kernel(double* e, const double* b, FineGeom g, Stencil 
   }
 }
 
+// Same result, one CTA per fine row (j, k): the row's skeleton tests are row-uniform and the
+// x test is one 32-bit remainder per point (the generic kernel above spends ~10 64-bit
+// divisions per point).  Identical arithmetic (apply_row, hole neighbours carry 0).
+template <int DIM>
+__global__ void __launch_bounds__(256) hole_rhs_rows_kernel(double* e, const double* b, FineGeom g, Stencil st, MeshDev m,
+                                                            const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const i64 rows = static_cast<i64>(g.ext[1]) * (DIM == 3 ? g.ext[2] : 1);
+  for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int j = static_cast<int>(row % g.ext[1]);
+    const int k = DIM == 3 ? static_cast<int>(row / g.ext[1]) : 0;
+    const int rj = j % m.n[1], rk = DIM == 3 ? k % m.n[2] : 0;
+    if (rj == m.n[1] - 1 || (DIM == 3 && rk == m.n[2] - 1)) continue;  // skeleton row
+    for (int i = threadIdx.x; i < g.ext[0]; i += blockDim.x) {
+      const int ri = i % m.n[0];
+      if (ri == m.n[0] - 1) continue;  // skeleton point
+      const i64 p = i + row * g.stride[1];
+      // neighbour along `axis` in direction dir is a skeleton point iff (idx + dir + 1) % n == 0
+      auto V = [&](i64 q, int axis, int dir) -> double {
+        if (axis < 0) return 0.0;
+        const int r = axis == 0 ? ri : (axis == 1 ? rj : rk);
+        const int n = m.n[axis];
+        const bool sk = dir < 0 ? r == 0 : r == n - 2;
+        return sk ? e[q] : 0.0;
+      };
+      double vp;
+      const double av = apply_row<DIM>(g, st, p, i, j, k, V, vp);
+      const double bp = b ? b[p] : 0.0;
+      e[p] = sub_rn(bp, av);
+    }
+  }
+}
+
 __global__ void dense_matvec_kernel(const double* A, const double* b, double* x, int n, const DevState* state) {
   if (!state->active) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -769,8 +802,16 @@ void launch_subsample_dots(int dim, const long long* rows, int nrows, const doub
 
 void launch_hole_rhs(int dim, double* e, const double* b, const FineGeom& g, const Stencil& st, const MeshDev& m,
                      DevState* state, cudaStream_t s) {
-  if (dim == 2) hole_rhs_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
-  else hole_rhs_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
+  if (std::getenv("ASDSM_HOLE_RHS_OLD") != nullptr) {  // (read at capture time)
+    if (dim == 2) hole_rhs_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
+    else hole_rhs_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(e, b, g, st, m, state);
+  } else {
+    const i64 rows = static_cast<i64>(g.ext[1]) * (dim == 3 ? g.ext[2] : 1);
+    const unsigned nb = static_cast<unsigned>(std::min<i64>(rows, 32LL * kNumSms));
+    const int bs = g.ext[0] >= 256 ? 256 : 128;
+    if (dim == 2) hole_rhs_rows_kernel<2><<<nb, bs, 0, s>>>(e, b, g, st, m, state);
+    else hole_rhs_rows_kernel<3><<<nb, bs, 0, s>>>(e, b, g, st, m, state);
+  }
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

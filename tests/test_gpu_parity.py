@@ -269,3 +269,15 @@ def test_small_axis_transform_agrees(spec, nf, nc, iters, monkeypatch):
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
     assert np.all(np.abs(a - b) <= 1e-6 * b)
+
+
+@pytest.mark.parametrize("spec,nf,nc", [("cfg:3:0", 129, 4), ("cfg:4:1", 99, 4), ("cfg:2:5", 0, 0), ("ex:4:1", 24, 4)])
+def test_hole_rhs_rows_bitwise(spec, nf, nc, monkeypatch):
+    """The row-per-CTA smooth-mode hole right-hand side (kernels.cu hole_rhs_rows_kernel) is the
+    same arithmetic as the generic kernel: the initial guesses agree bitwise."""
+    ctx, _, _ = _ctx(spec, nf, nc)
+    u_new = ctx.initial_guess()
+    monkeypatch.setenv("ASDSM_HOLE_RHS_OLD", "1")
+    ctx_o, _, _ = _ctx(spec, nf, nc)
+    u_old = ctx_o.initial_guess()
+    assert np.array_equal(u_new, u_old)
