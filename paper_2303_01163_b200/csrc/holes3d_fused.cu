@@ -644,15 +644,24 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     L.faces = static_cast<int>(off);
     int tc = 0;
     static const int tc_max = std::getenv("ASDSM_H3_TC") ? std::atoi(std::getenv("ASDSM_H3_TC")) : 8;
+    // Among the chunk sizes that fit, the one with the least modelled time: per chunk the
+    // step-A rounds (8-row blocks over 16 warps), the step-B rounds ((plane, j tile, n quad)
+    // tasks over 16 warps) and a fixed per-chunk cost (ring transforms, barriers), in the
+    // proportions measured at config 4 (clock64 trace: 4.9 / 6.3 / 9.5 k cycles).
+    const int nty = (A.ay.he + 7) / 8, nq = ((mx + 7) / 8 + 3) / 4;
+    double best = 1e300;
     for (int c = std::min(mt, tc_max); c >= 1; --c) {
       size_t o = off + static_cast<size_t>(my) * mx + 3 * static_cast<size_t>(c) * nring + nring +
                  4 * static_cast<size_t>(c) * (A.ax.he + A.ay.he);
       o = (o + 1) & ~static_cast<size_t>(1);
       size_t xs = static_cast<size_t>(c) * L.rp * L.skx + slack;
       xs = std::max(xs, 2 * static_cast<size_t>(mx) * my + 2 * static_cast<size_t>(std::max(mx, my)) * (A.ax.he + A.ay.he));
-      if (o + xs <= kMax) {
+      if (o + xs > kMax) continue;
+      const int ra = (c * L.rp + 7) / 8, rb = c * nty * nq;
+      const double t = ((mt + c - 1) / c) * (4.9 * ((ra + kH3Warps - 1) / kH3Warps) + 6.3 * ((rb + kH3Warps - 1) / kH3Warps) + 9.5);
+      if (t < best) {
+        best = t;
         tc = c;
-        break;
       }
     }
     if (tc == 0) return false;
