@@ -315,10 +315,10 @@ def main():
     pstream = torch.cuda.ExternalStream(lib.asdsm_plan_stream(ctx._h))
 
     def e2e_step():
-        pb.asdsm._check(lib.asdsm_set_bundle(ctx._h, dp(h_fine), slabs, dp(h_coarse),
-                                             dp(h_exact) if h_exact is not None else None, 0))
-        pb.asdsm._check(lib.asdsm_iterate(ctx._h, ctypes.byref(copt), dp(h_hist), ctypes.byref(nrec),
-                                          ctypes.byref(stop), dp(h_u), dp(h_r)))
+        # asdsm_solve: this step's right-hand sides up, the solve, history + u + r down; one sync
+        pb.asdsm._check(lib.asdsm_solve(ctx._h, dp(h_fine), slabs, dp(h_coarse),
+                                        dp(h_exact) if h_exact is not None else None, ctypes.byref(copt),
+                                        dp(h_hist), ctypes.byref(nrec), ctypes.byref(stop), dp(h_u), dp(h_r)))
 
     for _ in range(2):
         flush_l2(pstream)

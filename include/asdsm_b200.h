@@ -106,6 +106,13 @@ int asdsm_set_bundle(asdsm_plan* plan, const double* b_fine, const double* const
  * (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms), the final iterate u and residual r. */
 int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* history, int* nrec,
                   int* stop_code, double* u_out, double* r_out);
+/* One call from host buffers to host results: asdsm_set_bundle (host memory) + asdsm_iterate, the
+ * uploads, the solve and the downloads ordered on the plan's stream with a single synchronize
+ * (the host buffers are free again when it returns).  The reference's
+ * asdsm_iterate(problem, config, options) on a prebuilt SolverContext (solver.hpp:161-163). */
+int asdsm_solve(asdsm_plan* plan, const double* b_fine, const double* const* b_slab, const double* b_coarse,
+                const double* exact, const asdsm_iterate_options* opts, double* history, int* nrec,
+                int* stop_code, double* u_out, double* r_out);
 /* Same solve fully on `stream` (cudaStream_t as void*, NULL = legacy): no host sync. */
 int asdsm_iterate_async(asdsm_plan* plan, const asdsm_iterate_options* opts, void* stream);
 /* After asdsm_iterate_async: history/outputs to host (synchronizes the stream). */

@@ -257,7 +257,17 @@ class SolverContext {
     return s;
   }
 
-  IterationState iterate(const IterateOptions& o) const {
+  IterationState iterate(const IterateOptions& o) const { return run(o, nullptr); }
+
+  // New right-hand sides and a solve in one call (C-ABI asdsm_solve: uploads, solve and
+  // downloads ordered on the plan's stream, one synchronize).
+  IterationState solve(const RhsBundle& b, const IterateOptions& o) {
+    bundle_ = b;
+    return run(o, &bundle_);
+  }
+
+ private:
+  IterationState run(const IterateOptions& o, const RhsBundle* b) const {
     asdsm_iterate_options c{o.tol, o.max_iter, o.stagnation_window, o.stagnation_ratio, o.subsample, o.rng_seed,
                             o.sparse_residual ? 1 : 0};
     const size_t n = static_cast<size_t>(config_.point_count(MeshKind::fine(config_.dim)));
@@ -266,7 +276,14 @@ class SolverContext {
     st.r.resize(n);
     std::vector<double> hist(7 * static_cast<size_t>(o.max_iter + 1));
     int nrec = 0, stop = 0;
-    check(asdsm_iterate(plan_.get(), &c, hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
+    if (b) {
+      const double* slabs[3] = {nullptr, nullptr, nullptr};
+      for (int a = 0; a < config_.dim; ++a) slabs[a] = b->aniso[static_cast<size_t>(a)].data();
+      check(asdsm_solve(plan_.get(), b->fine.data(), slabs, b->coarse.data(), exact_.empty() ? nullptr : exact_.data(),
+                        &c, hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
+    } else {
+      check(asdsm_iterate(plan_.get(), &c, hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
+    }
     for (int k = 0; k < nrec; ++k) {
       const double* h = hist.data() + 7 * k;
       st.history.push_back({static_cast<int>(h[0]), h[1], h[2], h[3], h[4], h[5], h[6]});

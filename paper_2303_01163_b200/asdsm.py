@@ -132,6 +132,7 @@ def load_library():
         "asdsm_iterate": (I, [P, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_iterate_async": (I, [P, ctypes.POINTER(_Options), P]),
         "asdsm_fetch": (I, [P, P, D, IP, IP, D, D]),
+        "asdsm_solve": (I, [P, D, ctypes.POINTER(D), D, D, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_device_solution": (I, [P, P, ctypes.POINTER(ctypes.c_void_p)]),
         "asdsm_last_launch_count": (ctypes.c_int64, [P]),
         "asdsm_residual": (I, [P, D, D, D]),
@@ -464,6 +465,31 @@ class SolverContext:
         opts = options._c()
         _check(self._lib.asdsm_iterate(self._h, ctypes.byref(opts), _dptr(hist), ctypes.byref(nrec),
                                        ctypes.byref(stop), _dptr(u), _dptr(r)))
+        rows = hist[: nrec.value * 7].reshape(-1, 7)
+        history = [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in rows]
+        return IterationState(u, r, history, _STOP.get(stop.value, "max_iter"))
+
+    def solve(self, bundle, exact=None, options: IterateOptions = IterateOptions(), u_out=None,
+              r_out=None) -> IterationState:
+        """New right-hand sides + asdsm_iterate in one call (C-ABI asdsm_solve: the uploads, the
+        solve and the downloads on the plan's stream, one synchronize).  u_out / r_out: optional
+        float64 host arrays (e.g. pinned) the final iterate and residual are written to."""
+        n = self.fine_size()
+        u = np.empty(n, dtype=np.float64) if u_out is None else u_out
+        r = np.empty(n, dtype=np.float64) if r_out is None else r_out
+        slabs = (ctypes.POINTER(ctypes.c_double) * 3)()
+        keep = [np.ascontiguousarray(x, dtype=np.float64) for x in bundle["aniso"]]
+        for a, x in enumerate(keep):
+            slabs[a] = _dptr(x)
+        fine = np.ascontiguousarray(bundle["fine"], dtype=np.float64)
+        coarse = np.ascontiguousarray(bundle["coarse"], dtype=np.float64)
+        ex = None if exact is None else np.ascontiguousarray(exact, dtype=np.float64)
+        hist = np.empty((max(options.max_iter, 0) + 1) * 7, dtype=np.float64)
+        nrec, stop = ctypes.c_int(), ctypes.c_int()
+        opts = options._c()
+        _check(self._lib.asdsm_solve(self._h, _dptr(fine), slabs, _dptr(coarse), _dptr(ex), ctypes.byref(opts),
+                                     _dptr(hist), ctypes.byref(nrec), ctypes.byref(stop), _dptr(u), _dptr(r)))
+        self.bundle, self.exact = bundle, exact
         rows = hist[: nrec.value * 7].reshape(-1, 7)
         history = [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in rows]
         return IterationState(u, r, history, _STOP.get(stop.value, "max_iter"))

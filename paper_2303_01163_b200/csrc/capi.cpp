@@ -254,14 +254,10 @@ int asdsm_fetch(asdsm_plan* plan, void* stream, double* history, int* nrec, int*
     cudaStream_t s = stream ? as_stream(stream) : plan->stream;
     std::vector<double> rows;
     int stop = 0;
-    const int n = plan->solver->history(rows, stop, s);
+    const int n = plan->solver->fetch(rows, stop, u_out, r_out, s);
     if (history && n > 0) std::memcpy(history, rows.data(), rows.size() * sizeof(double));
     if (nrec) *nrec = n;
     if (stop_code) *stop_code = stop;
-    const size_t bytes = static_cast<size_t>(plan->solver->fine_size()) * sizeof(double);
-    if (u_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_out, plan->solver->u_current(s), bytes, cudaMemcpyDeviceToHost, s));
-    if (r_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(r_out, plan->solver->r_current(s), bytes, cudaMemcpyDeviceToHost, s));
-    ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
   });
 }
 
@@ -270,6 +266,17 @@ int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* h
   const int rc = asdsm_iterate_async(plan, opts, nullptr);
   if (rc != ASDSM_OK) return rc;
   return asdsm_fetch(plan, nullptr, history, nrec, stop_code, u_out, r_out);
+}
+
+int asdsm_solve(asdsm_plan* plan, const double* b_fine, const double* const* b_slab, const double* b_coarse,
+                const double* exact, const asdsm_iterate_options* opts, double* history, int* nrec, int* stop_code,
+                double* u_out, double* r_out) {
+  const int rc = guarded([&] {
+    // stream-ordered uploads: the synchronize at the end of the fetch covers the host buffers
+    plan->solver->set_bundle(b_fine, b_slab, b_coarse, exact, false, plan->stream);
+  });
+  if (rc != ASDSM_OK) return rc;
+  return asdsm_iterate(plan, opts, history, nrec, stop_code, u_out, r_out);
 }
 
 int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev) {

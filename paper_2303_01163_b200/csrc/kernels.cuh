@@ -66,6 +66,10 @@ void launch_divide(double* x, i64 n, const double* divisor, DevState* state, cud
 // Device-side state initialization (capturable in a CUDA graph; no host memcpy).
 void launch_state_init(DevState* state, int active, int have_e, cudaStream_t s);
 void launch_spin(double us, cudaStream_t s);
+// Current iterate into u[0]/r[0] (copy when the selector is 1, then selector = 0): a fetch can
+// enqueue its device-to-host copies without reading the selector on the host first.
+void launch_publish(DevState* state, double* u0, const double* u1, double* r0, const double* r1, i64 n,
+                    cudaStream_t s);
 
 // Final reductions + control (single CTA).
 enum CtrlOp {

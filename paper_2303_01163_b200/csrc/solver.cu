@@ -300,6 +300,8 @@ void Solver::set_bundle(const double* b_fine, const double* const* b_slab, const
 }
 
 Solver::~Solver() {
+  if (host_state_) cudaFreeHost(host_state_);
+  if (host_hist_) cudaFreeHost(host_hist_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   for (cudaStream_t& q : aux_)
     if (q) cudaStreamDestroy(q);
@@ -858,24 +860,41 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   }
 }
 
-int Solver::history(std::vector<double>& rows, int& stop_code, cudaStream_t s) const {
-  DevState h{};
-  ASDSM_CUDA_CHECK(cudaMemcpyAsync(&h, state_, sizeof(h), cudaMemcpyDeviceToHost, s));
+int Solver::history(std::vector<double>& rows, int& stop_code, cudaStream_t s) {
+  return fetch(rows, stop_code, nullptr, nullptr, s);
+}
+
+int Solver::fetch(std::vector<double>& rows, int& stop_code, double* u_out, double* r_out, cudaStream_t s) {
+  if (!host_state_) ASDSM_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_state_), sizeof(DevState), 0));
+  const int cap = std::max(history_cap_, 1);
+  if (cap > host_hist_cap_) {
+    if (host_hist_) cudaFreeHost(host_hist_);
+    host_hist_ = nullptr;
+    ASDSM_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_hist_), static_cast<size_t>(cap) * 7 * sizeof(double), 0));
+    host_hist_cap_ = cap;
+  }
+  const size_t nb = static_cast<size_t>(g_fine_.size) * sizeof(double);
+  if (u_out || r_out) launch_publish(state_, u_[0], u_[1], r_[0], r_[1], g_fine_.size, s);
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(host_state_, state_, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  if (history_)
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(host_hist_, history_, static_cast<size_t>(history_cap_) * 7 * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+  if (u_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_out, u_[0], nb, cudaMemcpyDefault, s));
+  if (r_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(r_out, r_[0], nb, cudaMemcpyDefault, s));
   ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
-  rows.assign(static_cast<size_t>(h.nrec) * 7, 0.0);
-  if (h.nrec > 0)
-    ASDSM_CUDA_CHECK(cudaMemcpyAsync(rows.data(), history_, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  const DevState& h = *host_state_;
+  const int nrec = history_ ? std::min(h.nrec, history_cap_) : 0;
+  rows.assign(host_hist_, host_hist_ + static_cast<size_t>(nrec) * 7);
   // wall_ms: time since the previous record (row 0: since the solve started), as the
   // reference's record() does (solver.cpp:586-610), from the device %globaltimer
   double prev = h.t0_ns;
-  for (int k = 0; k < h.nrec; ++k) {
+  for (int k = 0; k < nrec; ++k) {
     const double t = rows[static_cast<size_t>(k) * 7 + 6];
     rows[static_cast<size_t>(k) * 7 + 6] = (t - prev) / 1e6;
     prev = t;
   }
   stop_code = h.stop == 0 ? 3 : h.stop;
-  return h.nrec;
+  return nrec;
 }
 
 const double* Solver::u_current(cudaStream_t s) const {

@@ -55,7 +55,10 @@ class Solver {
   void run(const RunOptions& o, cudaStream_t s);
 
   // After run(): history rows (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms).
-  int history(std::vector<double>& rows, int& stop_code, cudaStream_t s) const;
+  int history(std::vector<double>& rows, int& stop_code, cudaStream_t s);
+  // After run(): history rows, and the final iterate / residual to u_out / r_out (host or
+  // device memory, nullable), enqueued together on `s` with a single synchronize.
+  int fetch(std::vector<double>& rows, int& stop_code, double* u_out, double* r_out, cudaStream_t s);
   const double* u_current(cudaStream_t s) const;  // synchronizes to read the selector
   const double* r_current(cudaStream_t s) const;
   double* u_buffer(int i) { return u_[i]; }
@@ -156,6 +159,9 @@ class Solver {
   DevState* state_ = nullptr;
   double* history_ = nullptr;
   int history_cap_ = 0;
+  DevState* host_state_ = nullptr;  // pinned staging of the state and history for fetch()
+  double* host_hist_ = nullptr;
+  int host_hist_cap_ = 0;
   int* coins_ = nullptr;
   int coins_cap_ = 0;
   RunOptions last_opts_{};

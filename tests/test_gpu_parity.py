@@ -281,3 +281,22 @@ def test_hole_rhs_rows_bitwise(spec, nf, nc, monkeypatch):
     ctx_o, _, _ = _ctx(spec, nf, nc)
     u_old = ctx_o.initial_guess()
     assert np.array_equal(u_new, u_old)
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:1:0", 0, 0, 6), ("cfg:0:0", 0, 0, 10), ("cfg:3:0", 29, 4, 4)])
+def test_one_call_solve(spec, nf, nc, iters):
+    """asdsm_solve (uploads + solve + one-sync fetch) against set_bundle + asdsm_iterate: bitwise.
+    With b scaled by 2 every stage is exactly homogeneous (zero initial guess, scale-free step and
+    normalizations, value-independent cross-point draws), so u and r double bit for bit."""
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=3)
+    st0 = ctx.iterate(opts)
+    bun = {k: ([2.0 * x for x in v] if k == "aniso" else 2.0 * v) for k, v in ctx.bundle.items()}
+    base = ctx.bundle
+    st2 = ctx.solve(bun, None, opts)
+    assert np.array_equal(st2.u, 2.0 * st0.u) and np.array_equal(st2.r, 2.0 * st0.r)
+    assert [h.s_hat for h in st2.history] == [h.s_hat for h in st0.history]
+    st1 = ctx.solve(base, None, opts)
+    assert np.array_equal(st1.u, st0.u) and np.array_equal(st1.r, st0.r)
+    assert [h.res_l2 for h in st1.history] == [h.res_l2 for h in st0.history]
+    assert st1.stop_reason == st0.stop_reason
