@@ -287,7 +287,9 @@ def main():
                 "frac": ach / hbm, "traffic": ncu_traffic(cid, c["name"]), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
     cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
-    upd = next((c for c in comps if c["name"] == "update_residual"), cand[0])
+    # the fine-grid update pass as the step runs it: fused with the step dots where it applies
+    upd = next((c for c in comps if c["name"] == "dots_update"),
+               next((c for c in comps if c["name"] == "update_residual"), cand[0]))
     roof = roof_of(upd)
     roof["share_of_step"] = upd["ms_per_launch"] * upd["launches_per_solve"] / ms
     dom = max(cand, key=lambda c: c["ms_per_launch"] * c["launches_per_solve"])

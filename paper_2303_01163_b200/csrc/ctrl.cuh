@@ -246,10 +246,12 @@ __device__ inline void block_reduce4_march(double s0, double m1, double s2, doub
 // Last-block fold: after every block has written its partials, the last block to finish
 // reduces them in a fixed order and applies the control op -- no separate ctrl launch.
 
-__device__ inline bool fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history) {
+__device__ inline bool fold_ctrl(const CtrlArgs& c, double* partials, DevState* S, double* history,
+                                 unsigned nblocks_part = 0) {
   if (c.op < 0) return false;
   __shared__ int last;
-  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  // nblocks_part: only blocks [0, nblocks_part) take part (the rest do not call this)
+  const unsigned nblocks = nblocks_part ? nblocks_part : gridDim.x * gridDim.y * gridDim.z;
   __syncthreads();
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     __threadfence();

@@ -30,7 +30,7 @@ struct DevState {
   double num_sub, den_sub;       // subsampled <r,Ae>, <Ae,Ae> (subsample > 0)
   double s_full;                 // all-rows step, for the residual-growth retry
   int retry;                     // subsampled step grew the residual: second update pending
-  int pad2_;
+  unsigned gen;                  // grid-barrier generation (fused dots + update pass)
 };
 
 struct FineGeom {

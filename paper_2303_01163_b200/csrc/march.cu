@@ -161,19 +161,20 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
 // per-row barrier: every load of a thread is independent, so the pass is one deep wave of
 // loads -- the right shape when the arrays sit in L2 (config 1) and at HBM scale alike.
 template <int MODE, bool VAR, int YC>
-__global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
-  pdl_launch_dependents();
-  pdl_wait();
+__device__ __forceinline__ void yc_body(const MarchArgs& A) {
   DevState* S = A.state;
-  if (!S->active) return;
-  const int cur = S->cur;
+  // state read through volatile: in the fused dots + update kernel it was written by another
+  // CTA of the same launch (after the grid barrier)
+  const volatile DevState* VS = S;
+  if (!VS->active) return;
+  const int cur = VS->cur;
   double s = 0.0;
   bool work = true;
   if (MODE == kMarchUpdate) {
-    s = S->s;
-    work = s != 0.0 && (!A.retry_pass || S->retry);
+    s = VS->s;
+    work = s != 0.0 && (!A.retry_pass || VS->retry);
   }
-  if (MODE == kMarchDots) work = S->have_e != 0;
+  if (MODE == kMarchDots) work = VS->have_e != 0;
   const int Nx = A.g.ext[0], Ny = A.g.ext[1];
   const i64 sy = A.g.stride[1];
   const Stencil& st = A.st;
@@ -247,13 +248,18 @@ __global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
-// DOTS restricted to the skeleton rows of a 2D mesh (rows at the y-stations, columns at the
-// x-stations, each point once): same per-point arithmetic as the full pass.
+template <int MODE, bool VAR, int YC>
+__global__ void __launch_bounds__(256) stencil2d_yc_kernel(MarchArgs A) {
+  pdl_launch_dependents();
+  pdl_wait();
+  yc_body<MODE, VAR, YC>(A);
+}
+
+// A e on the skeleton rows of a 2D mesh (rows at the y-stations, columns at the x-stations,
+// each point once), accumulated into <r, Ae> (a0) and <Ae, Ae> (a2) over a grid-stride loop
 template <bool VAR>
-__global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
-  DevState* S = A.state;
-  if (!S->active) return;
-  const bool work = S->have_e != 0;
+__device__ __forceinline__ void skel2d_dots_points(const MarchArgs& A, const DevState* S, bool work, double& a0,
+                                                   double& a2, unsigned nblk) {
   const int Nx = A.g.ext[0], Ny = A.g.ext[1];
   const i64 sy = A.g.stride[1];
   const Stencil& st = A.st;
@@ -261,9 +267,8 @@ __global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
   const double* __restrict__ rcur = S->cur ? A.r1 : A.r0;
   const int nc0 = A.nc[0], nc1 = A.nc[1], n0 = A.n[0], n1 = A.n[1];
   const i64 nrow = static_cast<i64>(nc1) * Nx, ncol = static_cast<i64>(nc0) * Ny;
-  double a0 = 0.0, a2 = 0.0;
   for (i64 t = work ? static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x : nrow + ncol; t < nrow + ncol;
-       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+       t += static_cast<i64>(nblk) * blockDim.x) {
     int x, y;
     if (t < nrow) {
       const int J = static_cast<int>(t / Nx);
@@ -288,6 +293,57 @@ __global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
     a0 += __ldg(rcur + p) * acc;
     a2 += acc * acc;
   }
+}
+
+// Skeleton-row step dots and the update in one launch.  Phase 1 is skel2d_dots_kernel's work;
+// its last block applies the step control and bumps DevState::gen; every CTA waits for the bump
+// (the grid is co-resident: cooperative launch, occupancy checked on the host; the wait is
+// bounded and traps rather than hang), then runs the update pass with the new step.  One
+// launch, one grid barrier, instead of two kernels with a launch boundary between them.
+template <int YC>
+__global__ void __launch_bounds__(256, 4) dots_update2d_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  unsigned gen0;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen0) : "l"(&S->gen) : "memory");
+  // phase 1 on the first blocks only (one skeleton point per thread): fewer arrivals and
+  // partials for the last block to fold; the other blocks go straight to the barrier
+  const i64 npts = static_cast<i64>(A.nc[1]) * A.g.ext[0] + static_cast<i64>(A.nc[0]) * A.g.ext[1];
+  const unsigned nd = static_cast<unsigned>(((npts + blockDim.x - 1) / blockDim.x < static_cast<i64>(gridDim.x) ? (npts + blockDim.x - 1) / blockDim.x : static_cast<i64>(gridDim.x)));
+  bool released = false;
+  if (blockIdx.x < nd) {
+    double a0 = 0.0, a2 = 0.0;
+    skel2d_dots_points<false>(A, S, S->have_e != 0, a0, a2, nd);
+    block_reduce4_march(a0, 0.0, a2, 0.0, A.partials);
+    if (fold_ctrl(A.dots_ctrl, A.partials, S, A.history, nd)) {
+      released = true;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&S->gen) : "memory");
+      }
+    }
+  }
+  if (!released && threadIdx.x == 0) {
+    unsigned g, n = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&S->gen) : "memory");
+      if (g != gen0) break;
+      __nanosleep(128);
+      if (++n > (1u << 24)) __trap();  // a grid that is not co-resident: fail, do not hang
+    } while (true);
+  }
+  __syncthreads();
+  yc_body<kMarchUpdate, false, YC>(A);
+}
+
+// DOTS restricted to the skeleton rows of a 2D mesh (rows at the y-stations, columns at the
+// x-stations, each point once): same per-point arithmetic as the full pass.
+template <bool VAR>
+__global__ void __launch_bounds__(128) skel2d_dots_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  double a0 = 0.0, a2 = 0.0;
+  skel2d_dots_points<VAR>(A, S, S->have_e != 0, a0, a2, gridDim.x);
   block_reduce4_march(a0, 0.0, a2, 0.0, A.partials);
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
@@ -483,6 +539,24 @@ unsigned march_blocks(const FineGeom& g) {
   return static_cast<unsigned>(((g.ext[0] + TX3 - 1) / TX3) * ((g.ext[1] + TY3 - 1) / TY3) * ((g.ext[2] + sz - 1) / sz));
 }
 
+static unsigned dots_update_blocks(const FineGeom& g) {
+  constexpr int kYc = 8;
+  const long long tiles = static_cast<long long>((g.ext[0] + 31) / 32) * ((g.ext[1] + 8 * kYc - 1) / (8 * kYc));
+  return static_cast<unsigned>(std::min<long long>(tiles, 4LL * kNumSms));
+}
+
+bool dots_update_supported(const FineGeom& g) {
+  static int resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    ASDSM_CUDA_CHECK(cudaGetDevice(&dev));
+    ASDSM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    ASDSM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dots_update2d_kernel<8>, 256, 0));
+    resident = sms * per_sm;
+  }
+  return g.dim == 2 && static_cast<long long>(dots_update_blocks(g)) <= resident;
+}
+
 void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   MarchArgs A = A0;
   A.strip = march_strip(A.g);
@@ -501,7 +575,20 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else KERNEL<kMarchDots, false><<<GRID, BLOCK, 0, s>>>(A);                        \
     }                                                                                   \
   } while (0)
-  if (A.g.dim == 3 && mode == kMarchDots && A.skel_only) {
+  if (mode == kMarchDotsUpdate) {
+    if (A.g.dim != 2 || var || !A.skel_only) throw AsdsmError(kUnsupported, "fused dots + update: 2D constant coefficients");
+    constexpr int kYc = 8;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(dots_update_blocks(A.g));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ASDSM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, dots_update2d_kernel<kYc>, A));
+  } else if (A.g.dim == 3 && mode == kMarchDots && A.skel_only) {
     if (var) skel3d_dots_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
     else skel3d_dots_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
   } else if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {

@@ -5,7 +5,9 @@ namespace asdsm_b200 {
 
 // kMarchCand: the residual of the update's candidate iterate (already written to the
 // non-current buffer by an axpy pass) -- the 3D update runs as axpy + kMarchCand
-enum { kMarchResidual = 0, kMarchUpdate = 1, kMarchDots = 2, kMarchCand = 3 };
+// kMarchDotsUpdate (2D, constant coefficients): the skeleton-row step dots and the update in one
+// launch -- dots, last-block step control, a grid barrier on DevState::gen, then the update
+enum { kMarchResidual = 0, kMarchUpdate = 1, kMarchDots = 2, kMarchCand = 3, kMarchDotsUpdate = 4 };
 
 struct MarchArgs {
   const double* u0;  // current iterate buffers (state->cur selects); DOTS: unused
@@ -40,7 +42,12 @@ struct MarchArgs {
   // (rounding level) -- the reference's subsampled path samples skeleton rows for that reason
   // (solver.cpp:463-465); here the full sum drops those rounding-level terms as well
   int skel_only;
+  CtrlArgs dots_ctrl;  // kMarchDotsUpdate: the step control (kCtrlStep) between the two phases
 };
+
+// kMarchDotsUpdate needs every CTA of its grid resident at once (it waits on a grid barrier):
+// true when this device's occupancy allows it (checked once)
+bool dots_update_supported(const FineGeom& g);
 
 int march_strip(const FineGeom& g);
 unsigned march_blocks(const FineGeom& g);

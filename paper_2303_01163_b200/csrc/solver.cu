@@ -263,6 +263,8 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     }
   }
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
+  dots_update_ok_ = !variable_ && mesh_.dim == 2 && std::getenv("ASDSM_DOTS_UPDATE") != nullptr &&
+                    dots_update_supported(fg_);
 }
 
 BoxArray Solver::hole_array(double* p) const {
@@ -835,23 +837,38 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   march_launch(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], ex, fg_, st_fine_,
                                           partials_, state_, c, history_), s);
 
+  // the step's dot products: their own pass, or (opt-in, ASDSM_DOTS_UPDATE=1) inside the update
+  // launch with a grid barrier between the two phases -- measured slower in the captured graph
+  // (config 1: 1.18-1.21 -> 1.23-1.26 ms per solve on the same box), kept for the record
+  const bool dots_in_update = dots_update_ok_ && sub_m_ == 0 && skel_dots_ && !variable_;
   for (int k = 1; k <= o.max_iter; ++k) {
+    CtrlArgs cstep = c;
+    cstep.op = kCtrlStep;
+    cstep.k = k;
     error_mode_guess(r_[0], r_[1], k, e_, s);
     if (sub_m_ > 0)
       launch_subsample_dots(mesh_.dim, sub_rows_ + static_cast<i64>(sub_m_) * k, sub_m_, e_, r_[0], r_[1], fg_,
                             st_fine_, partials_, state_, history_, s, coef_fine_);
     c.op = kCtrlStep;
     c.k = k;
-    MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_, st_fine_,
-                                partials_, state_, c, history_);
-    dots.skel_only = skel_dots_ ? 1 : 0;
-    march_launch(kMarchDots, dots, s);
+    if (!dots_in_update) {
+      MarchArgs dots = march_args(nullptr, nullptr, e_, nullptr, nullptr, nullptr, r_[0], r_[1], nullptr, fg_,
+                                  st_fine_, partials_, state_, c, history_);
+      dots.skel_only = skel_dots_ ? 1 : 0;
+      march_launch(kMarchDots, dots, s);
+    }
     c.op = kCtrlAccept;
     MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], ex, fg_, st_fine_, partials_, state_,
                               c, history_);
     set_factors(up, mesh_);
     up.sparse = o.sparse_residual ? 1 : 0;
-    march_launch(kMarchUpdate, up, s);
+    if (dots_in_update) {
+      up.skel_only = 1;
+      up.dots_ctrl = cstep;
+      march_launch(kMarchDotsUpdate, up, s);
+    } else {
+      march_launch(kMarchUpdate, up, s);
+    }
     if (sub_m_ > 0) {  // all-rows retry when the subsampled step grew the residual
       up.ctrl.op = kCtrlAccept2;
       up.retry_pass = 1;
@@ -979,6 +996,8 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   const i64 N = g_fine_.size;
   const i64 NH = mesh_.hole_count();
   const int iters = std::max(last_opts_.max_iter, 1);
+  // the step dots run inside the fused hole kernel on this plan (enqueue_run's condition)
+  const bool dots_in_update = dots_update_ok_ && sub_m_ == 0 && skel_dots_ && !variable_;
   auto timed = [&](const char* name, double bytes, double flops, int per_solve, auto&& body) {
     launch_state_init(state_, 1, 1, s);
     body();  // warm
@@ -1028,7 +1047,36 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
   });
   out[0].ms -= out[1].ms;
   out.pop_back();
-  {
+  if (dots_in_update) {
+    // the launch the step actually runs: skeleton dots, step control, grid barrier, update.
+    // The standalone update pass above stays listed (per_solve 0) as the unfused reference.
+    out[0].per_solve = 0;
+    out[0].name = "update_residual_standalone";
+    i64 nskel = 0;
+    for (int a = 0; a < mesh_.dim; ++a) {
+      i64 plane = mesh_.nc[a];
+      for (int b = 0; b < mesh_.dim; ++b)
+        if (b != a) plane *= mesh_.nf[b];
+      nskel += plane;
+    }
+    timed("dots_update", 8.0 * N * (5.0 + ex) + 16.0 * nskel, 0.0, iters, [&] {
+      launch_state_init(state_, 1, 1, s);
+      CtrlArgs c{};
+      c.op = -1;
+      CtrlArgs cstep{};
+      cstep.op = kCtrlStep;
+      MarchArgs up = march_args(u_[0], u_[1], e_, b_, u_[0], u_[1], r_[0], r_[1], has_exact_ ? exact_ : nullptr, fg_,
+                                st_fine_, partials_, state_, c, history_);
+      set_factors(up, mesh_);
+      up.skel_only = 1;
+      up.dots_ctrl = cstep;
+      march_launch(kMarchDotsUpdate, up, s);
+    });
+    timed("state_init", 0.0, 0.0, 0, [&] { launch_state_init(state_, 1, 1, s); });
+    out[out.size() - 2].ms -= out.back().ms;
+    out.pop_back();
+  }
+  if (!dots_in_update) {
     // skeleton-row dots move 2 doubles per skeleton point (+ the stencil's e neighbours, cached)
     i64 nskel_pts = N;
     if (skel_dots_) {

@@ -286,8 +286,9 @@ def test_hole_rhs_rows_bitwise(spec, nf, nc, monkeypatch):
 @pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:1:0", 0, 0, 6), ("cfg:0:0", 0, 0, 10), ("cfg:3:0", 29, 4, 4)])
 def test_one_call_solve(spec, nf, nc, iters):
     """asdsm_solve (uploads + solve + one-sync fetch) against set_bundle + asdsm_iterate: bitwise.
-    With b scaled by 2 every stage is exactly homogeneous (zero initial guess, scale-free step and
-    normalizations, value-independent cross-point draws), so u and r double bit for bit."""
+    With b scaled by 2 every stage is exactly homogeneous (zero initial guess, power-of-two
+    scaling through the normalizations, value-independent cross-point draws), so u, r and the
+    step s_hat double bit for bit."""
     ctx, mesh, _ = _ctx(spec, nf, nc)
     opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=3)
     st0 = ctx.iterate(opts)
@@ -295,8 +296,28 @@ def test_one_call_solve(spec, nf, nc, iters):
     base = ctx.bundle
     st2 = ctx.solve(bun, None, opts)
     assert np.array_equal(st2.u, 2.0 * st0.u) and np.array_equal(st2.r, 2.0 * st0.r)
-    assert [h.s_hat for h in st2.history] == [h.s_hat for h in st0.history]
+    # s_hat scales with b too: the error-mode correction is normalized
+    assert np.array_equal([h.s_hat for h in st2.history], [2.0 * h.s_hat for h in st0.history], equal_nan=True)
     st1 = ctx.solve(base, None, opts)
     assert np.array_equal(st1.u, st0.u) and np.array_equal(st1.r, st0.r)
     assert [h.res_l2 for h in st1.history] == [h.res_l2 for h in st0.history]
     assert st1.stop_reason == st0.stop_reason
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:1:0", 0, 0, 20), ("ex:3:1", 199, 9, 12)])
+def test_dots_update_launch_agrees(spec, nf, nc, iters, monkeypatch):
+    """The opt-in single launch of the step dots and the update (ASDSM_DOTS_UPDATE=1: grid
+    barrier on DevState::gen, cooperative launch) against the two-launch default: the dot
+    products are summed over a different block split, so the step differs in the last bits."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=5)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_two = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_DOTS_UPDATE", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_one = ctx1.iterate(opts)
+    a = np.array([h.res_l2 for h in st_one.history])
+    b = np.array([h.res_l2 for h in st_two.history])
+    k = np.arange(len(b))
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
+    assert np.max(np.abs(st_one.u - st_two.u)) <= 1e-8 * np.max(np.abs(st_two.u))
