@@ -322,11 +322,11 @@ def main():
                                         dp(h_exact) if h_exact is not None else None, ctypes.byref(copt),
                                         dp(h_hist), ctypes.byref(nrec), ctypes.byref(stop), dp(h_u), dp(h_r)))
 
-    for _ in range(2):
+    for _ in range(max(args.warmup, 3)):
         flush_l2(pstream)
         e2e_step()
     etimes = []
-    for _ in range(args.steps):
+    for _ in range(max(args.steps, 10)):
         flush_l2(pstream)
         a = torch.cuda.Event(enable_timing=True)
         bb = torch.cuda.Event(enable_timing=True)
@@ -339,7 +339,8 @@ def main():
     h2d = 8 * (b["fine"].size + sum(x.size for x in b["aniso"]) + b["coarse"].size + (ndof if h_exact is not None else 0))
     d2h = 8 * (2 * ndof + (iters + 1) * 7)
     e2e = {"value": world * ndof * iters / (ems / 1e3), "unit": "DOF-iter/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": ems, "steps": len(etimes),
+           "ms_all": [round(t, 4) for t in etimes]}
     assert np.allclose(h_u.numpy(), h_u.numpy())  # touch the result
 
     # ---- CPU baseline: the compiled reference on this box's host cores (rank 0, N=1)

@@ -407,6 +407,74 @@ __global__ void __launch_bounds__(256) skel3d_dots_kernel(MarchArgs A) {
   fold_ctrl(A.ctrl, A.partials, S, A.history);
 }
 
+// Same sums over the same points, one warp per skeleton row: x-plane rows (I, z) run along y,
+// y-plane rows (J, z) and z-plane rows (K, y) along x, so there is no 64-bit division per point
+// (the kernel above spends ~6) and each lane has four points' loads in flight at once.
+template <bool VAR>
+__global__ void __launch_bounds__(256) skel3d_dots_rows_kernel(MarchArgs A) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const bool work = S->have_e != 0;
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
+  const i64 sy = A.g.stride[1], sz = A.g.stride[2];
+  const Stencil& st = A.st;
+  const double* __restrict__ ee = A.e;
+  const double* __restrict__ rcur = S->cur ? A.r1 : A.r0;
+  const int n0 = A.n[0], n1 = A.n[1], n2 = A.n[2];
+  const int rx = A.nc[0] * Nz, ry = A.nc[1] * Nz, rz = A.nc[2] * Ny;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  double a0 = 0.0, a2 = 0.0;
+  for (int row = work ? gw : rx + ry + rz; row < rx + ry + rz; row += nw) {
+    int fam, x = 0, y = 0, z = 0, len;
+    if (row < rx) {  // (I, z): y varies
+      fam = 0;
+      z = row % Nz;
+      x = (row / Nz + 1) * n0 - 1;
+      len = Ny;
+    } else if (row < rx + ry) {  // (J, z): x varies
+      fam = 1;
+      const int q = row - rx;
+      z = q % Nz;
+      y = (q / Nz + 1) * n1 - 1;
+      len = Nx;
+    } else {  // (K, y): x varies; rows on a y-station belong to the y-planes
+      fam = 2;
+      const int q = row - rx - ry;
+      y = q % Ny;
+      z = (q / Ny + 1) * n2 - 1;
+      if ((y + 1) % n1 == 0) continue;
+      len = Nx;
+    }
+    const i64 base = fam == 0 ? x + z * sz : y * sy + z * sz;
+    const i64 step = fam == 0 ? sy : 1;
+    for (int v0 = lane; v0 < len; v0 += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + 32 * u;
+        if (v >= len) break;
+        const int px = fam == 0 ? x : v, py = fam == 0 ? v : y;
+        if (fam != 0 && (px + 1) % n0 == 0) continue;  // x-station points: counted with the x-planes
+        const i64 p = base + v * step;
+        const i64 N = A.g.size;
+        auto C = [&](int slot, double cst) { return VAR ? __ldg(A.coef + slot * N + p) : cst; };
+        double acc = 0.0;
+        if (z > 0) acc = __dadd_rn(acc, __dmul_rn(C(0, st.left[2]), __ldg(ee + p - sz)));
+        if (py > 0) acc = __dadd_rn(acc, __dmul_rn(C(1, st.left[1]), __ldg(ee + p - sy)));
+        if (px > 0) acc = __dadd_rn(acc, __dmul_rn(C(2, st.left[0]), __ldg(ee + p - 1)));
+        acc = __dadd_rn(acc, __dmul_rn(C(3, st.diag), __ldg(ee + p)));
+        if (px < Nx - 1 && st.has_right[0]) acc = __dadd_rn(acc, __dmul_rn(C(4, st.right[0]), __ldg(ee + p + 1)));
+        if (py < Ny - 1 && st.has_right[1]) acc = __dadd_rn(acc, __dmul_rn(C(5, st.right[1]), __ldg(ee + p + sy)));
+        if (z < Nz - 1 && st.has_right[2]) acc = __dadd_rn(acc, __dmul_rn(C(6, st.right[2]), __ldg(ee + p + sz)));
+        a0 += __ldg(rcur + p) * acc;
+        a2 += acc * acc;
+      }
+    }
+  }
+  block_reduce4_march(a0, 0.0, a2, 0.0, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
 // Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
@@ -589,8 +657,14 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     cfg.numAttrs = 1;
     ASDSM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, dots_update2d_kernel<kYc>, A));
   } else if (A.g.dim == 3 && mode == kMarchDots && A.skel_only) {
-    if (var) skel3d_dots_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
-    else skel3d_dots_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
+    static const bool by_point = std::getenv("ASDSM_SKEL3D_POINTS") != nullptr;
+    if (by_point) {
+      if (var) skel3d_dots_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
+      else skel3d_dots_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
+    } else {
+      if (var) skel3d_dots_rows_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
+      else skel3d_dots_rows_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
+    }
   } else if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {
     if (var) skel2d_dots_kernel<true><<<kNumSms, 128, 0, s>>>(A);
     else skel2d_dots_kernel<false><<<kNumSms, 128, 0, s>>>(A);

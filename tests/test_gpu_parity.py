@@ -321,3 +321,19 @@ def test_dots_update_launch_agrees(spec, nf, nc, iters, monkeypatch):
     assert len(a) == len(b)
     assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
     assert np.max(np.abs(st_one.u - st_two.u)) <= 1e-8 * np.max(np.abs(st_two.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:4:1", 24, 4, 6)])
+def test_skel3d_dots_rows_agree(spec, nf, nc, iters, monkeypatch):
+    """3D skeleton-plane step dots, one warp per skeleton row (default) against one thread per
+    point (ASDSM_SKEL3D_POINTS=1): same points and per-point arithmetic, another summation order."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=2)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_rows = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_SKEL3D_POINTS", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_pts = ctx1.iterate(opts)
+    a = np.array([h.s_hat for h in st_rows.history[1:]])
+    b = np.array([h.s_hat for h in st_pts.history[1:]])
+    assert np.all(np.abs(a - b) <= 1e-12 * np.abs(b) + 1e-300)
+    assert np.max(np.abs(st_rows.u - st_pts.u)) <= 1e-10 * np.max(np.abs(st_pts.u))
