@@ -42,6 +42,7 @@ struct MarchArgs {
   // (rounding level) -- the reference's subsampled path samples skeleton rows for that reason
   // (solver.cpp:463-465); here the full sum drops those rounding-level terms as well
   int skel_only;
+  int prefetch;        // 2D persistent pass: L2-prefetch the tile this many rounds ahead (0: off)
   CtrlArgs dots_ctrl;  // kMarchDotsUpdate: the step control (kCtrlStep) between the two phases
 };
 
