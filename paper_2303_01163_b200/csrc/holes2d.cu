@@ -9,6 +9,7 @@
 // (hole, block of modes) builds the ring rhs from the skeleton, forms fhat on the fly and
 // runs both Thomas sweeps in shared memory; the dense back transform is the DMMA GEMM.
 #include "holes2d.cuh"
+#include "partsolve.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -142,6 +143,83 @@ __global__ void hole2d_fwd_thomas_kernel(const double* __restrict__ e, double* _
     x = yp[static_cast<i64>(j) * ys_stride] - __ldg(cq + static_cast<i64>(j) * m0) * x;
     out[static_cast<i64>(j) * m0] = x;
   }
+}
+
+// Ring of one hole: fL, fR (columns 0 / m0-1), fB, fT (rows 0 / m1-1), ring_rhs's arithmetic
+__global__ void __launch_bounds__(256) hole2d_ring_kernel(const double* __restrict__ e, Hole2DArgs A,
+                                                          Hole2DPartArgs P, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const int m0 = A.m0, m1 = A.m1;
+  const int hole = blockIdx.x;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  const int ox = hx * A.n0, oy = hy * A.n1;
+  double* ring = P.ring + static_cast<i64>(hole) * (2 * m1 + 2 * m0);
+  for (int t = threadIdx.x; t < 2 * m1 + 2 * m0; t += blockDim.x) {
+    double v;
+    if (t < m1) v = ring_rhs(e, A, ox, oy, 0, t);
+    else if (t < 2 * m1) v = ring_rhs(e, A, ox, oy, m0 - 1, t - m1);
+    else if (t < 2 * m1 + m0) v = ring_rhs(e, A, ox, oy, t - 2 * m1, 0);
+    else v = ring_rhs(e, A, ox, oy, t - 2 * m1 - m0, m1 - 1);
+    ring[t] = v;
+  }
+}
+
+#ifndef ASDSM_PART_HOLE_WARPS
+#define ASDSM_PART_HOLE_WARPS 8
+#endif
+constexpr int kPartHoleWarps = ASDSM_PART_HOLE_WARPS;  // mode lines (warps) per CTA
+
+// One warp per (hole, mode k): line rhs fb, w0 fL + wm fR (interior rows), ft; partition solve;
+// the line to modes[hole][k][.] (coalesced).
+template <int SEG>
+__global__ void __launch_bounds__(32 * kPartHoleWarps) hole2d_part_kernel(double* __restrict__ modes, Hole2DArgs A,
+                                                                          Hole2DPartArgs P, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  extern __shared__ __align__(16) double sm[];
+  const int m0 = A.m0, m1 = A.m1;
+  const int lp = (m1 + 1) & ~1;  // line buffer stride
+  double* fL = sm;
+  double* fR = fL + m1;
+  double* fB = fR + m1;
+  double* fT = fB + m0;
+  double* lines = fT + m0 + ((2 * m1 + 2 * m0) & 1);  // [warps][lp]
+  double* tabs = lines + kPartHoleWarps * lp;         // [warps][pstride]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hole = blockIdx.x;
+  const int k0 = blockIdx.y * kPartHoleWarps;
+  const double* ring = P.ring + static_cast<i64>(hole) * (2 * m1 + 2 * m0);
+  for (int t = threadIdx.x; t < 2 * m1 + 2 * m0; t += blockDim.x) cp_async8(fL + t, ring + t);
+  for (int t = threadIdx.x; t < kPartHoleWarps * P.pstride; t += blockDim.x) {
+    const int w = t / P.pstride, o = t - w * P.pstride;
+    if (k0 + w < m0) cp_async8(tabs + t, P.part + static_cast<i64>(k0 + w) * P.pstride + o);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  const int k = k0 + warp;
+  const double* Wk = P.W + static_cast<i64>(min(k, m0 - 1)) * m0;  // row k: coalesced
+  const double w0 = __ldg(Wk), wm = __ldg(Wk + m0 - 1);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  if (k >= m0) return;
+  // the two full row transforms of mode k: lanes over i, then a shuffle tree
+  double fb = 0.0, ft = 0.0;
+  for (int i = lane; i < m0; i += 32) {
+    const double w = __ldg(Wk + i);
+    fb = fma(w, fB[i], fb);
+    ft = fma(w, fT[i], ft);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    ft += __shfl_xor_sync(0xffffffffu, ft, o);
+  }
+  double* line = lines + warp * lp;
+  for (int j = lane; j < m1; j += 32)
+    line[j] = j == 0 ? fb : (j == m1 - 1 ? ft : fma(wm, fR[j], w0 * fL[j]));
+  __syncwarp();
+  part_solve_line<SEG>(line, tabs + warp * P.pstride, m1, P.P, P.last, A.line_left, A.line_right);
+  __syncwarp();
+  double* out = modes + static_cast<i64>(hole) * m0 * m1 + static_cast<i64>(k) * m1;
+  for (int j = lane; j < m1; j += 32) out[j] = line[j];
 }
 
 // Same algorithm with every table slice this CTA needs (Wt[:, kblock], ipiv/cp[:, kblock])
@@ -891,6 +969,32 @@ void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevSta
   ++g_kernel_launches;
 }
 
+bool hole2d_part_supported(int seg) { return seg == 4 || seg == 8 || seg == 12 || seg == 16; }
+
+void launch_hole2d_ring(const double* e, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state,
+                        cudaStream_t s) {
+  hole2d_ring_kernel<<<static_cast<unsigned>(A.nbox0 * A.nbox1), 256, 0, s>>>(e, A, P, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+void launch_hole2d_part(double* modes, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state, cudaStream_t s) {
+  const int lp = (A.m1 + 1) & ~1;
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(A.m1 + A.m0) + 1 + kPartHoleWarps * static_cast<size_t>(lp) +
+                                        kPartHoleWarps * static_cast<size_t>(P.pstride));
+  if (smem > 100 * 1024) throw AsdsmError(kUnsupported, "partitioned hole solve exceeds shared memory");
+  const dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m0 + kPartHoleWarps - 1) / kPartHoleWarps));
+  switch (P.seg) {
+    case 4: hole2d_part_kernel<4><<<grid, 32 * kPartHoleWarps, smem, s>>>(modes, A, P, state); break;
+    case 8: hole2d_part_kernel<8><<<grid, 32 * kPartHoleWarps, smem, s>>>(modes, A, P, state); break;
+    case 12: hole2d_part_kernel<12><<<grid, 32 * kPartHoleWarps, smem, s>>>(modes, A, P, state); break;
+    case 16: hole2d_part_kernel<16><<<grid, 32 * kPartHoleWarps, smem, s>>>(modes, A, P, state); break;
+    default: throw AsdsmError(kUnsupported, "partitioned hole solve: segment length");
+  }
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void hole2d_prepare(size_t smem) {
   static bool done = false;
   if (done) return;
@@ -901,6 +1005,10 @@ void hole2d_prepare(size_t smem) {
                                         static_cast<int>(smem)));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kHole2DFusedMaxSmem)));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_part_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_part_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_part_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_part_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole2d_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kHole2DFusedMaxSmem)));
 }

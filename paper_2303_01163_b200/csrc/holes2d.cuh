@@ -41,5 +41,20 @@ void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevSta
 size_t hole2d_smem_bytes(int m0, int m1, int kb, bool y_in_smem, bool tables_in_smem = false);
 void hole2d_prepare(size_t smem);
 void launch_hole2d_fwd_thomas(const double* e, double* modes, const Hole2DArgs& A, DevState* state, cudaStream_t s);
+// Large holes, error mode, as two launches over a per-hole ring buffer ([hole][2 m1 + 2 m0]:
+// fL, fR, fB, fT): (1) one CTA per hole forms the ring; (2) one warp per (hole, mode k) forms the
+// two full row transforms of mode k (coalesced row of W, warp-shuffle sums), builds the mode
+// line and solves it with the warp partition method (SepSolver::part tables), writing modes as
+// [hole][k][j] (j contiguous: the back transform reads it with in_es = m1).
+struct Hole2DPartArgs {
+  const double* W;     // forward eigenvectors along x, [k][i] (row k contiguous)
+  const double* part;  // SepSolver::part of the hole solver, stride pstride per mode
+  int pstride, seg, P, last;
+  double* ring;        // [hole][2 m1 + 2 m0]
+};
+bool hole2d_part_supported(int seg);
+void launch_hole2d_ring(const double* e, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state,
+                        cudaStream_t s);
+void launch_hole2d_part(double* modes, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state, cudaStream_t s);
 
 }  // namespace asdsm_b200

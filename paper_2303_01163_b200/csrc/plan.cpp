@@ -284,7 +284,8 @@ std::vector<double> to_interleaved(const std::vector<cld>& v) {
 }  // namespace
 
 SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Stencil& st,
-                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what) {
+                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what,
+                           bool part_lines) {
   SepSolver s;
   s.dim = dim;
   for (int a = 0; a < 3; ++a) s.ext[a] = a < dim ? ext[a] : 1;
@@ -393,6 +394,7 @@ SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Sten
       s.th_ipiv = upload(dev, to_real(ipiv));
       s.th_cp = upload(dev, to_real(cp));
     }
+    if (part_lines && !s.complex_modes && m <= kPartMaxLine && m >= 2) build_partition_tables(s, m, l, r, dL, sigma, dev);
   } else {
     int levels = 0;
     while ((1 << levels) < m) ++levels;

@@ -150,7 +150,10 @@ struct DeviceAlloc {
 
 // Build a separable solver (host tables in long double, uploaded once).
 // `time_axis_in_box` marks an axis with the backward two-point stencil (not diagonalizable).
+// `part_lines`: also build the warp-partition tables (SepSolver::part) when the lines are solved
+// by per-thread Thomas (the 2D large-hole path solves them one warp per line instead).
 SepSolver build_sep_solver(DeviceAlloc& dev, int dim, const int* ext, const Stencil& st,
-                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what);
+                           int time_axis_in_box, int prefer_line_axis, i64 nbatch, const std::string& what,
+                           bool part_lines = false);
 
 }  // namespace asdsm_b200

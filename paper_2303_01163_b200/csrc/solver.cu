@@ -1,3 +1,4 @@
+#include <cstdio>
 // Host orchestration of one ASDSM solve on the device (proj/src/solver.cpp:486-680 restated
 // for a device-resident state).  All per-iteration decisions (normalization guard, step
 // clamp, accept/revert, stop rules) happen in ctrl kernels, so a whole solve is enqueued
@@ -96,7 +97,7 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     for (int a = 0; a < m.dim; ++a)
       sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
     sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
-    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block");
+    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block", m.dim == 2);
   } else {
     // per-point stencils (fdm.cpp:63-126 sampling) + block-Thomas factors for every box
     const std::vector<double> cf = sample_kind_coefficients(m, 0u, *varprob);
@@ -144,6 +145,8 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   if (!variable_) scratch = std::max(scratch, sep_scratch_bytes(sep_coarse_, 1));
   scratch0_ = dev_.alloc<unsigned char>(scratch);
   scratch1_ = dev_.alloc<unsigned char>(scratch);
+  if (m.dim == 2 && !variable_ && sep_hole_.part)  // per-hole ring of the partitioned hole solve
+    hole_ring_ = dev_.alloc<double>(static_cast<size_t>(nholes) * 2 * (sep_hole_.ext[0] + sep_hole_.ext[1]));
   if (m.dim == 3 && !variable_) {
     // the three slab solves of an iteration are independent: slabs 1 and 2 run on their own
     // streams (forked / joined with events, captured into the graph as parallel branches),
@@ -510,11 +513,21 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.line_left = H.line_left;
     A.line_right = H.line_right;
     double* modes = static_cast<double*>(scratch0_);
-    launch_hole2d_fwd_thomas(e, modes, A, state_, s);
+    // one warp per mode line with the partition method (measured, config 2: see DESIGN), else
+    // one thread per mode line (Thomas)
+    static const bool thomas = std::getenv("ASDSM_HOLE_THOMAS") != nullptr;
+    const bool part = !thomas && H.part && hole2d_part_supported(H.part_seg) && hole_ring_;
+    if (part) {
+      Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
+      launch_hole2d_ring(e, A, P, state_, s);
+      launch_hole2d_part(modes, A, P, state_, s);
+    } else {
+      launch_hole2d_fwd_thomas(e, modes, A, state_, s);
+    }
     GemmLines G{};
     G.o_ext[0] = A.m1;
     G.o_ext[1] = 1;
-    G.o_in[0] = A.m0;
+    G.o_in[0] = part ? 1 : A.m0;
     G.o_out[0] = g_fine_.stride[1];
     G.nbox[0] = A.nbox0;
     G.nbox[1] = A.nbox1;
@@ -524,9 +537,10 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     G.out_bs[0] = A.n0;
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
+    const i64 in_es = part ? A.m1 : 1;  // [hole][k][j] from the partition solve, else [hole][j][k]
     if (A.m0 >= kEoMinModes && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
-      launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, 1, 1, G, s);
-    else launch_dmma_transform(modes, e, H.V[0], A.m0, 1, 1, G, s);
+      launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, in_es, 1, G, s);
+    else launch_dmma_transform(modes, e, H.V[0], A.m0, in_es, 1, G, s);
     return;
   }
   if (!generic && mesh_.dim == 3 && b == nullptr && !H.complex_modes && H.nd == 2 && H.L == 2 && H.dax[0] == 0 &&

@@ -102,6 +102,7 @@ def _rel_floor(spec, nf, nc, iters, seed, ref):
     ("cfg:1:2", 199, 9, 20, 1),
     ("cfg:2:5", 199, 9, 20, 2),
     ("cfg:1:0", 0, 0, 20, 0),  # the headline mesh at full size (one-launch slab step path)
+    ("ex:1:1", 459, 3, 10, 2),  # holes of 114 x 114: the two-launch hole path (ring + partitioned lines)
 ])
 def test_iterate_history(spec, nf, nc, iters, seed):
     ctx, mesh, _ = _ctx(spec, nf, nc)
@@ -337,3 +338,21 @@ def test_skel3d_dots_rows_agree(spec, nf, nc, iters, monkeypatch):
     b = np.array([h.s_hat for h in st_pts.history[1:]])
     assert np.all(np.abs(a - b) <= 1e-12 * np.abs(b) + 1e-300)
     assert np.max(np.abs(st_rows.u - st_pts.u)) <= 1e-10 * np.max(np.abs(st_pts.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 459, 3, 8), ("ex:1:1", 919, 7, 6)])
+def test_partitioned_hole_lines_agree(spec, nf, nc, iters, monkeypatch):
+    """Large 2D holes (beyond the fused per-hole kernel): mode lines by one warp each with the
+    partition method (default) against one thread each with Thomas (ASDSM_HOLE_THOMAS=1)."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=4)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_p = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_HOLE_THOMAS", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_t = ctx1.iterate(opts)
+    a = np.array([h.res_l2 for h in st_p.history])
+    b = np.array([h.res_l2 for h in st_t.history])
+    k = np.arange(len(b))
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
+    assert np.max(np.abs(st_p.u - st_t.u)) <= 1e-8 * np.max(np.abs(st_t.u))
