@@ -107,6 +107,10 @@ int cmd_iterate(int argc, char** argv) {
     o.stagnation_window = 3;
     o.stagnation_ratio = 0.99;
   }
+  // explicit stop-rule options (test fixtures for the stop rules): tolerance, stagnation window/ratio
+  if (const char* v = std::getenv("REF_DUMP_TOL")) o.tol = std::atof(v);
+  if (const char* v = std::getenv("REF_DUMP_STAG_WINDOW")) o.stagnation_window = std::atoi(v);
+  if (const char* v = std::getenv("REF_DUMP_STAG_RATIO")) o.stagnation_ratio = std::atof(v);
   o.rng_seed = std::strtoull(argv[6], nullptr, 10);
   if (argc > 8) o.subsample = std::atof(argv[8]);
   std::vector<double> u0, r0;
