@@ -294,6 +294,12 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     cy1 = my > 1 ? Ty.ci[my - 1] : 0.0;
   };
   if (!CAUSAL) {
+#ifdef ASDSM_H3_TRACE
+    long long q0 = clock64(), q1 = 0, q2 = 0, q3 = 0;
+#define H3S(v) v = clock64()
+#else
+#define H3S(v)
+#endif
     double* YA = sm + L.faces;      // [2 (+/-)][mt][my]
     double* XB = YA + 2 * mt * my;  // [2][mt][mx]
     double* CH = XB + 2 * mt * mx;  // [2][my][mx]
@@ -330,6 +336,7 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     __syncthreads();
     double* G = X + mx * my;
     double* HZ = G + mx * my;
+    H3S(q1);
     zface_transform(e, A, h, 0, X, G, HZ, CH, Tx, Ty);
     if (mt > 1) zface_transform(e, A, h, mt - 1, X, G, HZ, CH + my * mx, Tx, Ty);
     else
@@ -422,7 +429,15 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         for (int q = 0; q < kPipe; ++q) cur[u][q] = nxt[u][q];
     }
     __syncthreads();
+    H3S(q2);
     back_planes(X, mt, 0, Tx, Ty, A, h, e);
+#ifdef ASDSM_H3_TRACE
+    __syncthreads();
+    q3 = clock64();
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 500))
+      printf("H3SYM blk %d faces %lld zfaces+sweeps %lld back %lld\n", blockIdx.x, q1 - q0, q2 - q1, q3 - q2);
+#endif
+#undef H3S
     return;
   }
   // ---------------- CAUSAL: planes in t order, TC at a time

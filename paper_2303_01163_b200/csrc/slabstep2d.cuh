@@ -27,6 +27,8 @@ struct SlabStep2DArgs {
 bool slabstep2d_supported(const MeshDev& m, const SepSolver* slab);
 size_t slabstep2d_smem_bytes(const SlabStep2DArgs& A);
 void slabstep2d_prepare();
+// the cluster of this build (2 x CTAs per slab) fits on this device with A's shared memory
+bool slabstep2d_launchable(const SlabStep2DArgs& A);
 void launch_slabstep2d(const SlabStep2DArgs& A, DevState* st, cudaStream_t s);
 
 }  // namespace asdsm_b200

@@ -261,7 +261,10 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
       skel_line_[0] = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * m.nf[1]);
       skel_line_[1] = dev_.alloc<double>(static_cast<size_t>(m.nc[1]) * m.nf[0]);
       skel_corr_ = dev_.alloc<double>(2 * static_cast<size_t>(m.nc[0]) * m.nc[1]);
-      if (step2d_) slabstep2d_prepare();
+      if (step2d_) {
+        slabstep2d_prepare();
+        step2d_ = slabstep2d_launchable(slabstep2d_args(nullptr, nullptr));
+      }
       seg2_ = dev_.alloc<double>(static_cast<size_t>(m.nc[0]) * 4 * (m.nc[1] + 1));
     }
   }
