@@ -25,9 +25,9 @@ constexpr int TX3 = 32, TY3 = 16;             // 3D: x-by-y tile (z chunk: March
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // 2D persistent stencil pass: prefetch the next tile's streamed arrays into L2 while this tile
-// computes (measured, config 2: update pass 309 -> 252 us, solve 20.3 -> 19.1 ms on one box; the
-// same in the 3D z-coarsened pass measured slower at configs 3/4, so it is 2D only;
-// ASDSM_NO_TILE_PREFETCH=1 turns it off)
+// computes (measured, config 2: update pass 309 -> 252 us with 8-row tiles; the same in the 3D
+// z-coarsened pass measured slower at configs 3/4, so it is 2D only; ASDSM_NO_TILE_PREFETCH=1
+// turns it off)
 template <int MODE>
 struct Src {
   const double* __restrict__ u;
@@ -697,9 +697,15 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   } else if (A.g.dim == 2) {
     // measured (configs 1-2): 8-row segments, a persistent grid of 4 CTAs per SM (more CTAs
     // pay in the completion count and block scheduling, fewer leave HBM latency exposed)
-    constexpr int kYc = 8;
+    // measured (configs 1-2, one box): 4-row segments on a 4-CTA/SM persistent grid, so every
+    // CTA walks ~2 tiles (config 1) and L2-prefetches the next one -- config 1 update pass 18.0 ->
+    // 15.0 us, config 2 245 -> 153 us against 8-row segments (80 registers with the prefetch:
+    // three CTAs per SM, a second wave at config 1); ASDSM_YC / ASDSM_YC_CPS override
+    static const int yc_env = std::getenv("ASDSM_YC") ? std::atoi(std::getenv("ASDSM_YC")) : 4;
+    static const int cps = std::getenv("ASDSM_YC_CPS") ? std::atoi(std::getenv("ASDSM_YC_CPS")) : 4;
+    const int kYc = yc_env == 8 ? 8 : (yc_env == 2 ? 2 : 4);
     const long long tiles = static_cast<long long>((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 8 * kYc - 1) / (8 * kYc));
-    const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, 4LL * kNumSms));
+    const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, static_cast<long long>(cps) * kNumSms));
 #define ASDSM_YC_DISPATCH(YCV)                                                                              \
   do {                                                                                                      \
     if (var) {                                                                                              \
@@ -712,7 +718,9 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
       else launch_pdl(stencil2d_yc_kernel<kMarchDots, false, YCV>, nb2, 256, 0, s, A);                     \
     }                                                                                                       \
   } while (0)
-    ASDSM_YC_DISPATCH(kYc);
+    if (kYc == 4) ASDSM_YC_DISPATCH(4);
+    else if (kYc == 2) ASDSM_YC_DISPATCH(2);
+    else ASDSM_YC_DISPATCH(8);
 #undef ASDSM_YC_DISPATCH
   } else if (mode == kMarchUpdate && std::getenv("ASDSM_MARCH3D") == nullptr) {
     // measured (configs 3/4): axpy + candidate residual beats the fused 3D update
