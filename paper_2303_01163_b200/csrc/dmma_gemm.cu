@@ -29,8 +29,11 @@ __device__ __forceinline__ void line_base(const GemmLines& L, i64 p, i64& ib, i6
   ob = h0 * L.out_bs[0] + h1 * L.out_bs[1] + h2 * L.out_bs[2] + o0 * L.o_out[0] + o1 * L.o_out[1];
 }
 
+#ifndef ASDSM_DENSE_MINB
+#define ASDSM_DENSE_MINB 3  // 168 registers, three CTAs per SM (config 4: 54.0 -> 53.8 ms)
+#endif
 template <bool kContigIn, bool kContigOut>
-__global__ void __launch_bounds__(NTH) dmma_transform_kernel(const double* __restrict__ in, double* __restrict__ out,
+__global__ void __launch_bounds__(NTH, ASDSM_DENSE_MINB) dmma_transform_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                              const double* __restrict__ M, int m, i64 in_es, i64 out_es,
                                                              GemmLines L) {
   __shared__ double As[BP][BK + PAD];

@@ -501,9 +501,15 @@ __global__ void __launch_bounds__(256) skel3d_dots_rows_kernel(MarchArgs A) {
 // Barrier-free 3D variant: persistent blocks of 32x8 threads over (32 x 8 x ZC) tiles; each
 // thread owns ZC consecutive z points and keeps the z-neighbours in registers (ZC+2 loads for
 // ZC points), x/y neighbours come through L1 (same or adjacent warps' lines).
-constexpr int ZC = 8;
+#ifndef ASDSM_ZC
+#define ASDSM_ZC 8
+#endif
+#ifndef ASDSM_ZC_MINB
+#define ASDSM_ZC_MINB 4
+#endif
+constexpr int ZC = ASDSM_ZC;
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256, 4) stencil3d_zc_kernel(MarchArgs A) {
+__global__ void __launch_bounds__(256, ASDSM_ZC_MINB) stencil3d_zc_kernel(MarchArgs A) {
   DevState* S = A.state;
   if (!S->active) return;
   const int cur = S->cur;
