@@ -269,6 +269,104 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
   (void)nf2;
 }
 
+// The same splines one warp per line (nc <= 30 knots per line): lanes load the knot values and
+// form the right-hand sides and the segment coefficients in parallel, lane 0 runs the short
+// Thomas chain; the working arrays live in shared memory (the thread-per-line kernel above keeps
+// them in local memory, one dependent local access per step).  Same operations in the same order
+// as spline_second_derivs / spline_segments: bitwise the same tables.
+constexpr int kDerivWarps = 4;
+constexpr int kWarpKnots = 32;
+
+__device__ __forceinline__ void spline_warp(const MeshDev& m, int axis, double* ys, double* dg, double* up, double* rh,
+                                            double* mmS, double* mm, double* seg) {
+  const int lane = threadIdx.x & 31;
+  const int nc = m.nc[axis], n = nc + 2, ni = n - 2;
+  __syncwarp();
+  if (lane < ni) {  // spline_second_derivs: rhs, diag, upper of row i
+    const int i = lane;
+    const double x0 = knot(m, axis, i), x1 = knot(m, axis, i + 1), x2 = knot(m, axis, i + 2);
+    const double hl = __dsub_rn(x1, x0);
+    const double hr = __dsub_rn(x2, x1);
+    dg[i] = __dadd_rn(hl, hr) / 3.0;
+    up[i] = hr / 6.0;
+    rh[i] = __dsub_rn(__dsub_rn(ys[i + 2], ys[i + 1]) / hr, __dsub_rn(ys[i + 1], ys[i]) / hl);
+  }
+  if (lane < n) mmS[lane] = 0.0;
+  __syncwarp();
+  if (lane == 0 && ni > 0) {
+    for (int i = 1; i < ni; ++i) {
+      const double lower = __dsub_rn(knot(m, axis, i + 1), knot(m, axis, i)) / 6.0;
+      const double w = lower / dg[i - 1];
+      dg[i] = __dsub_rn(dg[i], __dmul_rn(w, up[i - 1]));
+      rh[i] = __dsub_rn(rh[i], __dmul_rn(w, rh[i - 1]));
+    }
+    mmS[ni] = rh[ni - 1] / dg[ni - 1];
+    for (int i = ni - 1; i >= 1; --i) mmS[i] = __dsub_rn(rh[i - 1], __dmul_rn(up[i - 1], mmS[i + 1])) / dg[i - 1];
+  }
+  __syncwarp();
+  if (lane < n) mm[lane] = mmS[lane];
+  if (lane <= nc) {  // spline_segments: interval i
+    const int i = lane;
+    const double xi = knot(m, axis, i), xi1 = knot(m, axis, i + 1);
+    const double y0 = ys[i], y1 = ys[i + 1], m0 = mmS[i], m1 = mmS[i + 1];
+    const double h = __dsub_rn(xi1, xi);
+    double4 c;
+    c.x = y0;
+    c.y = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m0), m1)) / 6.0);
+    c.z = m0 / 2.0;
+    c.w = __dsub_rn(m1, m0) / __dmul_rn(6.0, h);
+    *reinterpret_cast<double4*>(seg + 4 * i) = c;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kDerivWarps) m3_derivs_warp_kernel(Merge3DArgs A, int stage, const DevState* st) {
+  if (!st->active || !st->have_e) return;
+  __shared__ double sh[kDerivWarps][5][kWarpKnots + 2];
+  const int a = blockIdx.y;  // slab
+  const MeshDev& m = A.m;
+  const PlaneCtx c = plane_ctx(A, a);
+  const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2], nf1 = m.nf[c.f1], nf2 = m.nf[c.f2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kDerivWarps + warp;
+  double* ys = sh[warp][0];
+  double* dg = sh[warp][1];
+  double* up = sh[warp][2];
+  double* rh = sh[warp][3];
+  double* mmS = sh[warp][4];
+  if (stage == 0) {
+    const int n1 = ncA * nf2, n2 = ncA * nf1, n3 = ncA * nc2;
+    if (t < n1) {
+      const int I = t % ncA, k2 = t / ncA;
+      if (lane < nc1 + 2) ys[lane] = (lane == 0 || lane == nc1 + 1) ? 0.0 : fam1_y(m, c, I, k2, lane - 1);
+      spline_warp(m, c.f1, ys, dg, up, rh, mmS, A.mF1[a] + static_cast<i64>(t) * (nc1 + 2),
+                  A.sF1[a] + static_cast<i64>(t) * 4 * (nc1 + 1));
+    } else if (t < n1 + n2) {
+      const int l = t - n1;
+      const int I = l % ncA, k1 = l / ncA;
+      if (lane < nc2 + 2) ys[lane] = (lane == 0 || lane == nc2 + 1) ? 0.0 : fam2_y(m, c, I, k1, lane - 1);
+      spline_warp(m, c.f2, ys, dg, up, rh, mmS, A.mF2[a] + static_cast<i64>(l) * (nc2 + 2),
+                  A.sF2[a] + static_cast<i64>(l) * 4 * (nc2 + 1));
+    } else if (t < n1 + n2 + n3) {
+      const int l = t - n1 - n2;
+      const int I = l % ncA, C2 = l / ncA;
+      if (lane < nc1 + 2) ys[lane] = (lane == 0 || lane == nc1 + 1) ? 0.0 : fam3_y(A, c, I, C2, lane - 1);
+      spline_warp(m, c.f1, ys, dg, up, rh, mmS, A.mF3a[a] + static_cast<i64>(l) * (nc1 + 2),
+                  A.sF3a[a] + static_cast<i64>(l) * 4 * (nc1 + 1));
+    }
+  } else {
+    const int n = ncA * nf1;
+    if (t >= n) return;
+    const int I = t % ncA, k1 = t / ncA;
+    if (lane < nc2 + 2)
+      ys[lane] = (lane == 0 || lane == nc2 + 1)
+                     ? 0.0
+                     : spline_eval_seg(m, c.f1, A.sF3a[a] + static_cast<i64>(I + ncA * (lane - 1)) * 4 * (nc1 + 1), k1 + 1);
+    spline_warp(m, c.f2, ys, dg, up, rh, mmS, A.mF3b[a] + static_cast<i64>(t) * (nc2 + 2),
+                A.sF3b[a] + static_cast<i64>(t) * 4 * (nc2 + 1));
+  }
+  (void)nf2;
+}
+
 // corrected slab a = slab + ((s1 + s2) - s3) at every slab point (solver.cpp:289-292), each
 // spline from its line's segment table
 __global__ void m3_apply_kernel(Merge3DArgs A, const DevState* st) {
@@ -389,8 +487,16 @@ void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_
     nl3 = std::max(nl3, m.nc[a] * m.nf[f1]);
     ns = std::max(ns, static_cast<i64>(m.nc[a]) * m.nf[f1] * m.nf[f2]);
   }
-  m3_derivs_kernel<<<dim3((nl + 31) / 32, 3), 32, 0, s>>>(A, 0, st);
-  m3_derivs_kernel<<<dim3((nl3 + 31) / 32, 3), 32, 0, s>>>(A, 1, st);
+  static const bool per_thread = std::getenv("ASDSM_M3_THREAD_LINES") != nullptr;
+  bool warp_ok = !per_thread;
+  for (int q = 0; q < 3; ++q) warp_ok = warp_ok && m.nc[q] + 2 <= kWarpKnots;
+  if (warp_ok) {
+    m3_derivs_warp_kernel<<<dim3((nl + kDerivWarps - 1) / kDerivWarps, 3), 32 * kDerivWarps, 0, s>>>(A, 0, st);
+    m3_derivs_warp_kernel<<<dim3((nl3 + kDerivWarps - 1) / kDerivWarps, 3), 32 * kDerivWarps, 0, s>>>(A, 1, st);
+  } else {
+    m3_derivs_kernel<<<dim3((nl + 31) / 32, 3), 32, 0, s>>>(A, 0, st);
+    m3_derivs_kernel<<<dim3((nl3 + 31) / 32, 3), 32, 0, s>>>(A, 1, st);
+  }
   m3_apply_kernel<<<dim3(nblk(ns, 256, 3 * kNumSms), 3), 256, 0, s>>>(A, st);
   g_kernel_launches += 3;
   const i64 nskel = static_cast<i64>(m.nc[0]) * m.nf[1] * m.nf[2] +

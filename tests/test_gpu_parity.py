@@ -356,3 +356,16 @@ def test_partitioned_hole_lines_agree(spec, nf, nc, iters, monkeypatch):
     assert len(a) == len(b)
     assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
     assert np.max(np.abs(st_p.u - st_t.u)) <= 1e-8 * np.max(np.abs(st_t.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:4:1", 24, 4, 6)])
+def test_merge3d_warp_splines_bitwise(spec, nf, nc, iters, monkeypatch):
+    """3D merge splines one warp per line (default) against one thread per line
+    (ASDSM_M3_THREAD_LINES=1): the same operations in the same order, so bitwise the same solve."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=6)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_w = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_M3_THREAD_LINES", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_t = ctx1.iterate(opts)
+    assert np.array_equal(st_w.u, st_t.u) and np.array_equal(st_w.r, st_t.r)
