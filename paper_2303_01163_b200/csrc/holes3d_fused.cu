@@ -38,7 +38,10 @@ constexpr int kH3Threads = 512;
 constexpr int kH3Warps = kH3Threads / 32;
 constexpr int kCausalLines = 8;  // CAUSAL: (k,l) lines per thread (mx*my <= 4096)
 constexpr int kSymLines = 2;     // SYM: lines per thread (mx*my <= 1024)
-constexpr int kPipe = 8;         // SYM: t steps per pivot-table load batch
+#ifndef ASDSM_H3_PIPE
+#define ASDSM_H3_PIPE 8
+#endif
+constexpr int kPipe = ASDSM_H3_PIPE;  // SYM: t steps per pivot-table load batch
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -343,6 +346,9 @@ __global__ void __launch_bounds__(kH3Threads, 1)
       for (int q = tid; q < mx * my; q += kH3Threads) CH[my * mx + q] = 0.0;
     for (int q = tid; q < L.xsize; q += kH3Threads) X[q] = 0.0;
     __syncthreads();
+#ifdef ASDSM_H3_TRACE
+    const long long q1b = clock64();
+#endif
     // line solves: lines c = tid + u * threads; pivot tables streamed kPipe steps ahead
     int kq[kSymLines], lq[kSymLines];
     bool ok[kSymLines];
@@ -435,7 +441,8 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     __syncthreads();
     q3 = clock64();
     if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 500))
-      printf("H3SYM blk %d faces %lld zfaces+sweeps %lld back %lld\n", blockIdx.x, q1 - q0, q2 - q1, q3 - q2);
+      printf("H3SYM blk %d faces %lld zfaces %lld sweeps %lld back %lld\n", blockIdx.x, q1 - q0, q1b - q1, q2 - q1b,
+             q3 - q2);
 #endif
 #undef H3S
     return;
