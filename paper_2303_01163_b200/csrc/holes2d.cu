@@ -189,10 +189,14 @@ __global__ void __launch_bounds__(32 * kPartHoleWarps) hole2d_part_kernel(double
   const int k0 = blockIdx.y * kPartHoleWarps;
   const double* ring = P.ring + static_cast<i64>(hole) * (2 * m1 + 2 * m0);
   for (int t = threadIdx.x; t < 2 * m1 + 2 * m0; t += blockDim.x) cp_async8(fL + t, ring + t);
+#ifdef ASDSM_PART_HOLE_STAGE
   for (int t = threadIdx.x; t < kPartHoleWarps * P.pstride; t += blockDim.x) {
     const int w = t / P.pstride, o = t - w * P.pstride;
     if (k0 + w < m0) cp_async8(tabs + t, P.part + static_cast<i64>(k0 + w) * P.pstride + o);
   }
+#else
+  (void)tabs;
+#endif
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   const int k = k0 + warp;
   const double* Wk = P.W + static_cast<i64>(min(k, m0 - 1)) * m0;  // row k: coalesced
@@ -216,7 +220,13 @@ __global__ void __launch_bounds__(32 * kPartHoleWarps) hole2d_part_kernel(double
   for (int j = lane; j < m1; j += 32)
     line[j] = j == 0 ? fb : (j == m1 - 1 ? ft : fma(wm, fR[j], w0 * fL[j]));
   __syncwarp();
+#ifdef ASDSM_PART_HOLE_STAGE
   part_solve_line<SEG>(line, tabs + warp * P.pstride, m1, P.P, P.last, A.line_left, A.line_right);
+#else
+  // the mode's table straight from L2 (shared by every hole; loads issued ahead of the chains),
+  // leaving shared memory to the lines: more CTAs per SM
+  part_solve_line<SEG>(line, P.part + static_cast<i64>(k) * P.pstride, m1, P.P, P.last, A.line_left, A.line_right);
+#endif
   __syncwarp();
   double* out = modes + static_cast<i64>(hole) * m0 * m1 + static_cast<i64>(k) * m1;
   for (int j = lane; j < m1; j += 32) out[j] = line[j];
@@ -980,8 +990,12 @@ void launch_hole2d_ring(const double* e, const Hole2DArgs& A, const Hole2DPartAr
 
 void launch_hole2d_part(double* modes, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state, cudaStream_t s) {
   const int lp = (A.m1 + 1) & ~1;
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(A.m1 + A.m0) + 1 + kPartHoleWarps * static_cast<size_t>(lp) +
-                                        kPartHoleWarps * static_cast<size_t>(P.pstride));
+#ifdef ASDSM_PART_HOLE_STAGE
+  const size_t tab = kPartHoleWarps * static_cast<size_t>(P.pstride);
+#else
+  const size_t tab = 0;
+#endif
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(A.m1 + A.m0) + 1 + kPartHoleWarps * static_cast<size_t>(lp) + tab);
   if (smem > 100 * 1024) throw AsdsmError(kUnsupported, "partitioned hole solve exceeds shared memory");
   const dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m0 + kPartHoleWarps - 1) / kPartHoleWarps));
   switch (P.seg) {
