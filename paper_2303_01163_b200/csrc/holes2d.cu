@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) hole2d_ring_kernel(const double* __restri
 }
 
 #ifndef ASDSM_PART_HOLE_WARPS
-#define ASDSM_PART_HOLE_WARPS 8
+#define ASDSM_PART_HOLE_WARPS 12  // measured 8 / 12 / 16 at config 2: 16.27 / 16.09 / 16.27 ms
 #endif
 constexpr int kPartHoleWarps = ASDSM_PART_HOLE_WARPS;  // mode lines (warps) per CTA
 
