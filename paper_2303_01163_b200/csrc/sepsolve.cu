@@ -303,7 +303,8 @@ template <int SEG>
 __global__ void __launch_bounds__(32 * kPartWarps) part_line_kernel(PartArgs A) {
   extern __shared__ __align__(16) double psm[];
   double* lines = psm;                        // [kPartWarps][m]
-  double* tabs = psm + kPartWarps * A.m;      // [kPartWarps][pstride]
+  double* tabs = psm + kPartWarps * A.m;      // [kPartWarps][pstride] (ASDSM_PART_LINE_STAGE)
+  (void)tabs;
   const int warp = threadIdx.x >> 5;
   const i64 line0 = static_cast<i64>(blockIdx.x) * kPartWarps;
   auto base_of = [&](i64 line) -> double* {
@@ -322,11 +323,13 @@ __global__ void __launch_bounds__(32 * kPartWarps) part_line_kernel(PartArgs A) 
     const i64 line = line0 + threadIdx.x;
     bases[threadIdx.x] = line < A.nlines ? base_of(line) : nullptr;
   }
+#ifdef ASDSM_PART_LINE_STAGE
   for (int q = threadIdx.x; q < kPartWarps * A.pstride; q += blockDim.x) {
     const int w = q / A.pstride, o = q - w * A.pstride;
     const i64 line = line0 + w;
     if (line < A.nlines) cp_async8(tabs + q, A.part + static_cast<i64>(line % A.ncombo) * A.pstride + o);
   }
+#endif
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   __syncthreads();
   const int n = kPartWarps * A.m;
@@ -344,7 +347,15 @@ __global__ void __launch_bounds__(32 * kPartWarps) part_line_kernel(PartArgs A) 
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
+#ifdef ASDSM_PART_LINE_STAGE
   if (bases[warp]) part_solve_line<SEG>(lines + warp * A.m, tabs + warp * A.pstride, A.m, A.P, A.last, A.l, A.r);
+#else
+  // the mode's partition table straight from L2 (measured, configs 3/4: 11.87 -> 11.79 ms,
+  // 53.89 -> 53.83 ms against staging it per CTA)
+  if (bases[warp])
+    part_solve_line<SEG>(lines + warp * A.m, A.part + static_cast<i64>((line0 + warp) % A.ncombo) * A.pstride, A.m, A.P,
+                         A.last, A.l, A.r);
+#endif
   __syncthreads();
   for (int q = threadIdx.x; q < n; q += blockDim.x) {
     int w, p;
@@ -488,7 +499,11 @@ void launch_line_solve(const SepSolver& S, const BoxArray& buf, cudaStream_t st)
     A.l = S.line_left;
     A.r = S.line_right;
     A.line_major = A.stride_L == 1 ? 1 : 0;
+#ifdef ASDSM_PART_LINE_STAGE
     const size_t smem = sizeof(double) * kPartWarps * (static_cast<size_t>(A.m) + A.pstride);
+#else
+    const size_t smem = sizeof(double) * kPartWarps * static_cast<size_t>(A.m);
+#endif
     if (smem > kPcrMaxSmem) throw AsdsmError(kUnsupported, "partitioned line solve exceeds shared memory");
     const unsigned grid = static_cast<unsigned>((A.nlines + kPartWarps - 1) / kPartWarps);
     switch (S.part_seg) {
