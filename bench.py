@@ -72,7 +72,7 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons (NVML, else nvidia-smi) sampled during the timed region."""
 
     def __init__(self, gpu=0):
         self.gpu = gpu
@@ -81,20 +81,42 @@ class ClockSampler:
         self._t = None
 
     def start(self):
-        def run():
+        # NVML in-process (what nvidia-smi reads) when available: no subprocess spawned inside the
+        # timed region; nvidia-smi otherwise
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                    ("sw_power_cap", 0x4)]
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = reasons_fn(h)
+                return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for _, b in bits]
+        except Exception:
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap")
+
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                return [x.strip() for x in out.split(",")] if out else None
+
+        def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    v = sample()
+                    if v:
+                        self.samples.append(v)
                 except Exception:
                     pass
-                self._stop.wait(0.1)
+                self._stop.wait(0.02)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -322,7 +344,7 @@ def main():
                                         dp(h_exact) if h_exact is not None else None, ctypes.byref(copt),
                                         dp(h_hist), ctypes.byref(nrec), ctypes.byref(stop), dp(h_u), dp(h_r)))
 
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(args.warmup, 5)):
         flush_l2(pstream)
         e2e_step()
     etimes = []
