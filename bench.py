@@ -1,16 +1,24 @@
 """ASDSM benchmark on B200.
 
 Metric: fine-grid DOF-iterations/s = (fine unknowns x ASDSM iterations) / solve time.  One
-"step" = one full ASDSM solve of the configured BASELINE.json problem (initial guess + K
-iterations, K from BASELINE.json), on a prebuilt plan (the reference's SolverContext: tables,
-operators) with the assembled right-hand-side bundle resident in HBM; L2 flushed between
-steps.  `e2e`: the same solve through the C-ABI with pinned HOST buffers (H2D of the bundle,
-D2H of u, r and the history inside the timed region).
+"step" = one full ASDSM solve of a BASELINE.json problem (initial guess + K iterations, K from
+BASELINE.json), on a prebuilt plan (the reference's SolverContext: tables, operators) with the
+assembled right-hand-side bundle resident in HBM; L2 flushed between steps.  `e2e`: the same
+solve through the C-ABI (asdsm_solve) with pinned HOST buffers (H2D of the bundle, D2H of u, r
+and the history inside the timed region).
+
+The headline line is `--config` (default 1, BASELINE configs[1]); with the default
+`--per-config`, every BASELINE config is measured the same way (value, e2e, rooflines, clocks,
+a bounded CPU sample of the reference) and listed under "per_config".
 
   python bench.py [--config 1] [--steps K] [--warmup W] [--gpus N] [--impl ours|reference]
+
+The reference arm (--impl reference) runs the reference's own C++ sources (oracle/_ref) on the
+host cores; it does not import this package.
 """
 import argparse
 import ctypes
+import glob
 import json
 import os
 import subprocess
@@ -22,14 +30,43 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
 
+# Workload names carry the mesh actually run: the reference needs (N_f + 1) = n (N_c + 1)
+# (mesh.cpp:63-68), so each BASELINE N maps to the nearest admissible N_f at the reference's
+# default N_c = 9.
 CONFIG_NAMES = [
-    "2d_steady_N128_manufactured",
-    "2d_steady_N1024_bumps8",
-    "2d_advection_N4096_bumps16",
-    "3d_steady_N256_manufactured",
-    "2d_time_N512_spacetime_bumps8",
+    "2d_steady_Nf129_Nc9_manufactured",
+    "2d_steady_Nf1029_Nc9_bumps8",
+    "2d_advection_Nf4099_Nc9_bumps16",
+    "3d_steady_Nf259_Nc9_manufactured",
+    "2d_time_Nf509_Nc9_spacetime_bumps8",
+]
+ITERATIONS = [10, 20, 20, 10, 10]
+# fine / coarse interior counts per axis of each config (include/asdsm_problems.hpp baseline_mesh)
+MESHES = [([129, 129], [9, 9]), ([1029, 1029], [9, 9]), ([4099, 4099], [9, 9]), ([259] * 3, [9] * 3),
+          ([509] * 3, [9] * 3)]
+
+
+def config_dict(cid, world):
+    """The `config` object of both arms (identical keys and values)."""
+    fine, coarse = MESHES[cid]
+    return {"workload": CONFIG_NAMES[cid], "config_id": cid, "fine_counts": fine, "coarse_counts": coarse,
+            "iterations": ITERATIONS[cid], "dof": int(np.prod(fine)),
+            "l2": "GPU arm: flushed between steps (256 MB write)",
+            "parallelism": f"replicas x{world}" if world > 1 else "1gpu"}
+# Bounded CPU samples of the reference per config: (nf, nc, iterations run, what).  Full solves
+# where they take seconds; the full mesh with 1 iteration for configs 2 and 3 (the rate of a
+# K-iteration solve is extrapolated from the measured initial-guess and iteration times); for
+# config 4 (509^3 does not fit a bounded sample: ~1000 hole solves of 50^3 per iteration) the
+# reference on 101^3 at N_c = 1, i.e. the same 50^3 space-time holes and the same ratio of hole,
+# skeleton and fine work per DOF.
+CPU_SAMPLE = [
+    (0, 0, 10, "full solve (initial guess + 10 iterations) at the config's mesh"),
+    (0, 0, 20, "full solve (initial guess + 20 iterations) at the config's mesh"),
+    (0, 0, 1, "the config's full 4099^2 mesh: initial guess + 1 iteration timed, the 20-iteration rate extrapolated"),
+    (0, 0, 1, "the config's full 259^3 mesh: initial guess + 1 iteration timed, the 10-iteration rate extrapolated"),
+    (101, 1, 1, "101^3 at N_c=1 (the config's 50^3 space-time holes): initial guess + 1 iteration timed, "
+                "the 10-iteration rate per DOF extrapolated"),
 ]
 FP64_PEAK_TFLOPS = 37.0  # measured on this pool's B200 (scripts/probe_fp64.cu: DMMA 37.0, DFMA 36.6)
 REF_DUMP = os.path.join(ROOT, "oracle", "_ref", "ref_dump")
@@ -44,22 +81,95 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-all-configs", dest="all_configs", action="store_false",
-                    help="skip timing every other BASELINE config (value only)")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false",
+                    help="measure the headline config only")
+    ap.add_argument("--only", type=str, default=None, help="comma list of configs for per_config")
     return ap.parse_args()
 
 
-def ncu_traffic(cid, kernel):
-    """DRAM bytes per launch (read + write) of `kernel` at config `cid` from the committed ncu
-    --set full capture (profiles/r*_traffic.json, newest round first), else None."""
-    import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+# ---------------------------------------------------------------------------------------------
+# reference (CPU) side: no import of this package
+# ---------------------------------------------------------------------------------------------
+
+def reference_sample(cid, seed):
+    """One bounded sample of config `cid` by the compiled reference (oracle/_ref: the reference's
+    own sources).  Returns (DOF-iter/s of the K-iteration solve, details).  Context setup
+    (factorizations) is excluded, as on the GPU arm (prebuilt plan)."""
+    nf, nc, it, what = CPU_SAMPLE[cid]
+    with tempfile.TemporaryDirectory() as d:
+        prefix = os.path.join(d, "r")
+        t0 = time.time()
+        subprocess.check_call([REF_DUMP, "iterate", f"cfg:{cid}:{seed}", str(nf), str(nc), str(it), "0", prefix],
+                              stdout=subprocess.DEVNULL)
+        wall = time.time() - t0
+        rows = np.array([[float(x) for x in line.split()] for line in open(prefix + ".hist.txt")
+                         if not line.startswith("#")])
+        meta = open(prefix + ".meta.txt").read().split("\n")
+    fine = [int(x) for x in meta[1].split()]
+    coarse = [int(x) for x in meta[2].split()]
+    ndof = int(np.prod(fine))
+    t_init = rows[0, 6] / 1e3
+    t_iter = float(np.mean(rows[1:, 6])) / 1e3 if len(rows) > 1 else 0.0
+    k = ITERATIONS[cid]
+    t_solve = t_init + k * t_iter  # == the measured total when the sample is the full solve
+    return ndof * k / t_solve, {
+        "sample_mesh": {"fine_counts": fine, "coarse_counts": coarse, "dof": ndof},
+        "iterations_timed": len(rows) - 1, "t_initial_guess_s": t_init, "t_iteration_s": t_iter,
+        "t_solve_s_extrapolated" if it != k else "t_solve_s": t_solve, "wall_s_incl_setup": wall}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's CPU implementation (oracle/_ref), all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cid = args.config
+    if not os.path.exists(REF_DUMP):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_dump not built"}))
+        return
+    cores = os.cpu_count() or 1
+    full = CPU_SAMPLE[cid][2] == ITERATIONS[cid] and CPU_SAMPLE[cid][0] == 0
+    for _ in range(args.warmup if full else 0):
+        reference_sample(cid, args.seed)
+    vals, det = [], None
+    for _ in range(args.steps if full else 1):
+        v, det = reference_sample(cid, args.seed)
+        vals.append(v)
+    value = float(np.mean(vals))
+    ndof = det["sample_mesh"]["dof"]
+    ms = ndof * ITERATIONS[cid] / value * 1e3
+    print(json.dumps({
+        "impl": "reference", "metric": "fine-grid DOF-iterations/sec", "value": value, "unit": "DOF-iter/s",
+        "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup if full else 0, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded, BASELINE.json config {cid})",
+        "config": config_dict(cid, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": cores, "kind": "reference",
+                         "sample": CPU_SAMPLE[cid][3] + "; the reference's own C++ (oracle/_ref) with the "
+                                   "Eigen SparseLU stand-in (RCM + band LU), hole solves threaded"},
+        "reference_detail": det,
+        "e2e": {"value": value, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------------------------
+
+def ncu_traffic(cid, component, kernels):
+    """DRAM bytes per launch (read + write) of `component` at config `cid` from a committed
+    `ncu --set full` capture (profiles/r*_traffic*.json, newest first), only when the captured
+    kernel is the one this plan's solve graph actually launches; else None."""
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic*.json")),
+                   key=lambda p: os.path.getmtime(p), reverse=True)
+    for path in paths:
         try:
-            k = json.load(open(path))["kernels"].get(f"{cid}/{kernel}")
+            k = json.load(open(path))["kernels"].get(f"{cid}/{component}")
         except Exception:
             continue
-        if k:
-            return float(k["dram_read_bytes"] + k["dram_write_bytes"])
+        if k and any(k["kernel"] == n or n.endswith("::" + k["kernel"]) for n in kernels):
+            return {"bytes": float(k["dram_read_bytes"] + k["dram_write_bytes"]), "kernel": k["kernel"],
+                    "source": os.path.relpath(path, ROOT)}
     return None
 
 
@@ -152,77 +262,22 @@ def max_over_ranks(value, device):
     return float(t.item())
 
 
-def reference_solve(cid, seed, iters):
-    """One solve of the compiled reference (oracle/_ref: the reference's own sources); returns
-    (solve seconds excluding context setup, history rows)."""
-    with tempfile.TemporaryDirectory() as d:
-        prefix = os.path.join(d, "r")
-        subprocess.check_call([REF_DUMP, "iterate", f"cfg:{cid}:{seed}", "0", "0", str(iters), "0", prefix],
-                              stdout=subprocess.DEVNULL)
-        rows = np.array([[float(x) for x in line.split()] for line in open(prefix + ".hist.txt") if not line.startswith("#")])
-    return float(rows[:, 6].sum()) / 1e3, rows
+# Which components are the north star's HBM-bound fine-grid / merge kernels (>= 60 % target).
+HBM_COMPONENTS = ("update_residual", "dots_update", "residual", "skeleton_merge", "merge3d", "gather")
 
 
-def run_reference_arm(args):
-    """--impl reference: the reference's CPU implementation (oracle/_ref), all host threads."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import paper_2303_01163_b200 as pb
-    cid = args.config
-    mesh, iters = pb.baseline_mesh(cid)
-    ndof = mesh.point_count(pb.MeshKind.fine(mesh.dim))
-    cores = os.cpu_count() or 1
-    if not os.path.exists(REF_DUMP):
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_dump not built"}))
-        return
-    # bounded sample: full solves for the small configs, (initial guess + 1 iteration) beyond
-    sample_iters = iters if ndof <= 2_000_000 else 1
-    for _ in range(args.warmup if sample_iters == iters else 0):
-        reference_solve(cid, args.seed, sample_iters)
-    times = []
-    for _ in range(args.steps if sample_iters == iters else 1):
-        t, rows = reference_solve(cid, args.seed, sample_iters)
-        times.append(t)
-    t = float(np.mean(times))
-    value = ndof * sample_iters / t
-    sample = (f"full solve ({iters} iterations + initial guess), context setup excluded"
-              if sample_iters == iters else "initial guess + 1 iteration, context setup excluded")
-    print(json.dumps({
-        "impl": "reference", "metric": "fine-grid DOF-iterations/sec", "value": value, "unit": "DOF-iter/s",
-        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (seeded, BASELINE.json config {cid})",
-        "config": {"workload": CONFIG_NAMES[cid], "config_id": cid, "fine_counts": mesh.fine_counts,
-                   "coarse_counts": mesh.coarse_counts, "iterations": iters, "dof": ndof},
-        "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": cores, "kind": "reference", "sample": sample},
-        "e2e": {"value": value, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
-
-
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference_arm(args)
-        return
+def measure_config(cid, args, world, rank, local, flush, steps, warmup):
+    """Value, e2e, per-component rooflines and clocks of config `cid` on this GPU."""
     import torch
     import paper_2303_01163_b200 as pb
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-
-    cid = args.config
     mesh, iters = pb.baseline_mesh(cid)
     prob = pb.baseline_problem(cid, args.seed + rank)  # replicas: independent problems per rank
     t0 = time.time()
     ctx = pb.SolverContext(mesh, prob)
     setup_s = time.time() - t0
     ndof = ctx.fine_size()
+    assert [list(mesh.fine_counts), list(mesh.coarse_counts), iters] == [*MESHES[cid], ITERATIONS[cid]]
     opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=args.seed)
     lib = pb.load_library()
     lib.asdsm_plan_stream.restype = ctypes.c_void_p
@@ -230,7 +285,6 @@ def main():
     stream = torch.cuda.Stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
     copt = opts._c()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def flush_l2(s):
         with torch.cuda.stream(s):
@@ -239,7 +293,7 @@ def main():
     def step():
         pb.asdsm._check(lib.asdsm_iterate_async(ctx._h, ctypes.byref(copt), sp))
 
-    for _ in range(max(args.warmup, 0)):
+    for _ in range(max(warmup, 0)):
         flush_l2(stream)
         step()
     torch.cuda.synchronize()
@@ -249,7 +303,7 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush_l2(stream)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -261,6 +315,7 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = ctx.launch_count()
+    kernels = ctx.kernels()
     ms = max_over_ranks(float(np.mean(times)), "cuda")
     value = world * ndof * iters / (ms / 1e3)
 
@@ -290,38 +345,30 @@ def main():
              "gbs": cby[i] / (cms[i] / 1e3) / 1e9 if cms[i] > 0 else None,
              "tflops": cfl[i] / (cms[i] / 1e3) / 1e12 if cms[i] > 0 and cfl[i] > 0 else None}
         comps.append(c)
-    # Rooflines.  The headline object is the fine-grid residual/update pass (north-star kernels 1
-    # and 4, the HBM-bound pass the >= 60 % target is stated for); every component gets its own
-    # entry in roofline_components, and the dominant kernel of the step is named with its bound
-    # (kernels that move < 1 MB per launch and do no GEMM work are latency bound: no roofline).
+
     def roof_of(c):
+        share = c["ms_per_launch"] * c["launches_per_solve"] / ms
         if c["flops_per_launch"] > 0 and c["flops_per_launch"] / max(c["bytes_per_launch"], 1) > FP64_PEAK_TFLOPS * 1e3 / hbm:
             ach = c["flops_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e12
             return {"kernel": c["name"], "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
-                    "peak_source": "fp64 DMMA/DFMA peak measured with scripts/probe_fp64.cu (MEASURED_PEAKS has no fp64)"}
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None, "share_of_step": share,
+                    "peak_source": "fp64 DMMA/DFMA peak measured with scripts/probe_fp64.cu (MEASURED_PEAKS has no "
+                                   "fp64); flops are dense-equivalent (the even/odd split executes half)"}
         if c["bytes_per_launch"] < 1e6:
             return {"kernel": c["name"], "bound": "latency", "achieved": None, "peak": None, "unit": None,
-                    "frac": None, "traffic": None,
+                    "frac": None, "traffic": None, "share_of_step": share,
                     "note": "under 1 MB per launch on a handful of SMs: dependency-chain latency, not bandwidth"}
         ach = c["bytes_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e9
+        tr = ncu_traffic(cid, c["name"], kernels)
         return {"kernel": c["name"], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": ncu_traffic(cid, c["name"]), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+                "frac": ach / hbm, "traffic": tr["bytes"] if tr else None,
+                "traffic_source": tr, "share_of_step": share,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
-    cand = [c for c in comps if c["name"] not in ("step_dots_overhead",)]
-    # the fine-grid update pass as the step runs it: fused with the step dots where it applies
-    upd = next((c for c in comps if c["name"] == "dots_update"),
-               next((c for c in comps if c["name"] == "update_residual"), cand[0]))
-    roof = roof_of(upd)
-    roof["share_of_step"] = upd["ms_per_launch"] * upd["launches_per_solve"] / ms
+    cand = [c for c in comps if c["launches_per_solve"] > 0]
     dom = max(cand, key=lambda c: c["ms_per_launch"] * c["launches_per_solve"])
-    roof_dom = roof_of(dom)
-    roof_dom["share_of_step"] = dom["ms_per_launch"] * dom["launches_per_solve"] / ms
-    roof_all = []
-    for c in cand:
-        r = roof_of(c)
-        roof_all.append({"kernel": c["name"], "bound": r["bound"], "achieved": r["achieved"], "unit": r["unit"],
-                         "frac": r["frac"], "share_of_step": c["ms_per_launch"] * c["launches_per_solve"] / ms})
+    roof_all = [roof_of(c) for c in cand]
+    roof_hbm = [r for r in roof_all if r["kernel"] in HBM_COMPONENTS]
 
     # ---- e2e through the C-ABI with pinned host buffers
     b = ctx.bundle
@@ -344,11 +391,11 @@ def main():
                                         dp(h_exact) if h_exact is not None else None, ctypes.byref(copt),
                                         dp(h_hist), ctypes.byref(nrec), ctypes.byref(stop), dp(h_u), dp(h_r)))
 
-    for _ in range(max(args.warmup, 5)):
+    for _ in range(max(warmup, 3)):
         flush_l2(pstream)
         e2e_step()
     etimes = []
-    for _ in range(max(args.steps, 10)):
+    for _ in range(max(steps, 5)):
         flush_l2(pstream)
         a = torch.cuda.Event(enable_timing=True)
         bb = torch.cuda.Event(enable_timing=True)
@@ -363,70 +410,95 @@ def main():
     e2e = {"value": world * ndof * iters / (ems / 1e3), "unit": "DOF-iter/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "ms_per_step": ems, "steps": len(etimes),
            "ms_all": [round(t, 4) for t in etimes]}
-    assert np.allclose(h_u.numpy(), h_u.numpy())  # touch the result
+    if not np.isfinite(h_u.numpy()).all():
+        raise RuntimeError("non-finite solution")
 
-    # ---- CPU baseline: the compiled reference on this box's host cores (rank 0, N=1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_DUMP) and ndof <= 2_000_000:
-        tcpu, _ = reference_solve(cid, args.seed, iters)
-        cpu = {"value": ndof * iters / tcpu, "unit": "DOF-iter/s", "cores": os.cpu_count(), "kind": "reference",
-               "sample": f"one full solve ({iters} iterations + initial guess) of the same problem by the reference's "
-                         "own code (oracle/_ref, Eigen stand-in), hole solves on all host threads, setup excluded",
-               "seconds": tcpu}
+    out = {
+        "value": value, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+        "config": config_dict(cid, world),
+        "e2e": e2e, "roofline": roof_of(dom), "roofline_hbm": roof_hbm, "roofline_components": roof_all,
+        "gpu_launches": launches, "kernels": kernels, "clocks": clocks, "components": comps, "setup_s": setup_s,
+        "res_l2_first_last": [float(res[0]), float(res[-1])], "step_ms_all": times,
+    }
+    del ctx
+    torch.cuda.synchronize()
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    sys.path.insert(0, ROOT)
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    cid = args.config
+    head = measure_config(cid, args, world, rank, local, flush, args.steps, args.warmup)
+    per = {}
+    if args.per_config and world == 1:
+        only = [int(x) for x in args.only.split(",")] if args.only else range(len(CONFIG_NAMES))
+        for c in only:
+            per[c] = head if c == cid else measure_config(c, args, world, rank, local, flush,
+                                                          max(3, min(args.steps, 5)), max(args.warmup, 3))
+
+    # ---- CPU baseline: the compiled reference on this box's host cores (rank 0, N=1), after
+    # every GPU measurement (nothing else runs on the host while it is timed)
+    cpu = {}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_DUMP):
+        for c in ([cid] + [c for c in per if c != cid]):
+            v, det = reference_sample(c, args.seed)
+            cpu[c] = {"value": v, "unit": "DOF-iter/s", "cores": os.cpu_count(), "kind": "reference",
+                      "sample": CPU_SAMPLE[c][3] + "; the reference's own C++ (oracle/_ref, Eigen SparseLU stand-in: "
+                                "RCM + band LU), hole solves threaded, context setup excluded", "detail": det}
 
     line = {
         "metric": "fine-grid DOF-iterations/sec",
-        "value": value,
+        "value": head["value"],
         "unit": "DOF-iter/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms,
+        "ms_per_step": head["ms_per_step"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": f"synthetic (seeded, BASELINE.json config {cid})",
-        "config": {"workload": CONFIG_NAMES[cid], "config_id": cid, "fine_counts": mesh.fine_counts,
-                   "coarse_counts": mesh.coarse_counts, "iterations": iters, "dof": ndof,
-                   "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1gpu"},
-        "e2e": e2e,
-        "roofline": roof,
-        "roofline_dominant": roof_dom,
-        "roofline_components": roof_all,
-        "cpu_baseline": cpu,
-        "gpu_launches": launches,
-        "clocks": clocks,
-        "components": comps,
-        "setup_s": setup_s,
-        "res_l2_first_last": [float(res[0]), float(res[-1])],
-        "step_ms_all": times,
+        "config": head["config"],
+        "e2e": head["e2e"],
+        "roofline": head["roofline"],
+        "roofline_hbm": head["roofline_hbm"],
+        "roofline_components": head["roofline_components"],
+        "cpu_baseline": cpu.get(cid),
+        "gpu_launches": head["gpu_launches"],
+        "clocks": head["clocks"],
+        "kernels": head["kernels"],
+        "components": head["components"],
+        "setup_s": head["setup_s"],
+        "res_l2_first_last": head["res_l2_first_last"],
+        "step_ms_all": head["step_ms_all"],
     }
-    if args.all_configs and rank == 0:
-        others = {}
-        for c2 in range(len(CONFIG_NAMES)):
-            m2, it2 = pb.baseline_mesh(c2)
-            ctx2 = pb.SolverContext(m2, pb.baseline_problem(c2, args.seed))
-            o2 = pb.IterateOptions(tol=0.0, max_iter=it2, stagnation_window=0, rng_seed=args.seed)._c()
-            for _ in range(2):
-                pb.asdsm._check(lib.asdsm_iterate_async(ctx2._h, ctypes.byref(o2), sp))
-            torch.cuda.synchronize()
-            tt = []
-            for _ in range(3):
-                flush_l2(stream)
-                a = torch.cuda.Event(enable_timing=True)
-                bb = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                pb.asdsm._check(lib.asdsm_iterate_async(ctx2._h, ctypes.byref(o2), sp))
-                bb.record(stream)
-                bb.synchronize()
-                tt.append(a.elapsed_time(bb))
-            m_ = float(np.mean(tt))
-            others[CONFIG_NAMES[c2]] = {"ms_per_step": m_, "value": ctx2.fine_size() * it2 / (m_ / 1e3),
-                                        "dof": ctx2.fine_size(), "iterations": it2}
-            del ctx2
-        line["all_configs"] = others
+    if per:
+        pc = []
+        for c, r in per.items():
+            e = {k: r[k] for k in ("config", "value", "ms_per_step", "steps", "warmup", "e2e", "roofline",
+                                   "roofline_hbm", "gpu_launches", "clocks", "res_l2_first_last")}
+            e["e2e"] = {k: v for k, v in e["e2e"].items() if k != "ms_all"}
+            e["cpu_baseline"] = cpu.get(c)
+            if c != cid:
+                e["roofline_components"] = r["roofline_components"]
+            pc.append(e)
+        line["per_config"] = pc
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

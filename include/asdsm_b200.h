@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define ASDSM_B200_ABI_VERSION 2
+#define ASDSM_B200_ABI_VERSION 3
 
 /* Status codes <-> errors.hpp exception classes. */
 enum asdsm_status {
@@ -98,9 +98,16 @@ int asdsm_point_count(const asdsm_plan* plan, unsigned coarse_mask, int holes, i
 int asdsm_projector_map(asdsm_plan* plan, unsigned from_mask, unsigned to_mask, int to_holes, int64_t* out);
 
 /* RhsBundle (solver.hpp:37-42) + optional exact samples (nullable); host or device memory.
- * b_slab[a] lives on the kind coarse along axis a. */
+ * b_slab[a] lives on the kind coarse along axis a.  Returns after the copies completed; device
+ * sources must be complete when it is called (synchronize their producer first). */
 int asdsm_set_bundle(asdsm_plan* plan, const double* b_fine, const double* const* b_slab,
                      const double* b_coarse, const double* exact, int on_device);
+/* Same, enqueued on `stream` (cudaStream_t as void*, NULL = the plan's stream) without a host
+ * synchronize: ordered after the caller's producer work on `stream` and before a following
+ * asdsm_iterate_async on the same stream.  Host sources must stay valid (and pinned for
+ * overlap) until the stream reaches the copies. */
+int asdsm_set_bundle_async(asdsm_plan* plan, const double* b_fine, const double* const* b_slab,
+                           const double* b_coarse, const double* exact, int on_device, void* stream);
 
 /* asdsm_iterate (solver.hpp:161-163).  Host outputs (all nullable): history rows of
  * (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms), the final iterate u and residual r. */
@@ -122,6 +129,9 @@ int asdsm_fetch(asdsm_plan* plan, void* stream, double* history, int* nrec, int*
 int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev);
 /* Kernels this library launched during the last iterate call. */
 int64_t asdsm_last_launch_count(const asdsm_plan* plan);
+/* The kernels of the plan's captured solve graph: "name<TAB>nodes<NEWLINE>" per kernel
+ * (demangled), NUL-terminated, truncated to len-1 bytes.  Empty before the first graph solve. */
+int asdsm_plan_kernels(const asdsm_plan* plan, char* buf, int64_t len);
 
 /* The plan's own stream (cudaStream_t as void*). */
 void* asdsm_plan_stream(asdsm_plan* plan);

@@ -274,7 +274,7 @@ class SolverContext {
     IterationState st;
     st.u.resize(n);
     st.r.resize(n);
-    std::vector<double> hist(7 * static_cast<size_t>(o.max_iter + 1));
+    std::vector<double> hist(7 * (static_cast<size_t>(std::max(o.max_iter, 0)) + 1));
     int nrec = 0, stop = 0;
     if (b) {
       const double* slabs[3] = {nullptr, nullptr, nullptr};

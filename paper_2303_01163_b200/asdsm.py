@@ -129,12 +129,14 @@ def load_library():
         "asdsm_point_count": (I, [P, ctypes.c_uint, I, I64]),
         "asdsm_projector_map": (I, [P, ctypes.c_uint, ctypes.c_uint, I, I64]),
         "asdsm_set_bundle": (I, [P, D, ctypes.POINTER(D), D, D, I]),
+        "asdsm_set_bundle_async": (I, [P, D, ctypes.POINTER(D), D, D, I, P]),
         "asdsm_iterate": (I, [P, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_iterate_async": (I, [P, ctypes.POINTER(_Options), P]),
         "asdsm_fetch": (I, [P, P, D, IP, IP, D, D]),
         "asdsm_solve": (I, [P, D, ctypes.POINTER(D), D, D, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_device_solution": (I, [P, P, ctypes.POINTER(ctypes.c_void_p)]),
         "asdsm_last_launch_count": (ctypes.c_int64, [P]),
+        "asdsm_plan_kernels": (I, [P, ctypes.c_char_p, ctypes.c_int64]),
         "asdsm_residual": (I, [P, D, D, D]),
         "asdsm_initial_guess": (I, [P, D]),
         "asdsm_error_guess": (I, [P, D, ctypes.c_uint64, D]),
@@ -500,6 +502,16 @@ class SolverContext:
 
     def launch_count(self) -> int:
         return int(self._lib.asdsm_last_launch_count(self._h))
+
+    def kernels(self) -> dict:
+        """{demangled kernel name: graph nodes} of the last captured solve graph."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(self._lib.asdsm_plan_kernels(self._h, buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, _, n = line.rpartition("\t")
+            out[name] = int(n)
+        return out
 
     def projector_map(self, from_kind: MeshKind, to_kind: MeshKind) -> np.ndarray:
         return build_projector(self.config, from_kind, to_kind, plan=self)

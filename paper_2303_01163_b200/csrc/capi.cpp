@@ -220,8 +220,21 @@ int asdsm_projector_map(asdsm_plan* plan, unsigned from_mask, unsigned to_mask, 
 int asdsm_set_bundle(asdsm_plan* plan, const double* b_fine, const double* const* b_slab, const double* b_coarse,
                      const double* exact, int on_device) {
   return guarded([&] {
+    // synchronous in both cases: host buffers are free again, and device copies are complete
+    // before any later call on any stream reads the bundle (the caller's producer of device
+    // sources must have finished: synchronize it, or use asdsm_set_bundle_async on that stream)
     plan->solver->set_bundle(b_fine, b_slab, b_coarse, exact, on_device != 0, plan->stream);
-    if (!on_device) ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_set_bundle_async(asdsm_plan* plan, const double* b_fine, const double* const* b_slab,
+                           const double* b_coarse, const double* exact, int on_device, void* stream) {
+  return guarded([&] {
+    // stream-ordered: after the caller's producer work on `stream`, before its next
+    // asdsm_iterate_async on `stream`
+    plan->solver->set_bundle(b_fine, b_slab, b_coarse, exact, on_device != 0,
+                             stream ? as_stream(stream) : plan->stream);
   });
 }
 
@@ -284,6 +297,18 @@ int asdsm_device_solution(asdsm_plan* plan, void* stream, const double** u_dev) 
 }
 
 int64_t asdsm_last_launch_count(const asdsm_plan* plan) { return plan->solver->last_launches(); }
+
+int asdsm_plan_kernels(const asdsm_plan* plan, char* buf, int64_t len) {
+  return guarded([&] {
+    std::string s;
+    for (const auto& k : plan->solver->graph_kernels()) s += k.first + "\t" + std::to_string(k.second) + "\n";
+    if (buf && len > 0) {
+      const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(len - 1));
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
 
 void* asdsm_plan_stream(asdsm_plan* plan) { return plan->stream; }
 

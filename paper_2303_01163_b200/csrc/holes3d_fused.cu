@@ -665,7 +665,7 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     const int nring = 2 * (mx + my);
     L.faces = static_cast<int>(off);
     int tc = 0;
-    static const int tc_max = std::getenv("ASDSM_H3_TC") ? std::atoi(std::getenv("ASDSM_H3_TC")) : 8;
+    const int tc_max = std::getenv("ASDSM_H3_TC") ? std::atoi(std::getenv("ASDSM_H3_TC")) : 8;
     // Among the chunk sizes that fit, the one with the least modelled time: per chunk the
     // step-A rounds (8-row blocks over 16 warps), the step-B rounds ((plane, j tile, n quad)
     // tasks over 16 warps) and a fixed per-chunk cost (ring transforms, barriers), in the

@@ -513,7 +513,7 @@ void launch_publish(DevState* state, double* u0, const double* u1, double* r0, c
 // 1.37 ms) but costs inside the captured graph (1.28 -> 1.32 ms), which is the faster of the
 // two -- so it is opt-in (ASDSM_PDL=1)
 bool pdl_enabled() {
-  static const bool on = std::getenv("ASDSM_PDL") != nullptr;
+  const bool on = std::getenv("ASDSM_PDL") != nullptr;
   return on;
 }
 

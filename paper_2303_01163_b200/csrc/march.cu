@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(TX3 * TY3) march3d_kernel(MarchArgs A) {
           a2 += acc * acc;
         } else {
           double r = __dsub_rn(bq, acc);
-          if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0) r = 0.0;
+          if (MODE == kMarchUpdate && A.sparse && (x + 1) % A.n[0] != 0 && (y + 1) % A.n[1] != 0 && (z + 1) % A.n[2] != 0)
+            r = 0.0;
           ro[p] = r;
           if (MODE == kMarchUpdate) uo[p] = vc;
           a0 += r * r;
@@ -656,8 +657,8 @@ bool dots_update_supported(const FineGeom& g) {
 
 void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   MarchArgs A = A0;
-  static const bool no_prefetch = std::getenv("ASDSM_NO_TILE_PREFETCH") != nullptr;
-  static const int dist = std::getenv("ASDSM_PREFETCH_DIST") ? std::atoi(std::getenv("ASDSM_PREFETCH_DIST")) : 1;
+  const bool no_prefetch = std::getenv("ASDSM_NO_TILE_PREFETCH") != nullptr;
+  const int dist = std::getenv("ASDSM_PREFETCH_DIST") ? std::atoi(std::getenv("ASDSM_PREFETCH_DIST")) : 1;
   A.prefetch = no_prefetch ? 0 : dist;
   A.strip = march_strip(A.g);
   const unsigned nb = march_blocks(A.g);
@@ -689,7 +690,7 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     cfg.numAttrs = 1;
     ASDSM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, dots_update2d_kernel<kYc>, A));
   } else if (A.g.dim == 3 && mode == kMarchDots && A.skel_only) {
-    static const bool by_point = std::getenv("ASDSM_SKEL3D_POINTS") != nullptr;
+    const bool by_point = std::getenv("ASDSM_SKEL3D_POINTS") != nullptr;
     if (by_point) {
       if (var) skel3d_dots_kernel<true><<<4 * kNumSms, 256, 0, s>>>(A);
       else skel3d_dots_kernel<false><<<4 * kNumSms, 256, 0, s>>>(A);
@@ -707,8 +708,8 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     // CTA walks ~2 tiles (config 1) and L2-prefetches the next one -- config 1 update pass 18.0 ->
     // 15.0 us, config 2 245 -> 153 us against 8-row segments (80 registers with the prefetch:
     // three CTAs per SM, a second wave at config 1); ASDSM_YC / ASDSM_YC_CPS override
-    static const int yc_env = std::getenv("ASDSM_YC") ? std::atoi(std::getenv("ASDSM_YC")) : 4;
-    static const int cps = std::getenv("ASDSM_YC_CPS") ? std::atoi(std::getenv("ASDSM_YC_CPS")) : 4;
+    const int yc_env = std::getenv("ASDSM_YC") ? std::atoi(std::getenv("ASDSM_YC")) : 4;
+    const int cps = std::getenv("ASDSM_YC_CPS") ? std::atoi(std::getenv("ASDSM_YC_CPS")) : 4;
     const int kYc = yc_env == 8 ? 8 : (yc_env == 2 ? 2 : 4);
     const long long tiles = static_cast<long long>((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 8 * kYc - 1) / (8 * kYc));
     const unsigned nb2 = static_cast<unsigned>(std::min<long long>(tiles, static_cast<long long>(cps) * kNumSms));

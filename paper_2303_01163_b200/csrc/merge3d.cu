@@ -487,7 +487,7 @@ void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_
     nl3 = std::max(nl3, m.nc[a] * m.nf[f1]);
     ns = std::max(ns, static_cast<i64>(m.nc[a]) * m.nf[f1] * m.nf[f2]);
   }
-  static const bool per_thread = std::getenv("ASDSM_M3_THREAD_LINES") != nullptr;
+  const bool per_thread = std::getenv("ASDSM_M3_THREAD_LINES") != nullptr;
   bool warp_ok = !per_thread;
   for (int q = 0; q < 3; ++q) warp_ok = warp_ok && m.nc[q] + 2 <= kWarpKnots;
   if (warp_ok) {

@@ -414,7 +414,7 @@ void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const Bo
   TOut* op = reinterpret_cast<TOut*>(out.ptr);
   if constexpr (std::is_same<TIn, double>::value && std::is_same<TMat, double>::value &&
                 std::is_same<TOut, double>::value) {
-    static const bool scalar = std::getenv("ASDSM_SCALAR_GEMM") != nullptr;
+    const bool scalar = std::getenv("ASDSM_SCALAR_GEMM") != nullptr;
     if (m <= kSmallModes && M.nlines < (1LL << 31) && std::getenv("ASDSM_NO_SMALL_TRANSFORM") == nullptr) {
       const i64 nb = std::min<i64>((M.nlines + 255) / 256, 16LL * kNumSms);
       small_transform_kernel<<<static_cast<unsigned>(nb), 256, 0, st>>>(ip, op, mat, m, in.stride[axis], out.stride[axis], M);

@@ -1,4 +1,6 @@
 #include <cstdio>
+#include <cxxabi.h>
+#include <map>
 // Host orchestration of one ASDSM solve on the device (proj/src/solver.cpp:486-680 restated
 // for a device-resident state).  All per-iteration decisions (normalization guard, step
 // clamp, accept/revert, stop rules) happen in ctrl kernels, so a whole solve is enqueued
@@ -19,6 +21,9 @@
 #include <random>
 
 namespace asdsm_b200 {
+
+static void record_graph_kernels(cudaGraph_t g, std::vector<std::pair<std::string, int>>& out);
+
 
 std::uint64_t mix_seed(std::uint64_t base, std::uint64_t k) {
   std::uint64_t z = base + 0x9E3779B97F4A7C15ull * (k + 1);
@@ -435,7 +440,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     solve_box(4, e, s);
     return;
   }
-  static const bool generic = std::getenv("ASDSM_GENERIC_FILL") != nullptr;
+  const bool generic = std::getenv("ASDSM_GENERIC_FILL") != nullptr;
   const SepSolver& H = sep_hole_;
   if (!generic && mesh_.dim == 2 && !H.complex_modes && H.nd == 1 && H.L == 1 && !H.use_pcr) {
     // One fused kernel per hole (holes2d.cu) in both modes; for larger holes in error mode: ring
@@ -452,7 +457,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nbox1 = mesh_.nc[1] + 1;
     // (a variant staging every table slice in shared memory first measured slower: its time
     // goes into a dependent shared-store chain; kept available as tables_in_smem)
-    static const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
+    const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
     hole2d_prepare(113 * 1024);
     A.kb = 32;
     A.tables_in_smem = (staged && hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 113 * 1024) ? 1 : 0;
@@ -471,7 +476,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.cp = H.th_cp;
     A.line_left = H.line_left;
     A.line_right = H.line_right;
-    static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
+    const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
     if (ring_from_lines_) {  // the slab step left the skeleton to the holes (fused kernel only)
       A.skel_line0 = skel_line_[0];
       A.skel_line1 = skel_line_[1];
@@ -497,7 +502,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     A.nf1 = mesh_.nf[1];
     A.nbox0 = mesh_.nc[0] + 1;
     A.nbox1 = mesh_.nc[1] + 1;
-    static const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
+    const bool staged = std::getenv("ASDSM_HOLE_STAGED") != nullptr;
     A.kb = 32;
     A.tables_in_smem = (staged && hole2d_smem_bytes(A.m0, A.m1, A.kb, true, true) <= 113 * 1024) ? 1 : 0;
     if (!A.tables_in_smem) {
@@ -518,7 +523,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     double* modes = static_cast<double*>(scratch0_);
     // one warp per mode line with the partition method (measured, config 2: see DESIGN), else
     // one thread per mode line (Thomas)
-    static const bool thomas = std::getenv("ASDSM_HOLE_THOMAS") != nullptr;
+    const bool thomas = std::getenv("ASDSM_HOLE_THOMAS") != nullptr;
     const bool part = !thomas && H.part && hole2d_part_supported(H.part_seg) && hole_ring_;
     if (part) {
       Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
@@ -798,7 +803,7 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
     ASDSM_CUDA_CHECK(cudaMemcpyAsync(sub_rows_, all.data(), all.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
   }
 
-  static const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
+  const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
   if (no_graph || s == nullptr) {
     const long long l0 = g_kernel_launches;
     enqueue_run(o, s);
@@ -808,7 +813,7 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
   const bool same = graph_exec_ && graph_opts_.tol == o.tol && graph_opts_.max_iter == o.max_iter &&
                     graph_opts_.stagnation_window == o.stagnation_window &&
                     graph_opts_.stagnation_ratio == o.stagnation_ratio && graph_opts_.subsample == o.subsample &&
-                    graph_opts_.sparse_residual == o.sparse_residual;
+                    graph_opts_.sparse_residual == o.sparse_residual && graph_has_exact_ == has_exact_;
   if (!same) {
     if (graph_exec_) {
       cudaGraphExecDestroy(graph_exec_);
@@ -826,13 +831,52 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
     }
     ASDSM_CUDA_CHECK(cudaStreamEndCapture(s, &g));
     graph_launches_ = g_kernel_launches - l0;
+    record_graph_kernels(g, graph_kernels_);
     const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
     cudaGraphDestroy(g);
     ASDSM_CUDA_CHECK(e);
     graph_opts_ = o;
+    graph_has_exact_ = has_exact_;
   }
   ASDSM_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
   launches_ = graph_launches_;
+}
+
+// Demangled names of the kernel nodes of a captured graph, with their multiplicity.
+static void record_graph_kernels(cudaGraph_t g, std::vector<std::pair<std::string, int>>& out) {
+  out.clear();
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return;
+  std::map<std::string, int> count;
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams p{};
+    if (cudaGraphKernelNodeGetParams(node, &p) != cudaSuccess) continue;
+    const char* mangled = nullptr;
+    if (cudaFuncGetName(&mangled, p.func) != cudaSuccess || !mangled) continue;
+    int status = 0;
+    char* dem = abi::__cxa_demangle(mangled, nullptr, nullptr, &status);
+    std::string name = status == 0 && dem ? std::string(dem) : std::string(mangled);
+    std::free(dem);
+    for (size_t q; (q = name.find("(anonymous namespace)::")) != std::string::npos;) name.erase(q, 23);
+    if (name.rfind("void ", 0) == 0) name = name.substr(5);
+    // drop the parameter list: the first '(' outside the template argument list
+    int depth = 0;
+    for (size_t q = 0; q < name.size(); ++q) {
+      if (name[q] == '<') ++depth;
+      else if (name[q] == '>') --depth;
+      else if (name[q] == '(' && depth == 0) {
+        name.resize(q);
+        break;
+      }
+    }
+    ++count[name];
+  }
+  cudaGetLastError();
+  out.assign(count.begin(), count.end());
 }
 
 void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
@@ -1152,7 +1196,7 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     A.cp = H.th_cp;
     A.line_left = H.line_left;
     A.line_right = H.line_right;
-    static const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
+    const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
     if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
       // one kernel: ring rhs, sweeps, DMMA back transform (writes the hole interior once)
       timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * static_cast<double>(NH), iters,

@@ -85,6 +85,9 @@ class Solver {
 
   // Launch count of the last run() (kernels of this library only).
   long long last_launches() const { return launches_; }
+  // Kernels of the captured solve graph (demangled name, node count), from the graph's own
+  // kernel nodes: what a solve actually launches (tests assert the intended variant ran).
+  const std::vector<std::pair<std::string, int>>& graph_kernels() const { return graph_kernels_; }
   ~Solver();
 
  private:
@@ -171,6 +174,8 @@ class Solver {
   long long launches_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;
   RunOptions graph_opts_{};
+  bool graph_has_exact_ = false;
+  std::vector<std::pair<std::string, int>> graph_kernels_;  // CtrlArgs.has_exact and the exact_ pointer are baked into the graph
   long long graph_launches_ = 0;
 };
 

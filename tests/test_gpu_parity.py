@@ -3,19 +3,17 @@
 Tolerances:
   * index maps, residual evaluation: bit-exact.
   * initial guess / final solution: max-norm relative 1e-10.
-  * per-iteration residual norms: |d res_k| <= max(1e-10 * res_k, 10 * spread_k * res_k,
-    eps * || |A| |u| ||_2), where spread_k is the reference's own reproducibility floor up to
-    iteration k (relative spread of its history when re-run with a different, equally valid
-    fill ordering of its direct solver: Cuthill-McKee instead of reverse Cuthill-McKee), and
-    the last term is the fp64 evaluation floor of b - A u itself (no two implementations
-    whose iterates differ in the last bit can agree on the residual more closely).
+  * per-iteration residual norms: |d res_k| <= res_k * max(1e-10, 10 * spread_k), where
+    spread_k is the reference's own reproducibility floor up to iteration k (relative spread of
+    its history when re-run with a different, equally valid fill ordering of its direct solver:
+    Cuthill-McKee instead of reverse Cuthill-McKee; ref_tools.history_tolerance).
 """
 import numpy as np
 import pytest
 
 import paper_2303_01163_b200 as pb
-from ref_tools import (csr_residual_exact, eval_floor, have_ref, ref_bundle, ref_error_guess, ref_iterate,
-                       ref_maps)
+from ref_tools import (csr_residual_exact, have_ref, history_tolerance, ref_bundle, ref_error_guess, ref_iterate,
+                       ref_iterate_pair, ref_maps)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")]
 
@@ -86,13 +84,26 @@ def test_error_guess_and_scaling(spec, nf, nc, seed):
     assert abs(s - s_ref) <= 1e-10 * abs(s_ref)
 
 
-def _rel_floor(spec, nf, nc, iters, seed, ref):
-    """Reference reproducibility floor: relative spread of its own residual history between two
-    equally valid fill orderings of its direct solver, made non-decreasing in k (rounding
-    differences, once present, propagate through the iteration)."""
-    alt = ref_iterate(spec, nf, nc, iters, seed, env={"ASDSM_STUB_ORDER": "cm"})
+def check_history(st, ref, alts):
+    """GPU history and final iterate against the reference run `ref` (alts: the same run under
+    other fill orderings, for the reproducibility floor)."""
+    got = np.array([h.res_l2 for h in st.history])
     want = ref["hist"][:, 1]
-    return np.maximum.accumulate(np.abs(alt["hist"][:, 1] - want) / want)
+    assert len(got) == len(want)
+    tol = history_tolerance(ref, alts)
+    bad = np.abs(got - want) > tol
+    assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
+    s_got = np.array([h.s_hat for h in st.history[1:]])
+    assert np.array_equal(s_got == 0.0, ref["hist"][1:, 5] == 0.0)  # same accept/revert decisions
+    scale = np.max(np.abs(ref["u"]))
+    assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * scale
+    return float(np.max(np.abs(got - want) / want)), float(np.max(np.abs(st.u - ref["u"])) / scale)
+
+
+def assert_variant_ran(ctx_a, ctx_b):
+    """Two plans of an A/B test really launched different kernels (the switch took effect)."""
+    ka, kb = ctx_a.kernels(), ctx_b.kernels()
+    assert ka and kb and set(ka) != set(kb), (sorted(ka), sorted(kb))
 
 
 @pytest.mark.parametrize("spec,nf,nc,iters,seed", [
@@ -106,19 +117,9 @@ def _rel_floor(spec, nf, nc, iters, seed, ref):
 ])
 def test_iterate_history(spec, nf, nc, iters, seed):
     ctx, mesh, _ = _ctx(spec, nf, nc)
-    ref = ref_iterate(spec, nf, nc, iters, seed)
+    ref, alts = ref_iterate_pair(spec, nf, nc, iters, seed)
     st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=seed))
-    got = np.array([h.res_l2 for h in st.history])
-    want = ref["hist"][:, 1]
-    assert len(got) == len(want)
-    tol = np.maximum(want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, seed, ref)),
-                     eval_floor(ref_bundle(spec, nf, nc), ref["u"]))
-    bad = np.abs(got - want) > tol
-    assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
-    s_got = np.array([h.s_hat for h in st.history[1:]])
-    assert np.array_equal(s_got == 0.0, ref["hist"][1:, 5] == 0.0)  # same accept/revert decisions
-    scale = np.max(np.abs(ref["u"]))
-    assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * scale
+    check_history(st, ref, alts)
 
 
 @pytest.mark.parametrize("spec,nf,nc", [("ex:4:1", 24, 4), ("cfg:3:0", 29, 4), ("cfg:4:3", 29, 4)])
@@ -151,18 +152,12 @@ def test_variable_coefficients_match_reference(spec, nf, nc, iters):
     rng = np.random.default_rng(3)
     u = rng.standard_normal(ctx.fine_size())
     assert np.array_equal(ctx.residual(u), csr_residual_exact(bun, u))  # per-point stencil, bitwise
-    ref = ref_iterate(spec, nf, nc, iters, 0)
+    ref, alts = ref_iterate_pair(spec, nf, nc, iters, 0)
     st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=0))
-    got = np.array([h.res_l2 for h in st.history])
-    want = ref["hist"][:, 1]
-    tol = np.maximum(want * np.maximum(1e-10, 10.0 * _rel_floor(spec, nf, nc, iters, 0, ref)), eval_floor(bun, ref["u"]))
-    bad = np.abs(got - want) > tol
-    assert not bad.any(), list(zip(np.nonzero(bad)[0], got[bad], want[bad], tol[bad]))
-    assert np.array_equal(np.array([h.s_hat for h in st.history[1:]]) == 0.0, ref["hist"][1:, 5] == 0.0)
-    assert np.max(np.abs(st.u - ref["u"])) <= 1e-10 * np.max(np.abs(ref["u"]))
+    check_history(st, ref, alts)
 
 
-@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:1:0", 0, 0, 20), ("cfg:0:0", 0, 0, 10), ("ex:3:1", 199, 9, 20)])
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:1:0", 0, 0, 20), ("cfg:1:2", 999, 9, 10)])
 def test_slab_step_kernels_agree(spec, nf, nc, iters, monkeypatch):
     """The one-launch 2D slab step (slabstep2d.cu: partitioned warp line solves, DSMEM cross
     values, reciprocal-multiply normalization) against the three-launch path (PCR slab solves,
@@ -174,6 +169,7 @@ def test_slab_step_kernels_agree(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_NO_SLABSTEP", "1")
     ctx_old, _, _ = _ctx(spec, nf, nc)
     st_old = ctx_old.iterate(opts)
+    assert_variant_ran(ctx, ctx_old)
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
     assert len(a) == len(b)
@@ -198,6 +194,7 @@ def test_even_odd_transforms_agree(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_DENSE_GEMM", "1")
     ctx_d, _, _ = _ctx(spec, nf, nc)
     st_d = ctx_d.iterate(opts)
+    assert_variant_ran(ctx, ctx_d)
     a = np.array([h.res_l2 for h in st_eo.history])
     b = np.array([h.res_l2 for h in st_d.history])
     assert len(a) == len(b)
@@ -205,12 +202,12 @@ def test_even_odd_transforms_agree(spec, nf, nc, iters, monkeypatch):
     assert np.max(np.abs(st_eo.u - st_d.u)) <= 1e-6 * np.max(np.abs(st_d.u))
 
 
-@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 6), ("cfg:3:0", 29, 4, 6), ("cfg:3:0", 79, 4, 4),
-                                              ("cfg:4:1", 99, 4, 5), ("cfg:4:1", 254, 4, 3), ("cfg:4:3", 29, 4, 6)])
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 6), ("cfg:3:0", 79, 4, 4),
+                                              ("cfg:4:1", 99, 4, 5), ("cfg:4:1", 254, 4, 3)])
 def test_fused_hole3d_fill_agrees(spec, nf, nc, iters, monkeypatch):
     """The one-kernel 3D hole fill (holes3d_fused.cu: faces, line solves and both DMMA back
     transforms per hole in shared memory; SYM schedule for the steady configs, CAUSAL plane
-    streaming for the space-time ones, m = 5 ... 50) against the four-launch path (faces kernel,
+    streaming for the space-time ones, m = 15 ... 50) against the four-launch path (faces kernel,
     Thomas kernel, two dense transform GEMMs).  One error guess must agree to rounding; the
     iteration amplifies last-bit differences, so its bound only has to catch a wrong fill."""
     ctx, _, _ = _ctx(spec, nf, nc)
@@ -223,6 +220,7 @@ def test_fused_hole3d_fill_agrees(spec, nf, nc, iters, monkeypatch):
     ctx_o, _, _ = _ctx(spec, nf, nc)
     e_old = ctx_o.error_guess(r, 7)
     st_old = ctx_o.iterate(opts)
+    assert_variant_ran(ctx, ctx_o)
     assert np.max(np.abs(e_new - e_old)) <= 1e-12 * np.max(np.abs(e_old))
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
@@ -246,6 +244,7 @@ def test_partitioned_slab_lines_agree(spec, nf, nc, iters, monkeypatch):
     ctx_o, _, _ = _ctx(spec, nf, nc)
     e_old = ctx_o.error_guess(r, 3)
     st_old = ctx_o.iterate(opts)
+    assert_variant_ran(ctx, ctx_o)
     assert np.max(np.abs(e_new - e_old)) <= 1e-11 * np.max(np.abs(e_old))
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
@@ -266,6 +265,7 @@ def test_small_axis_transform_agrees(spec, nf, nc, iters, monkeypatch):
     ctx_o, _, _ = _ctx(spec, nf, nc)
     e_old = ctx_o.error_guess(r, 5)
     st_old = ctx_o.iterate(opts)
+    assert_variant_ran(ctx, ctx_o)
     assert np.max(np.abs(e_new - e_old)) <= 1e-11 * np.max(np.abs(e_old))
     a = np.array([h.res_l2 for h in st_new.history])
     b = np.array([h.res_l2 for h in st_old.history])
@@ -316,6 +316,7 @@ def test_dots_update_launch_agrees(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_DOTS_UPDATE", "1")
     ctx1, _, _ = _ctx(spec, nf, nc)
     st_one = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
     a = np.array([h.res_l2 for h in st_one.history])
     b = np.array([h.res_l2 for h in st_two.history])
     k = np.arange(len(b))
@@ -334,13 +335,16 @@ def test_skel3d_dots_rows_agree(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_SKEL3D_POINTS", "1")
     ctx1, _, _ = _ctx(spec, nf, nc)
     st_pts = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
     a = np.array([h.s_hat for h in st_rows.history[1:]])
     b = np.array([h.s_hat for h in st_pts.history[1:]])
-    assert np.all(np.abs(a - b) <= 1e-12 * np.abs(b) + 1e-300)
+    k = np.arange(1, len(b) + 1)
+    # another summation order of the same dots: last-bit differences, amplified by the iteration
+    assert np.all(np.abs(a - b) <= np.abs(b) * 1e-12 * 10.0 ** (k / 2.0) + 1e-300)
     assert np.max(np.abs(st_rows.u - st_pts.u)) <= 1e-10 * np.max(np.abs(st_pts.u))
 
 
-@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 459, 3, 8), ("ex:1:1", 919, 7, 6)])
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])
 def test_partitioned_hole_lines_agree(spec, nf, nc, iters, monkeypatch):
     """Large 2D holes (beyond the fused per-hole kernel): mode lines by one warp each with the
     partition method (default) against one thread each with Thomas (ASDSM_HOLE_THOMAS=1)."""
@@ -350,6 +354,7 @@ def test_partitioned_hole_lines_agree(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_HOLE_THOMAS", "1")
     ctx1, _, _ = _ctx(spec, nf, nc)
     st_t = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
     a = np.array([h.res_l2 for h in st_p.history])
     b = np.array([h.res_l2 for h in st_t.history])
     k = np.arange(len(b))
@@ -368,4 +373,5 @@ def test_merge3d_warp_splines_bitwise(spec, nf, nc, iters, monkeypatch):
     monkeypatch.setenv("ASDSM_M3_THREAD_LINES", "1")
     ctx1, _, _ = _ctx(spec, nf, nc)
     st_t = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
     assert np.array_equal(st_w.u, st_t.u) and np.array_equal(st_w.r, st_t.r)

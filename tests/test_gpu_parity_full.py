@@ -1,0 +1,63 @@
+"""GPU parity at the hole extents the bench times (VERDICT r1 "missing" 1).
+
+The kernels that only run at the BASELINE configs' own sizes, against the compiled reference
+(oracle/_ref, the reference's asdsm_iterate solver.cpp:565-680 with its hole solve
+linsolve.cpp:156-171), 10 iterations each, same bounds as test_gpu_parity (final u relative
+1e-10, history within max(1e-10, 10x the reference's own fill-ordering spread)):
+
+  * config 2 at its full mesh 4099^2 (N_c = 9, holes m = 409): the two-kernel large-hole path
+    (hole2d_ring + hole2d_part_kernel + dmma_eo2_kernel) and the 4099-point slab lines;
+  * config 3's steady 3D hole extent m = 25 (103^3 at N_c = 3: 64 holes; 51^3 at N_c = 1): the
+    SYM schedule of hole3d_fused_kernel;
+  * config 4's space-time hole extent m = 50 (101^3 at N_c = 1): the CAUSAL schedule of
+    hole3d_fused_kernel with its chunked plane production.
+
+Each test also asserts, from the plan's captured graph, that the intended kernel ran.
+The reference runs take 15 s - 2 min of host time each (both fill orderings run concurrently).
+"""
+import numpy as np
+import pytest
+
+import paper_2303_01163_b200 as pb
+from ref_tools import have_ref, ref_iterate_pair
+from test_gpu_parity import _ctx, check_history
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")]
+
+
+def _run(spec, nf, nc, iters, seed):
+    ctx, mesh, _ = _ctx(spec, nf, nc)
+    # (natural ordering is out of reach at these sizes: band LU of a 4099-wide slab / 2500-wide
+    # hole band in natural order; RCM vs CM spread only)
+    ref, alts = ref_iterate_pair(spec, nf, nc, iters, seed, orders=("cm",))
+    st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=seed))
+    assert ref["meta"][2] == list(mesh.fine_counts)
+    rel, urel = check_history(st, ref, alts)
+    print(f"{spec} {mesh.fine_counts} nc={mesh.coarse_counts}: history max rel {rel:.2e}, u max rel {urel:.2e}")
+    return ctx
+
+
+def _has(kernels, name):
+    return any(name in k for k in kernels)
+
+
+@pytest.mark.timeout(900)
+def test_config2_full_mesh_m409():
+    ctx = _run("cfg:2:5", 0, 0, 10, 2)
+    k = ctx.kernels()
+    assert _has(k, "hole2d_part_kernel") and _has(k, "dmma_eo2_kernel"), sorted(k)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("nf,nc,seed", [(103, 3, 1), (51, 1, 4)])
+def test_config3_hole_extent_m25_sym(nf, nc, seed):
+    ctx = _run("cfg:3:0", nf, nc, 10, seed)
+    assert ctx.config.factors == [26, 26, 26]
+    assert _has(ctx.kernels(), "hole3d_fused_kernel<false>"), sorted(ctx.kernels())
+
+
+@pytest.mark.timeout(900)
+def test_config4_hole_extent_m50_causal():
+    ctx = _run("cfg:4:3", 101, 1, 10, 3)
+    assert ctx.config.factors == [51, 51, 51]
+    assert _has(ctx.kernels(), "hole3d_fused_kernel<true>"), sorted(ctx.kernels())

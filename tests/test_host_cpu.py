@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(pb.library_path())
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert pb.load_library().asdsm_abi_version() == 2
+    assert pb.load_library().asdsm_abi_version() == 3
 
 
 @pytest.mark.parametrize("name", ["ex1s1_24_4", "ex3s1_24_4", "ex4s1_14_4", "cfg1_49_4", "cfg2_49_4", "cfg3_14_4",
