@@ -102,7 +102,12 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     for (int a = 0; a < m.dim; ++a)
       sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
     sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
-    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, nholes, "hole block", m.dim == 2);
+    // 3D holes that fit the one-kernel fill (m <= 64 on the transform axes) need the Thomas
+    // pivot tables whatever the hole count (the fused kernel runs its own line solves), so the
+    // few-lines PCR choice is not taken for them
+    const bool fused3d_candidate = m.dim == 3 && hext[0] <= 64 && hext[1] <= 64;
+    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, fused3d_candidate ? std::max<i64>(nholes, 1 << 20) : nholes,
+                                 "hole block", m.dim == 2);
   } else {
     // per-point stencils (fdm.cpp:63-126 sampling) + block-Thomas factors for every box
     const std::vector<double> cf = sample_kind_coefficients(m, 0u, *varprob);
@@ -434,7 +439,7 @@ void Solver::solve_box(int which, double* data, cudaStream_t s) {
   launch_block_thomas(bt_[which], arr, state_, s);
 }
 
-void Solver::fill(double* e, const double* b, cudaStream_t s) {
+void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
   if (variable_) {
     launch_hole_rhs_var(mesh_.dim, e, b, fg_, coef_fine_, md_, state_, s);
     solve_box(4, e, s);
@@ -525,13 +530,16 @@ void Solver::fill(double* e, const double* b, cudaStream_t s) {
     // one thread per mode line (Thomas)
     const bool thomas = std::getenv("ASDSM_HOLE_THOMAS") != nullptr;
     const bool part = !thomas && H.part && hole2d_part_supported(H.part_seg) && hole_ring_;
-    if (part) {
-      Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
-      launch_hole2d_ring(e, A, P, state_, s);
-      launch_hole2d_part(modes, A, P, state_, s);
-    } else {
-      launch_hole2d_fwd_thomas(e, modes, A, state_, s);
+    if (stage & kFillLines) {
+      if (part) {
+        Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
+        launch_hole2d_ring(e, A, P, state_, s);
+        launch_hole2d_part(modes, A, P, state_, s);
+      } else {
+        launch_hole2d_fwd_thomas(e, modes, A, state_, s);
+      }
     }
+    if (!(stage & kFillBack)) return;
     GemmLines G{};
     G.o_ext[0] = A.m1;
     G.o_ext[1] = 1;
@@ -1174,61 +1182,22 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
             [&] { launch_slab2d_back(SA, partials_, state_, history_, true, s, &sk); });
       timed("skeleton_write", 16.0 * nskel, 0.0, iters, [&] { launch_skel2d_write_fast(sk, state_, s); });
     }
-    Hole2DArgs A{};
-    A.m0 = H.ext[0];
-    A.m1 = H.ext[1];
-    A.n0 = mesh_.n[0];
-    A.n1 = mesh_.n[1];
-    A.nf0 = mesh_.nf[0];
-    A.nf1 = mesh_.nf[1];
-    A.nbox0 = mesh_.nc[0] + 1;
-    A.nbox1 = mesh_.nc[1] + 1;
-    A.kb = 64;
-    A.y_in_smem = hole2d_smem_bytes(A.m0, A.m1, A.kb, true) <= 48 * 1024 ? 1 : 0;
-    if (!A.y_in_smem && hole2d_smem_bytes(A.m0, A.m1, 32, true) <= 48 * 1024) {
-      A.kb = 32;
-      A.y_in_smem = 1;
-    }
-    A.st = st_fine_;
-    A.Wt = H.Wt[0];
-    A.half = H.half[0];
-    A.ipiv = H.th_ipiv;
-    A.cp = H.th_cp;
-    A.line_left = H.line_left;
-    A.line_right = H.line_right;
-    const bool unfused = std::getenv("ASDSM_HOLE_UNFUSED") != nullptr;
-    if (!unfused && hole2d_fused_fits(A.m0, A.m1)) {
-      // one kernel: ring rhs, sweeps, DMMA back transform (writes the hole interior once)
-      timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
-            [&] { launch_hole2d_fused(e_, A, nullptr, state_, s); });
+    // the hole fill exactly as the solve launches it (Solver::fill): one fused kernel per hole,
+    // or (large holes) the mode-line solves and the DMMA back transform timed apart
+    const double eo = H.ext[0] >= kEoMinModes ? 0.5 : 1.0;  // even/odd split executes half the MACs
+    if (hole2d_fused_fits(H.ext[0], H.ext[1]) && std::getenv("ASDSM_HOLE_UNFUSED") == nullptr) {
+      timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * eo * static_cast<double>(NH), iters,
+            [&] { fill(e_, nullptr, s); });
     } else {
-    timed("hole2d_fwd_thomas", 8.0 * NH * (A.y_in_smem ? 1.0 : 3.0), 0.0, iters,
-          [&] { launch_hole2d_fwd_thomas(e_, static_cast<double*>(scratch0_), A, state_, s); });
-    GemmLines G{};
-    G.o_ext[0] = H.ext[1];
-    G.o_ext[1] = 1;
-    G.o_in[0] = H.ext[0];
-    G.o_out[0] = g_fine_.stride[1];
-    G.nbox[0] = mesh_.nc[0] + 1;
-    G.nbox[1] = mesh_.nc[1] + 1;
-    G.nbox[2] = 1;
-    G.in_bs[0] = static_cast<i64>(H.ext[0]) * H.ext[1];
-    G.in_bs[1] = G.in_bs[0] * G.nbox[0];
-    G.out_bs[0] = mesh_.n[0];
-    G.out_bs[1] = static_cast<i64>(mesh_.n[1]) * g_fine_.stride[1];
-    G.nlines = static_cast<i64>(H.ext[1]) * G.nbox[0] * G.nbox[1];
-    timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * static_cast<double>(NH), iters,
-          [&] {
-            if (H.ext[0] >= kEoMinModes)
-              launch_dmma_eo_transform(true, static_cast<const double*>(scratch0_), e_, H.half[0], H.ext[0], 1, 1, G, s);
-            else
-              launch_dmma_transform(static_cast<const double*>(scratch0_), e_, H.V[0], H.ext[0], 1, 1, G, s);
-          });
+      timed("hole2d_mode_lines", 8.0 * NH * 2.0, 0.0, iters, [&] { fill(e_, nullptr, s, kFillLines); });
+      timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * eo * static_cast<double>(NH), iters,
+            [&] { fill(e_, nullptr, s, kFillBack); });
     }
   } else {
     double hflops = 0;
     if (!variable_)
       for (int i = 0; i < H.nd; ++i) hflops += 2.0 * H.ext[H.dax[i]] * static_cast<double>(NH);
+    if (h3f_ok_ && std::getenv("ASDSM_HOLE3D_UNFUSED") == nullptr) hflops *= 0.5;  // even/odd on both axes
     timed("hole_fill", 8.0 * NH * 3.0, hflops, iters, [&] { fill(e_, nullptr, s); });
     timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
       for (int a = 0; a < mesh_.dim; ++a) {

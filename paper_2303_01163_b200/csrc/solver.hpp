@@ -96,7 +96,10 @@ class Solver {
   void smooth_guess(double* out, cudaStream_t s);
   void error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s);
   void skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s);
-  void fill(double* e, const double* b, cudaStream_t s);
+  // stage: kFillAll, or (2D two-kernel hole path, for per-component timing) kFillLines = ring rhs +
+  // mode-line solves only, kFillBack = the back transform only
+  enum { kFillLines = 1, kFillBack = 2, kFillAll = 3 };
+  void fill(double* e, const double* b, cudaStream_t s, int stage = kFillAll);
   BoxArray hole_array(double* p) const;
   BoxArray kind_array(const KindGeom& g, double* p) const;
 
