@@ -981,6 +981,90 @@ void launch_hole2d_fused(double* e, const Hole2DArgs& A, const double* b, DevSta
 
 bool hole2d_part_supported(int seg) { return seg == 4 || seg == 8 || seg == 12 || seg == 16; }
 
+namespace {
+constexpr int kSepRowsJ = 64;     // rows j per CTA (coalesced)
+// k groups per CTA (each thread sums every KG-th mode): 8, or 4 with more than 4 separators
+__host__ __device__ constexpr int sep_rows_kg(int ns) { return ns <= 4 ? 8 : 4; }
+
+// One CTA per (hole, 64 rows j), 8 k-groups: thread (jj, g) sums the modes k = g, g + 8, ... of
+// row j for the NS separators (loads of consecutive k in flight together), then the k-groups
+// combine in shared memory in a fixed order.
+template <int NS, int kSepRowsKG = sep_rows_kg(NS)>
+__global__ void __launch_bounds__(kSepRowsJ * kSepRowsKG) hole2d_sep_rows_kernel(const double* __restrict__ modes,
+                                                                                const double* __restrict__ V,
+                                                                                double* __restrict__ e, Hole2DArgs A,
+                                                                                const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  extern __shared__ double vs[];  // [s][k]: rows i_s of V, then the k-group partials [g][s][jj]
+  const int m0 = A.m0, m1 = A.m1, w1 = (m0 + 1) / (NS + 1);
+  for (int t = threadIdx.x; t < NS * m0; t += blockDim.x) {
+    const int sidx = t / m0, k = t - sidx * m0;
+    vs[t] = __ldg(V + static_cast<i64>((sidx + 1) * w1 - 1) * m0 + k);
+  }
+  __syncthreads();
+  double* part = vs + NS * m0;
+  const int hole = blockIdx.x;
+  const int jj = threadIdx.x % kSepRowsJ, g = threadIdx.x / kSepRowsJ;
+  const int j = blockIdx.y * kSepRowsJ + jj;
+  double acc[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) acc[q] = 0.0;
+  if (j < m1) {
+    const double* md = modes + static_cast<i64>(hole) * m0 * m1 + j;
+    int k = g;
+    for (; k + 3 * kSepRowsKG < m0; k += 4 * kSepRowsKG) {
+      double w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = __ldg(md + static_cast<i64>(k + u * kSepRowsKG) * m1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) acc[q] = fma(vs[q * m0 + k + u * kSepRowsKG], w[u], acc[q]);
+    }
+    for (; k < m0; k += kSepRowsKG) {
+      const double w = __ldg(md + static_cast<i64>(k) * m1);
+#pragma unroll
+      for (int q = 0; q < NS; ++q) acc[q] = fma(vs[q * m0 + k], w, acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NS; ++q) part[(g * NS + q) * kSepRowsJ + jj] = acc[q];
+  __syncthreads();
+  if (g != 0 || j >= m1) return;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  double* out = e + static_cast<i64>(hy * A.n1 + j) * A.nf0 + hx * A.n0;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double v = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < kSepRowsKG; ++gg) v += part[(gg * NS + q) * kSepRowsJ + jj];
+    out[(q + 1) * w1 - 1] = v;
+  }
+}
+}  // namespace
+
+void launch_hole2d_sep_rows(const double* modes, const double* V, double* e, const Hole2DArgs& A, int p,
+                            DevState* state, cudaStream_t s) {
+  if (p < 2 || p > 10 || (A.m0 + 1) % p != 0) throw AsdsmError(kUnsupported, "hole strip split");
+  const dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m1 + kSepRowsJ - 1) / kSepRowsJ));
+  const size_t smem = sizeof(double) * static_cast<size_t>(p - 1) * (A.m0 + sep_rows_kg(p - 1) * kSepRowsJ);
+  if (smem > 48 * 1024) throw AsdsmError(kUnsupported, "hole strip split: separator table exceeds shared memory");
+  const unsigned nt = kSepRowsJ * sep_rows_kg(p - 1);
+  switch (p - 1) {
+    case 1: hole2d_sep_rows_kernel<1><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 2: hole2d_sep_rows_kernel<2><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 3: hole2d_sep_rows_kernel<3><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 4: hole2d_sep_rows_kernel<4><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 5: hole2d_sep_rows_kernel<5><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 6: hole2d_sep_rows_kernel<6><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 7: hole2d_sep_rows_kernel<7><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 8: hole2d_sep_rows_kernel<8><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    default: hole2d_sep_rows_kernel<9><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+  }
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void launch_hole2d_ring(const double* e, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state,
                         cudaStream_t s) {
   hole2d_ring_kernel<<<static_cast<unsigned>(A.nbox0 * A.nbox1), 256, 0, s>>>(e, A, P, state);

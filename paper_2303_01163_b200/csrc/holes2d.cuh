@@ -57,4 +57,13 @@ void launch_hole2d_ring(const double* e, const Hole2DArgs& A, const Hole2DPartAr
                         cudaStream_t s);
 void launch_hole2d_part(double* modes, const Hole2DArgs& A, const Hole2DPartArgs& P, DevState* state, cudaStream_t s);
 
+// Strip split of large holes (error mode): once the mode lines of a hole are solved
+// (modes[hole][k][j]), its solution on the p - 1 separator columns i_s = s (w + 1) - 1 is
+// v(i_s, j) = sum_k V[i_s][k] modes[k][j]: a (p - 1) x m0 by m0 x m1 product per hole, written
+// into the fine array.  The p strips of w = (m0 + 1) / p - 1 columns between separators are then
+// holes of their own (Dirichlet data: skeleton and separators) with w-point transforms, so the
+// back transform costs w instead of m0 per point.
+void launch_hole2d_sep_rows(const double* modes, const double* V, double* e, const Hole2DArgs& A, int p,
+                            DevState* state, cudaStream_t s);
+
 }  // namespace asdsm_b200

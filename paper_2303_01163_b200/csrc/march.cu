@@ -729,6 +729,10 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
     else if (kYc == 2) ASDSM_YC_DISPATCH(2);
     else ASDSM_YC_DISPATCH(8);
 #undef ASDSM_YC_DISPATCH
+  } else if ((mode == kMarchUpdate || mode == kMarchResidual) && stream3d_supported(A) &&
+             std::getenv("ASDSM_MARCH3D") == nullptr) {
+    launch_stream3d(mode, A, s);
+    return;
   } else if (mode == kMarchUpdate && std::getenv("ASDSM_MARCH3D") == nullptr) {
     // measured (configs 3/4): axpy + candidate residual beats the fused 3D update
     axpy_update_kernel<<<8 * kNumSms, 256, 0, s>>>(A);

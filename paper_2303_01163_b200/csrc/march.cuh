@@ -53,5 +53,9 @@ bool dots_update_supported(const FineGeom& g);
 int march_strip(const FineGeom& g);
 unsigned march_blocks(const FineGeom& g);
 void launch_march(int mode, const MarchArgs& A, cudaStream_t s);
+// 3D constant-coefficient UPDATE / RESIDUAL as one TMA-staged z-march (stream3d.cu); opt-in
+// with ASDSM_STREAM3D=1 (read at launch / capture), the register-marching passes otherwise
+bool stream3d_supported(const MarchArgs& A);
+void launch_stream3d(int mode, const MarchArgs& A, cudaStream_t s);
 
 }  // namespace asdsm_b200

@@ -137,13 +137,16 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   }
 
   const i64 nf = g_fine_.size;
+  // fine arrays carry one grid row of slack: the 3D pass's pair-row tensor maps (stream3d.cu)
+  // address whole row pairs, and the last pair's odd row lies past the array when N_y N_z is odd
+  const size_t nfa = static_cast<size_t>(nf) + static_cast<size_t>(m.nf[0]) + 2;
   for (int i = 0; i < 2; ++i) {
-    u_[i] = dev_.alloc<double>(static_cast<size_t>(nf));
-    r_[i] = dev_.alloc<double>(static_cast<size_t>(nf));
+    u_[i] = dev_.alloc<double>(nfa);
+    r_[i] = dev_.alloc<double>(nfa);
   }
-  b_ = dev_.alloc<double>(static_cast<size_t>(nf));
-  e_ = dev_.alloc<double>(static_cast<size_t>(nf));
-  exact_ = dev_.alloc<double>(static_cast<size_t>(nf));
+  b_ = dev_.alloc<double>(nfa);
+  e_ = dev_.alloc<double>(nfa);
+  exact_ = dev_.alloc<double>(nfa);
   size_t scratch = variable_ ? 16 : sep_scratch_bytes(sep_hole_, nholes);
   for (int a = 0; a < m.dim; ++a) {
     const size_t n = static_cast<size_t>(g_slab_[a].size);
@@ -157,6 +160,34 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
   scratch1_ = dev_.alloc<unsigned char>(scratch);
   if (m.dim == 2 && !variable_ && sep_hole_.part)  // per-hole ring of the partitioned hole solve
     hole_ring_ = dev_.alloc<double>(static_cast<size_t>(nholes) * 2 * (sep_hole_.ext[0] + sep_hole_.ext[1]));
+  if (hole_ring_ && !sep_hole_.complex_modes && sep_hole_.nd == 1 && sep_hole_.L == 1 && sep_hole_.dax[0] == 0 &&
+      !sep_hole_.use_pcr && !hole2d_fused_fits(sep_hole_.ext[0], sep_hole_.ext[1])) {
+    // strip split of the large holes: the fewest strips (p | m0 + 1) of at most kStripMaxW
+    // columns; ASDSM_STRIPS=p overrides (0: off)
+    constexpr int kStripMaxW = 96;
+    const int n0 = sep_hole_.ext[0] + 1;
+    int p = 0;
+    // (the separator kernel keeps p - 1 rows of V and its k-group partials in 48 KB)
+    auto fits = [&](int q) {
+      return q >= 2 && q <= 10 && n0 % q == 0 && (q - 1) * (n0 - 1 + (q <= 5 ? 512 : 256)) * 8 <= 48 * 1024;
+    };
+    if (const char* env = std::getenv("ASDSM_STRIPS")) {
+      p = std::atoi(env);
+      if (!fits(p)) p = 0;
+    } else {
+      for (int q = 2; q <= 10 && !p; ++q)
+        if (fits(q) && n0 / q - 1 <= kStripMaxW) p = q;
+    }
+    if (p) {
+      int sext[3] = {n0 / p - 1, sep_hole_.ext[1], 1};
+      sep_strip_ = build_sep_solver(dev_, 2, sext, st_fine_, tax, -1, nholes * p, "hole strip", true);
+      if (!sep_strip_.complex_modes && sep_strip_.nd == 1 && sep_strip_.L == 1 && sep_strip_.dax[0] == 0 &&
+          !sep_strip_.use_pcr && sep_strip_.part && hole2d_part_supported(sep_strip_.part_seg)) {
+        strip_p_ = p;
+        strip_ring_ = dev_.alloc<double>(static_cast<size_t>(nholes) * p * 2 * (sext[0] + sext[1]));
+      }
+    }
+  }
   if (m.dim == 3 && !variable_) {
     // the three slab solves of an iteration are independent: slabs 1 and 2 run on their own
     // streams (forked / joined with events, captured into the graph as parallel branches),
@@ -530,6 +561,10 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
     // one thread per mode line (Thomas)
     const bool thomas = std::getenv("ASDSM_HOLE_THOMAS") != nullptr;
     const bool part = !thomas && H.part && hole2d_part_supported(H.part_seg) && hole_ring_;
+    // strip split (error mode, partitioned lines): separators from the hole's modes, then every
+    // strip as a hole of w columns (ASDSM_STRIPS; read at capture time)
+    const bool strips = part && strip_p_ > 0;
+    const SepSolver& T = strips ? sep_strip_ : H;
     if (stage & kFillLines) {
       if (part) {
         Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
@@ -538,6 +573,26 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
       } else {
         launch_hole2d_fwd_thomas(e, modes, A, state_, s);
       }
+      if (strips) {
+        launch_hole2d_sep_rows(modes, H.V[0], e, A, strip_p_, state_, s);
+        const int w = T.ext[0];
+        A.m0 = w;
+        A.n0 = w + 1;
+        A.nbox0 *= strip_p_;
+        A.Wt = T.Wt[0];
+        A.half = T.half[0];
+        A.ipiv = T.th_ipiv;
+        A.cp = T.th_cp;
+        A.line_left = T.line_left;
+        A.line_right = T.line_right;
+        Hole2DPartArgs P{T.W[0], T.part, T.part_stride, T.part_seg, T.part_P, T.part_last, strip_ring_};
+        launch_hole2d_ring(e, A, P, state_, s);
+        launch_hole2d_part(modes, A, P, state_, s);
+      }
+    } else if (strips) {
+      A.m0 = T.ext[0];
+      A.n0 = T.ext[0] + 1;
+      A.nbox0 *= strip_p_;
     }
     if (!(stage & kFillBack)) return;
     GemmLines G{};
@@ -555,8 +610,8 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
     const i64 in_es = part ? A.m1 : 1;  // [hole][k][j] from the partition solve, else [hole][j][k]
     if (A.m0 >= kEoMinModes && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
-      launch_dmma_eo_transform(true, modes, e, H.half[0], A.m0, in_es, 1, G, s);
-    else launch_dmma_transform(modes, e, H.V[0], A.m0, in_es, 1, G, s);
+      launch_dmma_eo_transform(true, modes, e, T.half[0], A.m0, in_es, 1, G, s);
+    else launch_dmma_transform(modes, e, T.V[0], A.m0, in_es, 1, G, s);
     return;
   }
   if (!generic && mesh_.dim == 3 && b == nullptr && !H.complex_modes && H.nd == 2 && H.L == 2 && H.dax[0] == 0 &&
@@ -1184,13 +1239,17 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     }
     // the hole fill exactly as the solve launches it (Solver::fill): one fused kernel per hole,
     // or (large holes) the mode-line solves and the DMMA back transform timed apart
-    const double eo = H.ext[0] >= kEoMinModes ? 0.5 : 1.0;  // even/odd split executes half the MACs
     if (hole2d_fused_fits(H.ext[0], H.ext[1]) && std::getenv("ASDSM_HOLE_UNFUSED") == nullptr) {
+      const double eo = H.ext[0] >= kEoMinModes ? 0.5 : 1.0;  // even/odd split executes half the MACs
       timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * eo * static_cast<double>(NH), iters,
             [&] { fill(e_, nullptr, s); });
     } else {
-      timed("hole2d_mode_lines", 8.0 * NH * 2.0, 0.0, iters, [&] { fill(e_, nullptr, s, kFillLines); });
-      timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * H.ext[0] * eo * static_cast<double>(NH), iters,
+      // (strip split: the back transform runs over the strips' w-point transforms)
+      const int mt = strip_p_ ? sep_strip_.ext[0] : H.ext[0];
+      const double eot = mt >= kEoMinModes ? 0.5 : 1.0;
+      timed(strip_p_ ? "hole2d_mode_lines_separators_strip_lines" : "hole2d_mode_lines", 8.0 * NH * 2.0, 0.0, iters,
+            [&] { fill(e_, nullptr, s, kFillLines); });
+      timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * mt * eot * static_cast<double>(NH), iters,
             [&] { fill(e_, nullptr, s, kFillBack); });
     }
   } else {

@@ -142,6 +142,11 @@ class Solver {
   double* skel_corr_ = nullptr;                 //   and the cross-point corrections
   bool ring_from_lines_ = false;                // fill(): holes evaluate + write the skeleton
   double* hole_ring_ = nullptr;                 // 2D large holes: [hole][2 m1 + 2 m0] ring + row transforms
+  // 2D large holes, error mode: strip split (holes2d.cuh launch_hole2d_sep_rows) -- p strips of
+  // w columns per hole between p - 1 separator columns, each solved as a hole of its own
+  int strip_p_ = 0;
+  SepSolver sep_strip_{};
+  double* strip_ring_ = nullptr;
   bool dots_update_ok_ = false;                 // kMarchDotsUpdate on (ASDSM_DOTS_UPDATE=1) and applicable
   // optimal-step dot products over the skeleton rows only (ASDSM_FULL_DOTS=1: every row)
   bool skel_dots_ = std::getenv("ASDSM_FULL_DOTS") == nullptr;                          // one-launch slab step (slabstep2d.cu) eligible

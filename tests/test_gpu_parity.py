@@ -375,3 +375,41 @@ def test_merge3d_warp_splines_bitwise(spec, nf, nc, iters, monkeypatch):
     st_t = ctx1.iterate(opts)
     assert_variant_ran(ctx, ctx1)
     assert np.array_equal(st_w.u, st_t.u) and np.array_equal(st_w.r, st_t.r)
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:4:1", 24, 4, 6)])
+def test_stream3d_tma_pass_bitwise(spec, nf, nc, iters, monkeypatch):
+    """The opt-in TMA-staged 3D update / residual pass (ASDSM_STREAM3D=1, stream3d.cu: pair-row
+    tensor maps, v = u + s e formed once per point) against the default axpy + z-coarsened
+    residual passes: the same row sums in the reference's CSR order, so bitwise the same solve."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=3)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_d = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_STREAM3D", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_t = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    assert any("stream3d_kernel" in k for k in ctx1.kernels()), sorted(ctx1.kernels())
+    assert np.array_equal(st_d.u, st_t.u) and np.array_equal(st_d.r, st_t.r)
+    assert np.array_equal(np.array([h.res_l2 for h in st_d.history]), np.array([h.res_l2 for h in st_t.history]))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])
+def test_hole_strip_split_agrees(spec, nf, nc, iters, monkeypatch):
+    """Large 2D holes split into strips (default: separator columns from the hole's own modes,
+    then every strip solved as a hole with w-point transforms, holes2d.cu hole2d_sep_rows_kernel)
+    against the whole-hole back transform (ASDSM_STRIPS=0): the same exact hole solve."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=4)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_s = ctx.iterate(opts)
+    assert any("hole2d_sep_rows_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
+    monkeypatch.setenv("ASDSM_STRIPS", "0")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_w = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    a = np.array([h.res_l2 for h in st_s.history])
+    b = np.array([h.res_l2 for h in st_w.history])
+    k = np.arange(len(b))
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
+    assert np.max(np.abs(st_s.u - st_w.u)) <= 1e-8 * np.max(np.abs(st_w.u))
