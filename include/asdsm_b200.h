@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define ASDSM_B200_ABI_VERSION 3
+#define ASDSM_B200_ABI_VERSION 4
 
 /* Status codes <-> errors.hpp exception classes. */
 enum asdsm_status {
@@ -66,8 +66,34 @@ void asdsm_default_options(asdsm_iterate_options* o);
 int asdsm_problem_example(int example, int setting, asdsm_problem** out);
 /* BASELINE.json config id (0..4) with its seeded synthetic source. */
 int asdsm_problem_config(int config_id, uint64_t seed, asdsm_problem** out);
+/* A caller-defined ProblemSpec (fdm.hpp:17-30: dim, time_dependent, alpha/beta per spatial
+ * axis, source, boundary, optional exact -- the reference's ScalarField callables) as C
+ * callbacks, each with its own context pointer.  A field is evaluated at a point x[0..dim-1]
+ * (the last coordinate is t when time_dependent), at the sampling points of the reference's
+ * assembly (fdm.cpp:63-171), on host threads during plan creation and right-hand-side assembly
+ * only -- never during a solve; fields must be pure (thread-safe).  alpha/beta entries past the
+ * spatial axes are ignored (may be NULL); exact may be NULL.  The problem keeps the pointers:
+ * contexts must outlive it.  Plans made from it take the separable constant-coefficient solvers
+ * when every fine-node sample of alpha_a and beta_a is the same value, the per-point
+ * (variable-coefficient) path otherwise -- the operator is the reference's either way. */
+typedef double (*asdsm_field_fn)(const double* x, void* ctx);
+typedef struct {
+  asdsm_field_fn fn;
+  void* ctx;
+} asdsm_field;
+typedef struct {
+  int32_t dim;            /* 2 or 3 */
+  int32_t time_dependent; /* last axis is t (backward difference; boundary = initial data) */
+  asdsm_field alpha[3];   /* diffusion per spatial axis, positive */
+  asdsm_field beta[3];    /* advection per spatial axis */
+  asdsm_field source;
+  asdsm_field boundary;
+  asdsm_field exact;      /* fn NULL: no exact solution attached */
+} asdsm_problem_spec;
+int asdsm_problem_create(const asdsm_problem_spec* spec, asdsm_problem** out);
 void asdsm_problem_destroy(asdsm_problem* p);
-/* dim, time-dependence, constant coefficients (alpha/beta have 3 entries), exact available. */
+/* dim, time-dependence, constant coefficients (alpha/beta have 3 entries), exact available.
+ * A caller-defined problem reports constant_coeffs = 0: plans decide it from their samples. */
 int asdsm_problem_info(const asdsm_problem* p, int* dim, int* time_dependent, int* constant_coeffs,
                        double* alpha, double* beta, int* has_exact);
 /* Mesh of a BASELINE config (fine/coarse counts, 3 entries each) and its iteration budget. */
@@ -120,6 +146,16 @@ int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* h
 int asdsm_solve(asdsm_plan* plan, const double* b_fine, const double* const* b_slab, const double* b_coarse,
                 const double* exact, const asdsm_iterate_options* opts, double* history, int* nrec,
                 int* stop_code, double* u_out, double* r_out);
+/* asdsm_iterate with IterateOptions::observer (solver.hpp:65-66): `observer` is called after each
+ * recorded iteration (k = 0 first) with the history rows so far (7 doubles each, as
+ * asdsm_iterate), the current iterate u and residual r (n fine values each; host arrays valid
+ * during the call) -- the reference's IterationState at that point.  The solve runs launch by
+ * launch with one stream synchronize per iteration instead of the captured graph (same
+ * arithmetic, so the same results); the final outputs are asdsm_iterate's. */
+typedef void (*asdsm_observer_fn)(const double* history, int nrec, const double* u, const double* r, int64_t n,
+                                  void* ctx);
+int asdsm_iterate_observed(asdsm_plan* plan, const asdsm_iterate_options* opts, asdsm_observer_fn observer, void* ctx,
+                           double* history, int* nrec, int* stop_code, double* u_out, double* r_out);
 /* Same solve fully on `stream` (cudaStream_t as void*, NULL = legacy): no host sync. */
 int asdsm_iterate_async(asdsm_plan* plan, const asdsm_iterate_options* opts, void* stream);
 /* After asdsm_iterate_async: history/outputs to host (synchronizes the stream). */

@@ -21,6 +21,7 @@ from .asdsm import (  # noqa: F401
     NoExactSolution,
     NotASubmesh,
     Problem,
+    ProblemSpec,
     SingularMatrix,
     SkeletonNotHollow,
     SolverContext,

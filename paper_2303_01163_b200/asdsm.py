@@ -14,7 +14,7 @@ import ctypes
 import math
 import os
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
@@ -92,6 +92,22 @@ def library_path() -> str:
     return os.environ.get("ASDSM_LIB") or os.path.join(_HERE, "libasdsm_b200.so")
 
 
+_FIELD_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)
+
+
+class _Field(ctypes.Structure):
+    _fields_ = [("fn", _FIELD_FN), ("ctx", ctypes.c_void_p)]
+
+
+class _ProblemSpec(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("time_dependent", ctypes.c_int32), ("alpha", _Field * 3),
+                ("beta", _Field * 3), ("source", _Field), ("boundary", _Field), ("exact", _Field)]
+
+
+_OBSERVER_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
+
+
 class _Options(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32),
                 ("stagnation_window", ctypes.c_int32), ("stagnation_ratio", ctypes.c_double),
@@ -117,6 +133,7 @@ def load_library():
         "asdsm_abi_version": (I, []),
         "asdsm_problem_example": (I, [I, I, ctypes.POINTER(P)]),
         "asdsm_problem_config": (I, [I, ctypes.c_uint64, ctypes.POINTER(P)]),
+        "asdsm_problem_create": (I, [ctypes.POINTER(_ProblemSpec), ctypes.POINTER(P)]),
         "asdsm_problem_destroy": (None, [P]),
         "asdsm_problem_info": (I, [P, IP, IP, IP, D, D, IP]),
         "asdsm_config_mesh": (I, [I, IP, IP, IP, IP, IP]),
@@ -132,6 +149,7 @@ def load_library():
         "asdsm_set_bundle_async": (I, [P, D, ctypes.POINTER(D), D, D, I, P]),
         "asdsm_iterate": (I, [P, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_iterate_async": (I, [P, ctypes.POINTER(_Options), P]),
+        "asdsm_iterate_observed": (I, [P, ctypes.POINTER(_Options), _OBSERVER_FN, P, D, IP, IP, D, D]),
         "asdsm_fetch": (I, [P, P, D, IP, IP, D, D]),
         "asdsm_solve": (I, [P, D, ctypes.POINTER(D), D, D, ctypes.POINTER(_Options), D, IP, IP, D, D]),
         "asdsm_device_solution": (I, [P, P, ctypes.POINTER(ctypes.c_void_p)]),
@@ -315,6 +333,57 @@ class Problem:
         return out
 
 
+class ProblemSpec:
+    """The reference's ProblemSpec (fdm.hpp:17-30) with caller-defined fields: Python callables
+    f(x) of a point x (a sequence of `dim` floats; the last one is t when time_dependent).
+    alpha / beta hold one callable per spatial axis.  The fields are evaluated on the host while
+    a plan is built and its right-hand sides assembled (asdsm_problem_create), never during a
+    solve; `problem()` returns the library handle (a Problem) usable wherever a catalogue
+    problem is."""
+
+    def __init__(self, dim: int, alpha, beta, source, boundary, exact=None, time_dependent: bool = False):
+        self.dim = int(dim)
+        self.time_dependent = bool(time_dependent)
+        self.alpha = list(alpha)
+        self.beta = list(beta)
+        self.source = source
+        self.boundary = boundary
+        self.exact = exact
+
+    def spatial_axes(self) -> int:
+        return self.dim - 1 if self.time_dependent else self.dim
+
+    def problem(self) -> "Problem":
+        lib = load_library()
+        dim = self.dim
+        keep = []
+
+        def field(f):
+            if f is None:
+                return _Field(_FIELD_FN(), None)
+
+            def tramp(x, _ctx, f=f):
+                return float(f(tuple(x[a] for a in range(dim))))
+            cb = _FIELD_FN(tramp)
+            keep.append(cb)
+            return _Field(cb, None)
+
+        spec = _ProblemSpec()
+        spec.dim = dim
+        spec.time_dependent = int(self.time_dependent)
+        for a in range(self.spatial_axes()):
+            spec.alpha[a] = field(self.alpha[a])
+            spec.beta[a] = field(self.beta[a])
+        spec.source = field(self.source)
+        spec.boundary = field(self.boundary)
+        spec.exact = field(self.exact)
+        h = ctypes.c_void_p()
+        _check(lib.asdsm_problem_create(ctypes.byref(spec), ctypes.byref(h)))
+        prob = Problem(h, "caller-defined ProblemSpec")
+        prob._keep = keep  # the callbacks live as long as the handle
+        return prob
+
+
 def make_problem(example: int, setting: int) -> Problem:
     """make_problem (problems.hpp:20, problems.cpp:114-141)."""
     lib = load_library()
@@ -357,6 +426,9 @@ class IterateOptions:
     subsample: float = 0.0
     rng_seed: int = 0
     sparse_residual: bool = False
+    # called with the IterationState after each recorded iteration (k = 0 first), as
+    # solver.hpp:65-66 (C-ABI asdsm_iterate_observed: launch by launch, one sync per iteration)
+    observer: Optional[Callable[["IterationState"], None]] = None
 
     def _c(self):
         return _Options(self.tol, self.max_iter, self.stagnation_window, self.stagnation_ratio, self.subsample,
@@ -465,8 +537,18 @@ class SolverContext:
         hist = np.empty((max(options.max_iter, 0) + 1) * 7, dtype=np.float64)
         nrec, stop = ctypes.c_int(), ctypes.c_int()
         opts = options._c()
-        _check(self._lib.asdsm_iterate(self._h, ctypes.byref(opts), _dptr(hist), ctypes.byref(nrec),
-                                       ctypes.byref(stop), _dptr(u), _dptr(r)))
+        if options.observer is None:
+            _check(self._lib.asdsm_iterate(self._h, ctypes.byref(opts), _dptr(hist), ctypes.byref(nrec),
+                                           ctypes.byref(stop), _dptr(u), _dptr(r)))
+        else:
+            def seen(hp, nr, up, rp, nn, _ctx):
+                h = np.ctypeslib.as_array(hp, shape=(max(nr, 1) * 7,))[: nr * 7].reshape(-1, 7)
+                options.observer(IterationState(
+                    np.ctypeslib.as_array(up, shape=(nn,)).copy(), np.ctypeslib.as_array(rp, shape=(nn,)).copy(),
+                    [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in h], ""))
+            cb = _OBSERVER_FN(seen)
+            _check(self._lib.asdsm_iterate_observed(self._h, ctypes.byref(opts), cb, None, _dptr(hist),
+                                                    ctypes.byref(nrec), ctypes.byref(stop), _dptr(u), _dptr(r)))
         rows = hist[: nrec.value * 7].reshape(-1, 7)
         history = [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in rows]
         return IterationState(u, r, history, _STOP.get(stop.value, "max_iter"))

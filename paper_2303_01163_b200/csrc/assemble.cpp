@@ -91,4 +91,48 @@ void sample_exact(const Mesh& m, const asdsm_cat::Problem& p, double* out) {
   for (auto& t : th) t.join();
 }
 
+bool uniform_coefficients(const Mesh& m, const asdsm_cat::Problem& p, double* alpha, double* beta) {
+  const int dim = m.dim;
+  for (int a = 0; a < 3; ++a) alpha[a] = beta[a] = 0.0;
+  asdsm_cat::Coord x0{0.0, 0.0, 0.0};
+  for (int a = 0; a < dim; ++a) x0[static_cast<size_t>(a)] = m.h[a];
+  for (int a = 0; a < dim; ++a) {
+    if (a == m.time_axis) continue;
+    alpha[a] = p.alpha[static_cast<size_t>(a)](x0);
+    beta[a] = p.beta[static_cast<size_t>(a)](x0);
+  }
+  const i64 rows = static_cast<i64>(m.nf[1]) * (dim == 3 ? m.nf[2] : 1);
+  std::vector<char> ok(static_cast<size_t>(rows), 1), pos(static_cast<size_t>(rows), 1);
+  auto work = [&](i64 r0, i64 r1) {
+    for (i64 row = r0; row < r1; ++row) {
+      const int j = static_cast<int>(row % m.nf[1]) + 1;
+      const int k = dim == 3 ? static_cast<int>(row / m.nf[1]) + 1 : 0;
+      for (int i = 1; i <= m.nf[0]; ++i) {
+        asdsm_cat::Coord x{static_cast<double>(i) * m.h[0], static_cast<double>(j) * m.h[1],
+                           dim == 3 ? static_cast<double>(k) * m.h[2] : 0.0};
+        for (int a = 0; a < dim; ++a) {
+          if (a == m.time_axis) continue;
+          const double al = p.alpha[static_cast<size_t>(a)](x);
+          if (!(al > 0.0)) pos[static_cast<size_t>(row)] = 0;
+          if (al != alpha[a] || p.beta[static_cast<size_t>(a)](x) != beta[a]) ok[static_cast<size_t>(row)] = 0;
+        }
+      }
+    }
+  };
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const i64 nt = std::min<i64>(hw, rows);
+  if (nt <= 1 || static_cast<i64>(m.nf[0]) * rows < 100000) {
+    work(0, rows);
+  } else {
+    std::vector<std::thread> th;
+    for (i64 t = 0; t < nt; ++t) th.emplace_back(work, rows * t / nt, rows * (t + 1) / nt);
+    for (auto& t : th) t.join();
+  }
+  for (char c : pos)
+    if (!c) throw AsdsmError(kError, "diffusion coefficient not positive");
+  for (char c : ok)
+    if (!c) return false;
+  return true;
+}
+
 }  // namespace asdsm_b200

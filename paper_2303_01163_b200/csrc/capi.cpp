@@ -3,6 +3,7 @@
 #include "../../include/asdsm_b200.h"
 
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -21,6 +22,7 @@ struct asdsm_plan {
 
 struct asdsm_problem {
   asdsm_cat::Problem p;
+  bool callbacks = false;  // caller-defined fields: constant or variable decided per plan
 };
 
 namespace {
@@ -85,6 +87,33 @@ int asdsm_problem_config(int config_id, uint64_t seed, asdsm_problem** out) {
     auto* p = new asdsm_problem;
     p->p = asdsm_cat::baseline_problem(config_id, seed);
     *out = p;
+  });
+}
+
+int asdsm_problem_create(const asdsm_problem_spec* spec, asdsm_problem** out) {
+  return guarded([&] {
+    if (!spec || !out) throw AsdsmError(kError, "null problem spec");
+    if (spec->dim != 2 && spec->dim != 3) throw AsdsmError(kDimensionMismatch, "problem dimension must be 2 or 3");
+    const int ns = spec->dim - (spec->time_dependent ? 1 : 0);
+    auto wrap = [&](const asdsm_field& f, const char* what) -> asdsm_cat::Field {
+      if (!f.fn) throw AsdsmError(kError, std::string("problem field missing: ") + what);
+      const asdsm_field_fn fn = f.fn;
+      void* ctx = f.ctx;
+      return [fn, ctx](const asdsm_cat::Coord& x) { return fn(x.data(), ctx); };
+    };
+    auto p = std::make_unique<asdsm_problem>();
+    p->callbacks = true;
+    p->p.dim = spec->dim;
+    p->p.time_dependent = spec->time_dependent != 0;
+    for (int a = 0; a < ns; ++a) {
+      p->p.alpha[static_cast<size_t>(a)] = wrap(spec->alpha[a], "alpha");
+      p->p.beta[static_cast<size_t>(a)] = wrap(spec->beta[a], "beta");
+    }
+    p->p.source = wrap(spec->source, "source");
+    p->p.boundary = wrap(spec->boundary, "boundary");
+    if (spec->exact.fn) p->p.exact = wrap(spec->exact, "exact");
+    p->p.constant_coeffs = false;
+    *out = p.release();
   });
 }
 
@@ -163,7 +192,16 @@ int asdsm_plan_create_problem(const asdsm_problem* problem, int dim, const int* 
       throw CudaError("no CUDA device: the B200 path has no CPU fallback");
     auto plan = std::make_unique<asdsm_plan>();
     ASDSM_CUDA_CHECK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
-    plan->solver = std::make_unique<Solver>(m, problem->p);
+    if (problem->callbacks) {
+      // caller-defined fields: constant coefficients iff every fine-node sample agrees (the
+      // operator the reference assembles is then exactly the constant-coefficient one)
+      asdsm_cat::Problem q = problem->p;
+      if (q.dim != dim) throw AsdsmError(kDimensionMismatch, "problem/mesh dimension mismatch");
+      q.constant_coeffs = uniform_coefficients(m, q, q.alpha_c.data(), q.beta_c.data());
+      plan->solver = std::make_unique<Solver>(m, q);
+    } else {
+      plan->solver = std::make_unique<Solver>(m, problem->p);
+    }
     *out = plan.release();
   });
 }
@@ -277,6 +315,27 @@ int asdsm_fetch(asdsm_plan* plan, void* stream, double* history, int* nrec, int*
 int asdsm_iterate(asdsm_plan* plan, const asdsm_iterate_options* opts, double* history, int* nrec, int* stop_code,
                   double* u_out, double* r_out) {
   const int rc = asdsm_iterate_async(plan, opts, nullptr);
+  if (rc != ASDSM_OK) return rc;
+  return asdsm_fetch(plan, nullptr, history, nrec, stop_code, u_out, r_out);
+}
+
+int asdsm_iterate_observed(asdsm_plan* plan, const asdsm_iterate_options* opts, asdsm_observer_fn observer,
+                           void* ctx, double* history, int* nrec, int* stop_code, double* u_out, double* r_out) {
+  const int rc = guarded([&] {
+    const RunOptions r = to_run(opts);
+    plan->max_iter_run = r.max_iter;
+    Solver& S = *plan->solver;
+    const size_t n = static_cast<size_t>(S.fine_size());
+    std::vector<double> rows, u(observer ? n : 0), res(observer ? n : 0);
+    std::function<bool(int)> hook = [&](int) {
+      bool active = true;
+      const int nr = S.snapshot(rows, active, observer ? u.data() : nullptr, observer ? res.data() : nullptr,
+                                plan->stream);
+      if (observer) observer(rows.data(), nr, u.data(), res.data(), static_cast<int64_t>(n), ctx);
+      return active;
+    };
+    S.run_observed(r, plan->stream, hook);
+  });
   if (rc != ASDSM_OK) return rc;
   return asdsm_fetch(plan, nullptr, history, nrec, stop_code, u_out, r_out);
 }

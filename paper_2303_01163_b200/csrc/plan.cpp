@@ -10,9 +10,12 @@ namespace asdsm_b200 {
 using ld = long double;
 using cld = std::complex<long double>;
 
-DeviceAlloc::~DeviceAlloc() {
+void DeviceAlloc::release_all() {
   for (void* p : ptrs) cudaFree(p);
+  ptrs.clear();
 }
+
+DeviceAlloc::~DeviceAlloc() { release_all(); }
 
 // MeshConfig::create (proj/src/mesh.cpp:47-76): same validation order and messages.
 Mesh Mesh::create(int dim, const int* nf, const int* nc, int time_axis) {

@@ -145,6 +145,7 @@ struct DeviceAlloc {
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
+  void release_all();  // frees every allocation made so far
   ~DeviceAlloc();
 };
 

@@ -99,15 +99,35 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     nholes *= m.nc[a] + 1;
   }
   if (!variable_) {
-    for (int a = 0; a < m.dim; ++a)
-      sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
-    sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
-    // 3D holes that fit the one-kernel fill (m <= 64 on the transform axes) need the Thomas
-    // pivot tables whatever the hole count (the fused kernel runs its own line solves), so the
-    // few-lines PCR choice is not taken for them
-    const bool fused3d_candidate = m.dim == 3 && hext[0] <= 64 && hext[1] <= 64;
-    sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1, fused3d_candidate ? std::max<i64>(nholes, 1 << 20) : nholes,
-                                 "hole block", m.dim == 2);
+    try {
+      for (int a = 0; a < m.dim; ++a)
+        sep_slab_[a] = build_sep_solver(dev_, m.dim, g_slab_[a].ext, st_slab_[a], tax, -1, 1, "slab " + std::to_string(a));
+      sep_coarse_ = build_sep_solver(dev_, m.dim, g_coarse_.ext, st_coarse_, tax, -1, 1, "coarse mesh");
+      // 3D holes that fit the one-kernel fill (m <= 64 on the transform axes) need the Thomas
+      // pivot tables whatever the hole count (the fused kernel runs its own line solves), so the
+      // few-lines PCR choice is not taken for them
+      const bool fused3d_candidate = m.dim == 3 && hext[0] <= 64 && hext[1] <= 64;
+      sep_hole_ = build_sep_solver(dev_, m.dim, hext, st_fine_, tax, -1,
+                                   fused3d_candidate ? std::max<i64>(nholes, 1 << 20) : nholes, "hole block", m.dim == 2);
+    } catch (const AsdsmError& e) {
+      if (e.code != kUnsupported || std::getenv("ASDSM_NO_SEPARABLE_FALLBACK")) throw;
+      dev_.release_all();
+      for (auto& S : sep_slab_) S = SepSolver{};
+      sep_coarse_ = SepSolver{};
+      sep_hole_ = SepSolver{};
+      const_fields_ = asdsm_cat::Problem{};
+      const_fields_.dim = m.dim;
+      const_fields_.time_dependent = m.time_axis >= 0;
+      const_fields_.constant_coeffs = false;
+      for (int a = 0; a < 3; ++a) {
+        const double al = alpha_[a], be = beta_[a];
+        const_fields_.alpha[static_cast<size_t>(a)] = [al](const asdsm_cat::Coord&) { return al; };
+        const_fields_.beta[static_cast<size_t>(a)] = [be](const asdsm_cat::Coord&) { return be; };
+      }
+      separable_fallback_ = true;
+      init(&const_fields_);
+      return;
+    }
   } else {
     // per-point stencils (fdm.cpp:63-126 sampling) + block-Thomas factors for every box
     const std::vector<double> cf = sample_kind_coefficients(m, 0u, *varprob);
@@ -792,6 +812,47 @@ void Solver::error_mode_guess(const double* r0, const double* r1, int k, double*
 }
 
 void Solver::run(const RunOptions& o, cudaStream_t s) {
+  prepare_run(o, s);
+  const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
+  if (no_graph || s == nullptr) {
+    const long long l0 = g_kernel_launches;
+    enqueue_run(o, s);
+    launches_ = g_kernel_launches - l0;
+    return;
+  }
+  run_graph(o, s);
+}
+
+void Solver::run_observed(const RunOptions& o, cudaStream_t s, const std::function<bool(int)>& after_record) {
+  prepare_run(o, s);
+  const long long l0 = g_kernel_launches;
+  enqueue_run(o, s, &after_record);
+  launches_ = g_kernel_launches - l0;
+}
+
+int Solver::snapshot(std::vector<double>& rows, bool& active, double* u_out, double* r_out, cudaStream_t s) {
+  if (!host_state_) ASDSM_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_state_), sizeof(DevState), 0));
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(host_state_, state_, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  const DevState h = *host_state_;
+  const int nrec = history_ ? std::min(h.nrec, history_cap_) : 0;
+  rows.resize(static_cast<size_t>(nrec) * 7);
+  const size_t nb = static_cast<size_t>(g_fine_.size) * sizeof(double);
+  if (nrec) ASDSM_CUDA_CHECK(cudaMemcpyAsync(rows.data(), history_, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (u_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(u_out, u_[h.cur], nb, cudaMemcpyDefault, s));
+  if (r_out) ASDSM_CUDA_CHECK(cudaMemcpyAsync(r_out, r_[h.cur], nb, cudaMemcpyDefault, s));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(s));
+  double prev = h.t0_ns;  // wall_ms per row, as fetch()
+  for (int k = 0; k < nrec; ++k) {
+    const double t = rows[static_cast<size_t>(k) * 7 + 6];
+    rows[static_cast<size_t>(k) * 7 + 6] = (t - prev) / 1e6;
+    prev = t;
+  }
+  active = h.active != 0;
+  return nrec;
+}
+
+void Solver::prepare_run(const RunOptions& o, cudaStream_t s) {
   last_opts_ = o;
   const int cap = std::max(o.max_iter, 0) + 1;
   if (cap > history_cap_) {
@@ -865,14 +926,9 @@ void Solver::run(const RunOptions& o, cudaStream_t s) {
     }
     ASDSM_CUDA_CHECK(cudaMemcpyAsync(sub_rows_, all.data(), all.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
   }
+}
 
-  const bool no_graph = std::getenv("ASDSM_NO_GRAPH") != nullptr;
-  if (no_graph || s == nullptr) {
-    const long long l0 = g_kernel_launches;
-    enqueue_run(o, s);
-    launches_ = g_kernel_launches - l0;
-    return;
-  }
+void Solver::run_graph(const RunOptions& o, cudaStream_t s) {
   const bool same = graph_exec_ && graph_opts_.tol == o.tol && graph_opts_.max_iter == o.max_iter &&
                     graph_opts_.stagnation_window == o.stagnation_window &&
                     graph_opts_.stagnation_ratio == o.stagnation_ratio && graph_opts_.subsample == o.subsample &&
@@ -942,7 +998,7 @@ static void record_graph_kernels(cudaGraph_t g, std::vector<std::pair<std::strin
   out.assign(count.begin(), count.end());
 }
 
-void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
+void Solver::enqueue_run(const RunOptions& o, cudaStream_t s, const std::function<bool(int)>* after_record) {
   reset_state(o, s);
   CtrlArgs c{};
   c.has_exact = has_exact_;
@@ -960,6 +1016,7 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
   const double* ex = has_exact_ ? exact_ : nullptr;
   march_launch(kMarchResidual, march_args(u_[0], u_[1], nullptr, b_, nullptr, nullptr, r_[0], r_[1], ex, fg_, st_fine_,
                                           partials_, state_, c, history_), s);
+  if (after_record && !(*after_record)(0)) return;
 
   // the step's dot products: their own pass, or (opt-in, ASDSM_DOTS_UPDATE=1) inside the update
   // launch with a grid barrier between the two phases -- measured slower in the captured graph
@@ -998,6 +1055,7 @@ void Solver::enqueue_run(const RunOptions& o, cudaStream_t s) {
       up.retry_pass = 1;
       march_launch(kMarchUpdate, up, s);
     }
+    if (after_record && !(*after_record)(k)) return;
   }
 }
 

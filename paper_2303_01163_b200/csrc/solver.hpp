@@ -2,6 +2,7 @@
 // SolverContext + asdsm_iterate (proj/include/asdsm/solver.hpp:114-163).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -37,6 +38,7 @@ class Solver {
   // Variable coefficients (ProblemSpec with per-point alpha/beta): per-point stencils and
   // block-Thomas direct solves.
   Solver(const Mesh& m, const asdsm_cat::Problem& problem);
+  bool separable_fallback() const { return separable_fallback_; }
   bool variable() const { return variable_; }
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
@@ -53,6 +55,12 @@ class Solver {
 
   // Initial guess + up to max_iter error-mode corrections, all control on the device.
   void run(const RunOptions& o, cudaStream_t s);
+  // IterateOptions::observer (solver.hpp:65): the solve launch by launch (no captured graph),
+  // `after_record(k)` on the host after record k is enqueued (k = 0 first); it returns false to
+  // stop enqueueing (the device state has stopped).  snapshot() reads the state in between.
+  void run_observed(const RunOptions& o, cudaStream_t s, const std::function<bool(int)>& after_record);
+  // history rows so far, and the current iterate / residual (host, nullable); returns nrec.
+  int snapshot(std::vector<double>& rows, bool& active, double* u_out, double* r_out, cudaStream_t s);
 
   // After run(): history rows (k, res_l2, res_inf, err_max, err_l2, s_hat, wall_ms).
   int history(std::vector<double>& rows, int& stop_code, cudaStream_t s);
@@ -92,7 +100,9 @@ class Solver {
 
  private:
   void reset_state(const RunOptions& o, cudaStream_t s);
-  void enqueue_run(const RunOptions& o, cudaStream_t s);
+  void enqueue_run(const RunOptions& o, cudaStream_t s, const std::function<bool(int)>* after_record = nullptr);
+  void prepare_run(const RunOptions& o, cudaStream_t s);
+  void run_graph(const RunOptions& o, cudaStream_t s);
   void smooth_guess(double* out, cudaStream_t s);
   void error_mode_guess(const double* r0, const double* r1, int k, double* out, cudaStream_t s);
   void skeleton(const double* const* sol, const double* u_cc, const int* coin, double* out, cudaStream_t s);
@@ -104,6 +114,12 @@ class Solver {
   BoxArray kind_array(const KindGeom& g, double* p) const;
 
   void init(const asdsm_cat::Problem* varprob);
+  // constant coefficients whose boxes the separable solvers cannot take (an eigenvector
+  // scaling too ill-conditioned on every candidate transform axis -- strong advection over a
+  // long box -- or complex modes on two diagonalized axes): the same operator as constant
+  // per-point fields on the block-Thomas path (no CPU fallback, no Unsupported)
+  asdsm_cat::Problem const_fields_{};
+  bool separable_fallback_ = false;
   void solve_box(int which, double* data, cudaStream_t s);
   void march_launch(int mode, struct MarchArgs A, cudaStream_t s);  // variable mode: 0..2 slab, 3 coarse, 4 holes
   Mesh mesh_;

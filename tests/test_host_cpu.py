@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(pb.library_path())
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert pb.load_library().asdsm_abi_version() == 3
+    assert pb.load_library().asdsm_abi_version() == 4
 
 
 @pytest.mark.parametrize("name", ["ex1s1_24_4", "ex3s1_24_4", "ex4s1_14_4", "cfg1_49_4", "cfg2_49_4", "cfg3_14_4",
@@ -126,3 +126,20 @@ def test_cxx_dropin_header_builds_and_fails_loudly_without_gpu(tmp_path):
     exe = build_example(tmp_path)
     rc, out = run_example(exe, 1, 1, 99, 9, 3)
     assert rc == 3 and out.startswith("error,CudaFailure"), out
+
+
+def test_reference_binding_has_no_cpu_fallback():
+    """The compiled reference-side binding (tests/cxx/ref_binding.cpp) raises the reference's
+    asdsm::Error from the C-ABI status when no GPU is present -- after the reference itself ran."""
+    import os
+    import subprocess
+    import tempfile
+    import torch
+    binp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "ref_binding")
+    if not os.path.exists(binp) or torch.cuda.is_available():
+        pytest.skip("needs the built binding and no GPU")
+    with tempfile.TemporaryDirectory() as d:
+        p = subprocess.run([binp, "ex:1:1", "49", "4", "2", "0", os.path.join(d, "o")], capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 3 and "no CUDA device" in p.stderr
+        assert os.path.exists(os.path.join(d, "o.ref.hist.txt"))
