@@ -183,6 +183,32 @@ int asdsm_initial_guess(asdsm_plan* plan, double* u_out);                       
 int asdsm_error_guess(asdsm_plan* plan, const double* r, uint64_t seed, double* e_out); /* solver.hpp:135 */
 int asdsm_optimal_scaling(asdsm_plan* plan, const double* r, const double* e, double* s_out); /* solver.hpp:109 */
 
+/* ---- public solver stages (solver.hpp:70-105; host arrays of this plan's mesh kinds) ------
+ * Single device operations with the reference's operation order (bitwise its results, except
+ * fill_holes whose direct solves round differently) and argument checks.  They reuse the plan's
+ * work buffers: a following asdsm_iterate re-initializes them. */
+/* richardson_extrapolate (solver.hpp:72-73): u1_cc + u2_cc - u_cc on the coarse mesh. */
+int asdsm_richardson_extrapolate(asdsm_plan* plan, const double* u1_cc, const double* u2_cc, const double* u_cc,
+                                 double* out);
+/* choose_cross_points (solver.hpp:78-79, 2D): the coarse restriction of u_cf (coarse along x) or
+ * u_fc (coarse along y) picked by mt19937_64(rng_seed). */
+int asdsm_choose_cross_points(asdsm_plan* plan, const double* u_fc, const double* u_cf, uint64_t rng_seed,
+                              double* out);
+/* spline_correct (solver.hpp:84-85, 2D): u_aniso (on the kind coarse along 1 - dense_axis) plus
+ * the zero-clamped natural cubic spline of the coarse correction e_cc along dense_axis. */
+int asdsm_spline_correct(asdsm_plan* plan, const double* u_aniso, const double* e_cc, int dense_axis, double* out);
+/* build_skeleton (solver.hpp:90-91, 2D; SkeletonInputs solver.hpp:23-29): u_cc given exactly when
+ * normalized == 0 (else InvalidKind); fine-mesh output, holes exactly zero. */
+int asdsm_build_skeleton(asdsm_plan* plan, const double* u_fc, const double* u_cf, const double* u_cc, int normalized,
+                         uint64_t rng_seed, double* out);
+/* merge_3d (solver.hpp:98-100): u_x/u_y/u_z on the kinds coarse along x/y/z, u_ccc nullable
+ * (error mode: seeded slab choices). */
+int asdsm_merge_3d(asdsm_plan* plan, const double* u_x, const double* u_y, const double* u_z, const double* u_ccc,
+                   uint64_t rng_seed, double* out);
+/* fill_holes (solver.hpp:104-105): the skeleton completed by the hole solves against b_fine
+ * (nullable: zero); SKELETON_NOT_HOLLOW when the input has values on hole positions. */
+int asdsm_fill_holes(asdsm_plan* plan, const double* skeleton, const double* b_fine, double* out);
+
 #ifdef __cplusplus
 }
 #endif

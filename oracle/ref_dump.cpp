@@ -6,11 +6,17 @@
 //   bundle   <spec> <nf> <nc> <prefix>                  SolverContext::assembled_bundle (solver.cpp:504)
 //   errguess <spec> <nf> <nc> <seed> <r.f64> <prefix>   SolverContext::error_guess (solver.cpp:550)
 //   maps     <spec> <nf> <nc> <prefix>                  build_projector / hole_blocks (mesh.cpp:210-305)
+//   stage    <name> <spec> <nf> <nc> <seed> <in> <out>  a public solver stage on fields read from
+//            <in>.<field>.f64 (solver.hpp:70-105): richardson (u1 u2 ucc), choose (ufc ucf),
+//            spline0 / spline1 (ua ecc; dense axis 0 / 1), skeleton_s (ufc ucf ucc), skeleton_e
+//            (ufc ucf), merge_s (ux uy uz uccc), merge_e (ux uy uz), fill (skel b) -> <out>.f64
 // <spec> is ex:E:S (reference example E, setting S, problems.cpp:114) or cfg:ID:SEED (a
 // BASELINE.json config from include/asdsm_problems.hpp).  nf/nc = 0 keeps the catalogue mesh.
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <optional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -204,6 +210,53 @@ int cmd_maps(int argc, char** argv) {
   return 0;
 }
 
+GridFunction read_field(const std::string& in, const char* name, const MeshKind& kind, const MeshConfig& m) {
+  GridFunction g(kind, m.point_count(kind));
+  std::ifstream f(in + "." + name + ".f64", std::ios::binary);
+  if (!f) throw std::runtime_error(std::string("missing input field ") + name);
+  f.read(reinterpret_cast<char*>(g.values.data()), static_cast<std::streamsize>(g.values.size() * sizeof(double)));
+  return g;
+}
+
+int cmd_stage(int argc, char** argv) {
+  if (argc < 9) return 2;
+  const std::string name = argv[2];
+  Case c = make_case(argv[3], std::atoi(argv[4]), std::atoi(argv[5]));
+  const std::uint64_t seed = std::strtoull(argv[6], nullptr, 10);
+  const std::string in = argv[7], out = argv[8];
+  const MeshConfig& m = c.mesh;
+  const int dim = m.dim;
+  const MeshKind cc = MeshKind::coarse(dim), ff = MeshKind::fine(dim);
+  auto slab = [&](int a) { return MeshKind::coarse_along(dim, a); };
+  GridFunction r;
+  if (name == "richardson") {
+    r = richardson_extrapolate(read_field(in, "u1", cc, m), read_field(in, "u2", cc, m), read_field(in, "ucc", cc, m));
+  } else if (name == "choose") {
+    SkeletonInputs si{read_field(in, "ufc", slab(1), m), read_field(in, "ucf", slab(0), m), std::nullopt, true};
+    r = choose_cross_points(si, m, seed);
+  } else if (name == "spline0" || name == "spline1") {
+    const int dense = name == "spline0" ? 0 : 1;
+    r = spline_correct(read_field(in, "ua", slab(1 - dense), m), read_field(in, "ecc", cc, m), dense, m);
+  } else if (name == "skeleton_s" || name == "skeleton_e") {
+    const bool smooth = name == "skeleton_s";
+    SkeletonInputs si{read_field(in, "ufc", slab(1), m), read_field(in, "ucf", slab(0), m), std::nullopt, !smooth};
+    if (smooth) si.u_cc = read_field(in, "ucc", cc, m);
+    r = build_skeleton(si, m, seed);
+  } else if (name == "merge_s" || name == "merge_e") {
+    std::optional<GridFunction> uccc;
+    if (name == "merge_s") uccc = read_field(in, "uccc", cc, m);
+    r = merge_3d(read_field(in, "ux", slab(0), m), read_field(in, "uy", slab(1), m), read_field(in, "uz", slab(2), m),
+                 uccc, m, seed);
+  } else if (name == "fill") {
+    const SolverContext ctx(m, c.problem);
+    r = fill_holes(read_field(in, "skel", ff, m), ctx.fine_operator(), read_field(in, "b", ff, m), m);
+  } else {
+    throw std::invalid_argument("unknown stage " + name);
+  }
+  write_bin(out + ".f64", r.values);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -217,6 +270,7 @@ int main(int argc, char** argv) {
     if (cmd == "bundle") return cmd_bundle(argc, argv);
     if (cmd == "errguess") return cmd_errguess(argc, argv);
     if (cmd == "maps") return cmd_maps(argc, argv);
+    if (cmd == "stage") return cmd_stage(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_dump: %s\n", e.what());
     return 3;

@@ -159,6 +159,12 @@ def load_library():
         "asdsm_initial_guess": (I, [P, D]),
         "asdsm_error_guess": (I, [P, D, ctypes.c_uint64, D]),
         "asdsm_optimal_scaling": (I, [P, D, D, D]),
+        "asdsm_richardson_extrapolate": (I, [P, D, D, D, D]),
+        "asdsm_choose_cross_points": (I, [P, D, D, ctypes.c_uint64, D]),
+        "asdsm_spline_correct": (I, [P, D, D, I, D]),
+        "asdsm_build_skeleton": (I, [P, D, D, D, I, ctypes.c_uint64, D]),
+        "asdsm_merge_3d": (I, [P, D, D, D, D, ctypes.c_uint64, D]),
+        "asdsm_fill_holes": (I, [P, D, D, D]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -577,6 +583,61 @@ class SolverContext:
         rows = hist[: nrec.value * 7].reshape(-1, 7)
         history = [IterationRecord(int(x[0]), x[1], x[2], x[3], x[4], x[5], x[6]) for x in rows]
         return IterationState(u, r, history, _STOP.get(stop.value, "max_iter"))
+
+    # ---- the reference's public solver stages (solver.hpp:70-105) on this plan's mesh ----------
+    def _kind_len(self, mask: int) -> int:
+        return self.config.point_count(MeshKind.from_mask(self.config.dim, mask))
+
+    def _in(self, a, mask):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.size != self._kind_len(mask):
+            raise DimensionMismatch("stage input has the wrong point count for its mesh kind")
+        return a
+
+    def richardson_extrapolate(self, u1_cc, u2_cc, u_cc) -> np.ndarray:
+        full = (1 << self.config.dim) - 1
+        ins = [self._in(x, full) for x in (u1_cc, u2_cc, u_cc)]
+        out = np.empty(self._kind_len(full))
+        _check(self._lib.asdsm_richardson_extrapolate(self._h, *[_dptr(x) for x in ins], _dptr(out)))
+        return out
+
+    def choose_cross_points(self, u_fc, u_cf, rng_seed: int = 0) -> np.ndarray:
+        a, b = self._in(u_fc, 2), self._in(u_cf, 1)
+        out = np.empty(self._kind_len(3))
+        _check(self._lib.asdsm_choose_cross_points(self._h, _dptr(a), _dptr(b), ctypes.c_uint64(rng_seed), _dptr(out)))
+        return out
+
+    def spline_correct(self, u_aniso, e_cc, dense_axis: int) -> np.ndarray:
+        if not 0 <= dense_axis <= 1:
+            raise IndexOutOfRange("dense_axis must be 0 or 1")
+        mask = 1 << (1 - dense_axis)
+        a, e = self._in(u_aniso, mask), self._in(e_cc, 3)
+        out = np.empty(a.size)
+        _check(self._lib.asdsm_spline_correct(self._h, _dptr(a), _dptr(e), int(dense_axis), _dptr(out)))
+        return out
+
+    def build_skeleton(self, u_fc, u_cf, u_cc=None, normalized: bool = False, rng_seed: int = 0) -> np.ndarray:
+        a, b = self._in(u_fc, 2), self._in(u_cf, 1)
+        c = None if u_cc is None else self._in(u_cc, 3)
+        out = np.empty(self.fine_size())
+        _check(self._lib.asdsm_build_skeleton(self._h, _dptr(a), _dptr(b), _dptr(c), int(bool(normalized)),
+                                              ctypes.c_uint64(rng_seed), _dptr(out)))
+        return out
+
+    def merge_3d(self, u_x, u_y, u_z, u_ccc=None, rng_seed: int = 0) -> np.ndarray:
+        ins = [self._in(x, 1 << a) for a, x in enumerate((u_x, u_y, u_z))]
+        c = None if u_ccc is None else self._in(u_ccc, 7)
+        out = np.empty(self.fine_size())
+        _check(self._lib.asdsm_merge_3d(self._h, *[_dptr(x) for x in ins], _dptr(c), ctypes.c_uint64(rng_seed),
+                                        _dptr(out)))
+        return out
+
+    def fill_holes(self, skeleton, b_fine=None) -> np.ndarray:
+        sk = self._in(skeleton, 0)
+        b = None if b_fine is None else self._in(b_fine, 0)
+        out = np.empty(sk.size)
+        _check(self._lib.asdsm_fill_holes(self._h, _dptr(sk), _dptr(b), _dptr(out)))
+        return out
 
     def variable(self) -> bool:
         """True when the plan runs the variable-coefficient (block-Thomas) path."""

@@ -431,4 +431,118 @@ int asdsm_optimal_scaling(asdsm_plan* plan, const double* r, const double* e, do
   });
 }
 
+// ---- public solver stages (solver.hpp:70-105) -------------------------------------------
+
+int asdsm_richardson_extrapolate(asdsm_plan* plan, const double* u1_cc, const double* u2_cc, const double* u_cc,
+                                 double* out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const size_t nb = static_cast<size_t>(S.kind_size((1u << S.mesh().dim) - 1u)) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.coarse_buffer(1), u1_cc, nb, cudaMemcpyHostToDevice, plan->stream));
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.coarse_buffer(2), u2_cc, nb, cudaMemcpyHostToDevice, plan->stream));
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.coarse_buffer(0), u_cc, nb, cudaMemcpyHostToDevice, plan->stream));
+    S.stage_richardson(S.coarse_buffer(1), S.coarse_buffer(2), S.coarse_buffer(0), S.coarse_buffer(1), plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(out, S.coarse_buffer(1), nb, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_choose_cross_points(asdsm_plan* plan, const double* u_fc, const double* u_cf, uint64_t rng_seed,
+                              double* out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    if (S.mesh().dim != 2) throw AsdsmError(kInvalidKind, "choose_cross_points: the 2D anisotropic meshes");
+    const int axis = S.cross_point_choice(rng_seed) == 0 ? 0 : 1;  // u_cf is coarse along 0, u_fc along 1
+    const size_t ns = static_cast<size_t>(S.kind_size(1u << axis)) * sizeof(double);
+    const size_t nb = static_cast<size_t>(S.kind_size(3u)) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.slab_buffer(axis), axis == 0 ? u_cf : u_fc, ns, cudaMemcpyHostToDevice,
+                                     plan->stream));
+    S.stage_restrict(S.slab_buffer(axis), axis, S.coarse_buffer(1), plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(out, S.coarse_buffer(1), nb, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int asdsm_spline_correct(asdsm_plan* plan, const double* u_aniso, const double* e_cc, int dense_axis, double* out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    if (S.mesh().dim != 2) throw AsdsmError(kInvalidKind, "spline correction applies to the 2D anisotropic meshes");
+    if (dense_axis < 0 || dense_axis > 1) throw AsdsmError(kIndexOutOfRange, "dense_axis must be 0 or 1");
+    const int other = 1 - dense_axis;
+    const size_t ns = static_cast<size_t>(S.kind_size(1u << other)) * sizeof(double);
+    const size_t nb = static_cast<size_t>(S.kind_size(3u)) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.slab_buffer(other), u_aniso, ns, cudaMemcpyHostToDevice, plan->stream));
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.coarse_buffer(1), e_cc, nb, cudaMemcpyHostToDevice, plan->stream));
+    S.stage_spline_correct(S.slab_buffer(other), S.coarse_buffer(1), dense_axis, S.slab_buffer(other), plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(out, S.slab_buffer(other), ns, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+namespace {
+void skeleton_call(asdsm_plan* plan, const double* const* sol, const double* u_cc, uint64_t seed, double* out) {
+  Solver& S = *plan->solver;
+  const int dim = S.mesh().dim;
+  double* dsol[3] = {nullptr, nullptr, nullptr};
+  for (int a = 0; a < dim; ++a) {
+    dsol[a] = S.slab_buffer(a);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(dsol[a], sol[a], static_cast<size_t>(S.kind_size(1u << a)) * sizeof(double),
+                                     cudaMemcpyHostToDevice, plan->stream));
+  }
+  if (u_cc)
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.coarse_buffer(0), u_cc,
+                                     static_cast<size_t>(S.kind_size((1u << dim) - 1u)) * sizeof(double),
+                                     cudaMemcpyHostToDevice, plan->stream));
+  const double* cs[3] = {dsol[0], dsol[1], dsol[2]};
+  S.stage_skeleton(cs, u_cc ? S.coarse_buffer(0) : nullptr, seed, S.e_buffer(), plan->stream);
+  ASDSM_CUDA_CHECK(cudaMemcpyAsync(out, S.e_buffer(), static_cast<size_t>(S.fine_size()) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, plan->stream));
+  ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+}
+}  // namespace
+
+int asdsm_build_skeleton(asdsm_plan* plan, const double* u_fc, const double* u_cf, const double* u_cc, int normalized,
+                         uint64_t rng_seed, double* out) {
+  return guarded([&] {
+    if (plan->solver->mesh().dim != 2) throw AsdsmError(kInvalidKind, "build_skeleton is the 2D path; merge_3d handles 3D");
+    if ((u_cc != nullptr) == (normalized != 0))
+      throw AsdsmError(kInvalidKind, "coarse solution must be present exactly for unnormalized inputs");
+    const double* sol[2] = {u_cf, u_fc};
+    skeleton_call(plan, sol, u_cc, rng_seed, out);
+  });
+}
+
+int asdsm_merge_3d(asdsm_plan* plan, const double* u_x, const double* u_y, const double* u_z, const double* u_ccc,
+                   uint64_t rng_seed, double* out) {
+  return guarded([&] {
+    if (plan->solver->mesh().dim != 3) throw AsdsmError(kInvalidKind, "merge_3d is the 3D path");
+    const double* sol[3] = {u_x, u_y, u_z};
+    skeleton_call(plan, sol, u_ccc, rng_seed, out);
+  });
+}
+
+int asdsm_fill_holes(asdsm_plan* plan, const double* skeleton, const double* b_fine, double* out) {
+  return guarded([&] {
+    Solver& S = *plan->solver;
+    const Mesh& m = S.mesh();
+    const i64 n = S.fine_size();
+    // SkeletonNotHollow (solver.cpp:420-421): the input must vanish on every hole position
+    for (i64 p = 0; p < n; ++p) {
+      i64 q = p;
+      bool hole = true;
+      for (int a = 0; a < m.dim && hole; ++a) {
+        hole = (static_cast<int>(q % m.nf[a]) + 1) % m.n[a] != 0;
+        q /= m.nf[a];
+      }
+      if (hole && skeleton[p] != 0.0) throw AsdsmError(kSkeletonNotHollow, "fill_holes: skeleton has values inside holes");
+    }
+    const size_t nb = static_cast<size_t>(n) * sizeof(double);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.e_buffer(), skeleton, nb, cudaMemcpyHostToDevice, plan->stream));
+    if (b_fine) ASDSM_CUDA_CHECK(cudaMemcpyAsync(S.r_buffer(1), b_fine, nb, cudaMemcpyHostToDevice, plan->stream));
+    S.stage_fill(S.e_buffer(), b_fine ? S.r_buffer(1) : nullptr, plan->stream);
+    ASDSM_CUDA_CHECK(cudaMemcpyAsync(out, S.e_buffer(), nb, cudaMemcpyDeviceToHost, plan->stream));
+    ASDSM_CUDA_CHECK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
 }  // extern "C"

@@ -71,6 +71,20 @@ class Solver {
   const double* r_current(cudaStream_t s) const;
   double* u_buffer(int i) { return u_[i]; }
   double* r_buffer(int i) { return r_[i]; }
+  // The reference's public stages (solver.hpp:70-105, stages.cu) on device arrays of this plan's
+  // mesh kinds: richardson_extrapolate, the coarse restriction choose_cross_points picks from
+  // (cross_point_choice: 0 = u_cf, 1 = u_fc), spline_correct, build_skeleton / merge_3d (sol[a]:
+  // the field on the kind coarse along a; u_cc null in error mode) and fill_holes (e: the
+  // skeleton in, completed out; b null: zero right-hand side).
+  void stage_richardson(const double* u1, const double* u2, const double* ucc, double* out, cudaStream_t s);
+  void stage_restrict(const double* slab, int axis, double* out, cudaStream_t s);
+  int cross_point_choice(std::uint64_t seed) const;
+  void stage_spline_correct(const double* u, const double* ecc, int dense, double* out, cudaStream_t s);
+  void stage_skeleton(const double* const* sol, const double* u_cc, std::uint64_t seed, double* out, cudaStream_t s);
+  void stage_fill(double* e, const double* b, cudaStream_t s);
+  double* slab_buffer(int a) { return sol_slab_[a]; }
+  double* coarse_buffer(int i) { return i == 0 ? u_cc_ : i == 1 ? cc_e1_ : cc_e2_; }
+  i64 kind_size(unsigned mask) const { return mask == 0 ? g_fine_.size : mask == (1u << mesh_.dim) - 1u ? g_coarse_.size : g_slab_[mask == 1u ? 0 : mask == 2u ? 1 : 2].size; }
   double* e_buffer() { return e_; }
   const double* b_fine() const { return b_; }
 
