@@ -14,6 +14,8 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
+#include <array>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -119,7 +121,8 @@ struct MeshConfig {
 // ---- problems (problems.hpp:20-29) ------------------------------------------------------
 class ProblemSpec {
  public:
-  explicit ProblemSpec(asdsm_problem* h) : h_(h, asdsm_problem_destroy) {
+  explicit ProblemSpec(asdsm_problem* h, std::shared_ptr<void> keep = nullptr)
+      : h_(h, asdsm_problem_destroy), keep_(std::move(keep)) {
     double al[3], be[3];
     check(asdsm_problem_info(h, &dim_, &time_dependent_, &constant_coeffs_, al, be, &has_exact_));
   }
@@ -145,8 +148,43 @@ class ProblemSpec {
 
  private:
   std::shared_ptr<asdsm_problem> h_;
+  std::shared_ptr<void> keep_;  // caller-defined fields the library calls back into
   int dim_ = 0, time_dependent_ = 0, constant_coeffs_ = 0, has_exact_ = 0;
 };
+
+// A caller-defined problem (fdm.hpp:17-30): the reference's ProblemSpec fields as callables of a
+// point (axes beyond dim are zero), passed to the library as callbacks (asdsm_problem_create).
+using Coord = std::array<double, 3>;
+using ScalarField = std::function<double(const Coord&)>;
+struct FieldSpec {
+  int dim = 2;
+  bool time_dependent = false;
+  std::array<ScalarField, 3> alpha{}, beta{};  // per spatial axis
+  ScalarField source, boundary, exact;         // exact optional
+  int spatial_axes() const { return time_dependent ? dim - 1 : dim; }
+};
+
+inline ProblemSpec make_problem(const FieldSpec& fields) {
+  auto keep = std::make_shared<FieldSpec>(fields);
+  auto call = [](const double* x, void* ctx) {
+    const Coord c{x[0], x[1], x[2]};
+    return (*static_cast<const ScalarField*>(ctx))(c);
+  };
+  auto field = [&](const ScalarField& f) { return asdsm_field{f ? +call : nullptr, const_cast<ScalarField*>(&f)}; };
+  asdsm_problem_spec spec{};
+  spec.dim = keep->dim;
+  spec.time_dependent = keep->time_dependent ? 1 : 0;
+  for (int a = 0; a < keep->spatial_axes(); ++a) {
+    spec.alpha[a] = field(keep->alpha[static_cast<size_t>(a)]);
+    spec.beta[a] = field(keep->beta[static_cast<size_t>(a)]);
+  }
+  spec.source = field(keep->source);
+  spec.boundary = field(keep->boundary);
+  spec.exact = field(keep->exact);
+  asdsm_problem* h = nullptr;
+  check(asdsm_problem_create(&spec, &h));
+  return ProblemSpec(h, keep);
+}
 
 inline ProblemSpec make_problem(int example, int setting) {  // problems.hpp:20
   asdsm_problem* h = nullptr;
@@ -191,7 +229,7 @@ struct IterationState {  // solver.hpp:54-59 (u, r: GridFunction::values on the 
   std::string stop_reason;  // "tol" | "max_iter" | "stagnation"
 };
 
-struct IterateOptions {  // solver.hpp:56-68 (no observer: the loop runs on the device)
+struct IterateOptions {  // solver.hpp:56-68
   double tol = 1e-12;
   int max_iter = 20;
   int stagnation_window = 3;
@@ -199,6 +237,9 @@ struct IterateOptions {  // solver.hpp:56-68 (no observer: the loop runs on the 
   double subsample = 0.0;
   std::uint64_t rng_seed = 0;
   bool sparse_residual = false;
+  // called after each recorded iteration, k = 0 first (asdsm_iterate_observed: the solve runs
+  // launch by launch with one synchronize per iteration instead of the captured graph)
+  std::function<void(const IterationState&)> observer;
 };
 
 // SolverContext (solver.hpp:114-155): device-resident operators, tables and rhs bundle.
@@ -281,6 +322,18 @@ class SolverContext {
       for (int a = 0; a < config_.dim; ++a) slabs[a] = b->aniso[static_cast<size_t>(a)].data();
       check(asdsm_solve(plan_.get(), b->fine.data(), slabs, b->coarse.data(), exact_.empty() ? nullptr : exact_.data(),
                         &c, hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
+    } else if (o.observer) {
+      auto obs = [](const double* h, int nr, const double* u, const double* r, std::int64_t nn, void* ctx) {
+        IterationState s;
+        s.u.assign(u, u + nn);
+        s.r.assign(r, r + nn);
+        for (int k = 0; k < nr; ++k)
+          s.history.push_back({static_cast<int>(h[7 * k]), h[7 * k + 1], h[7 * k + 2], h[7 * k + 3], h[7 * k + 4],
+                               h[7 * k + 5], h[7 * k + 6]});
+        (*static_cast<const std::function<void(const IterationState&)>*>(ctx))(s);
+      };
+      check(asdsm_iterate_observed(plan_.get(), &c, obs, const_cast<std::function<void(const IterationState&)>*>(&o.observer),
+                                   hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
     } else {
       check(asdsm_iterate(plan_.get(), &c, hist.data(), &nrec, &stop, st.u.data(), st.r.data()));
     }

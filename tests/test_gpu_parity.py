@@ -391,7 +391,10 @@ def test_stream3d_tma_pass_bitwise(spec, nf, nc, iters, monkeypatch):
     assert_variant_ran(ctx, ctx1)
     assert any("stream3d_kernel" in k for k in ctx1.kernels()), sorted(ctx1.kernels())
     assert np.array_equal(st_d.u, st_t.u) and np.array_equal(st_d.r, st_t.r)
-    assert np.array_equal(np.array([h.res_l2 for h in st_d.history]), np.array([h.res_l2 for h in st_t.history]))
+    # (the norms are reduced over another grid shape: the same values summed in another order)
+    a = np.array([h.res_l2 for h in st_d.history])
+    b = np.array([h.res_l2 for h in st_t.history])
+    assert np.all(np.abs(a - b) <= 1e-14 * b)
 
 
 @pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])

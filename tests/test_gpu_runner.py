@@ -90,6 +90,17 @@ def test_cxx_dropin_header_matches_python_api(tmp_path):
     exe = build_example(tmp_path)
     rc, out = run_example(exe, 1, 1, 99, 9, 8, 2)
     assert rc == 0, out
+    # the same problem as caller-defined fields (FieldSpec -> asdsm_problem_create) with an
+    # observer (asdsm_iterate_observed): the identical history, every record observed in order
+    import os
+    os.environ["ASDSM_EXAMPLE_FIELDS"] = "1"
+    try:
+        rc2, out2 = run_example(exe, 1, 1, 99, 9, 8, 2)
+    finally:
+        del os.environ["ASDSM_EXAMPLE_FIELDS"]
+    assert rc2 == 0, out2
+    lines2 = out2.strip().splitlines()
+    assert lines2[0] == "observed,9" and lines2[1:] == out.strip().splitlines(), out2
     rows = [line.split(",") for line in out.strip().splitlines()]
     assert rows[-1] == ["stop", "max_iter"]
     got = np.array([[float(x) for x in r] for r in rows[:-1]])
