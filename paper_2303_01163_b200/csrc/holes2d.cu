@@ -993,7 +993,8 @@ template <int NS, int kSepRowsKG = sep_rows_kg(NS)>
 __global__ void __launch_bounds__(kSepRowsJ * kSepRowsKG) hole2d_sep_rows_kernel(const double* __restrict__ modes,
                                                                                 const double* __restrict__ V,
                                                                                 double* __restrict__ e, Hole2DArgs A,
-                                                                                const DevState* state) {
+                                                                                const DevState* state,
+                                                                                double* __restrict__ dense) {
   if (!state->active || !state->have_e) return;
   extern __shared__ double vs[];  // [s][k]: rows i_s of V, then the k-group partials [g][s][jj]
   const int m0 = A.m0, m1 = A.m1, w1 = (m0 + 1) / (NS + 1);
@@ -1038,28 +1039,50 @@ __global__ void __launch_bounds__(kSepRowsJ * kSepRowsKG) hole2d_sep_rows_kernel
     double v = 0.0;
 #pragma unroll
     for (int gg = 0; gg < kSepRowsKG; ++gg) v += part[(gg * NS + q) * kSepRowsJ + jj];
-    out[(q + 1) * w1 - 1] = v;
+    if (dense) dense[(static_cast<i64>(hole) * NS + q) * m1 + j] = v;  // [hole][s][j]
+    else out[(q + 1) * w1 - 1] = v;
+  }
+}
+
+// Separator values [s][j] (one column per hole, from the separator GEMM) into the fine array.
+__global__ void hole2d_sep_scatter_kernel(const double* __restrict__ sep, double* __restrict__ e, Hole2DArgs A,
+                                          int p, const DevState* state) {
+  if (!state->active || !state->have_e) return;
+  const int m1 = A.m1, ns = p - 1, w1 = (A.m0 + 1) / p;
+  const int hole = blockIdx.x;
+  const int hx = hole % A.nbox0, hy = hole / A.nbox0;
+  const double* src = sep + static_cast<i64>(hole) * ns * m1;
+  for (int t = threadIdx.x; t < ns * m1; t += blockDim.x) {
+    const int q = t / m1, j = t - q * m1;
+    e[static_cast<i64>(hy * A.n1 + j) * A.nf0 + hx * A.n0 + (q + 1) * w1 - 1] = src[t];
   }
 }
 }  // namespace
 
+void launch_hole2d_sep_scatter(const double* sep, double* e, const Hole2DArgs& A, int p, DevState* state,
+                               cudaStream_t s) {
+  hole2d_sep_scatter_kernel<<<static_cast<unsigned>(A.nbox0 * A.nbox1), 256, 0, s>>>(sep, e, A, p, state);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
 void launch_hole2d_sep_rows(const double* modes, const double* V, double* e, const Hole2DArgs& A, int p,
-                            DevState* state, cudaStream_t s) {
+                            DevState* state, cudaStream_t s, double* dense) {
   if (p < 2 || p > 10 || (A.m0 + 1) % p != 0) throw AsdsmError(kUnsupported, "hole strip split");
   const dim3 grid(static_cast<unsigned>(A.nbox0 * A.nbox1), static_cast<unsigned>((A.m1 + kSepRowsJ - 1) / kSepRowsJ));
   const size_t smem = sizeof(double) * static_cast<size_t>(p - 1) * (A.m0 + sep_rows_kg(p - 1) * kSepRowsJ);
   if (smem > 48 * 1024) throw AsdsmError(kUnsupported, "hole strip split: separator table exceeds shared memory");
   const unsigned nt = kSepRowsJ * sep_rows_kg(p - 1);
   switch (p - 1) {
-    case 1: hole2d_sep_rows_kernel<1><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 2: hole2d_sep_rows_kernel<2><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 3: hole2d_sep_rows_kernel<3><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 4: hole2d_sep_rows_kernel<4><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 5: hole2d_sep_rows_kernel<5><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 6: hole2d_sep_rows_kernel<6><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 7: hole2d_sep_rows_kernel<7><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    case 8: hole2d_sep_rows_kernel<8><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
-    default: hole2d_sep_rows_kernel<9><<<grid, nt, smem, s>>>(modes, V, e, A, state); break;
+    case 1: hole2d_sep_rows_kernel<1><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 2: hole2d_sep_rows_kernel<2><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 3: hole2d_sep_rows_kernel<3><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 4: hole2d_sep_rows_kernel<4><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 5: hole2d_sep_rows_kernel<5><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 6: hole2d_sep_rows_kernel<6><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 7: hole2d_sep_rows_kernel<7><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    case 8: hole2d_sep_rows_kernel<8><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
+    default: hole2d_sep_rows_kernel<9><<<grid, nt, smem, s>>>(modes, V, e, A, state, dense); break;
   }
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;

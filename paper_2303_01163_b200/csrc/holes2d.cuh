@@ -64,6 +64,14 @@ void launch_hole2d_part(double* modes, const Hole2DArgs& A, const Hole2DPartArgs
 // holes of their own (Dirichlet data: skeleton and separators) with w-point transforms, so the
 // back transform costs w instead of m0 per point.
 void launch_hole2d_sep_rows(const double* modes, const double* V, double* e, const Hole2DArgs& A, int p,
-                            DevState* state, cudaStream_t s);
+                            DevState* state, cudaStream_t s, double* dense = nullptr);
+// The separator values can also come from one GEMM per iteration: the solution on the separators
+// is linear in the hole's ring right-hand side (2 m1 + 2 m0 values, holes2d ring layout), so
+// sep = K ring with K the (p-1) m1 x (2 m1 + 2 m0) separator response matrix -- the same for
+// every hole (congruent holes), built once at plan creation by running the mode-line and
+// separator kernels on unit rings (dense != nullptr: [hole][s][j] output instead of the fine
+// array).  launch_hole2d_sep_scatter writes the GEMM's [hole][s][j] columns into the fine array.
+void launch_hole2d_sep_scatter(const double* sep, double* e, const Hole2DArgs& A, int p, DevState* state,
+                               cudaStream_t s);
 
 }  // namespace asdsm_b200

@@ -7,6 +7,8 @@
 // without host synchronization and can be captured in a CUDA graph.
 #include "solver.hpp"
 
+#include <cublas_v2.h>
+
 #include "dmma_gemm.cuh"
 #include "holes2d.cuh"
 #include "holes3d.cuh"
@@ -330,6 +332,7 @@ void Solver::init(const asdsm_cat::Problem* varprob) {
     }
   }
   ASDSM_CUDA_CHECK(cudaMemset(exact_, 0, sizeof(double) * static_cast<size_t>(nf)));
+  if (strip_p_ && std::getenv("ASDSM_SEP_MODES") == nullptr) build_separator_matrix();
   dots_update_ok_ = !variable_ && mesh_.dim == 2 && std::getenv("ASDSM_DOTS_UPDATE") != nullptr &&
                     dots_update_supported(fg_);
 }
@@ -368,7 +371,57 @@ void Solver::set_bundle(const double* b_fine, const double* const* b_slab, const
   if (exact) ASDSM_CUDA_CHECK(cudaMemcpyAsync(exact_, exact, nf, kind, s));
 }
 
+// The separator response matrix K of the strip split: column c is the solution on the p - 1
+// separator columns of one hole for the ring right-hand side e_c (holes2d ring layout fL fR fB
+// fT).  Built with the iteration's own kernels -- the mode lines of `nholes` virtual holes with
+// unit rings per batch, then the separator product in its dense-output form -- so K carries
+// exactly the arithmetic of the per-iteration separator path it replaces.
+void Solver::build_separator_matrix() {
+  const SepSolver& H = sep_hole_;
+  const int m0 = H.ext[0], m1 = H.ext[1];
+  const i64 nholes = static_cast<i64>(mesh_.nc[0] + 1) * (mesh_.nc[1] + 1);
+  sep_rows_ = (strip_p_ - 1) * m1;
+  sep_cols_ = 2 * m1 + 2 * m0;
+  const i64 batches = (sep_cols_ + nholes - 1) / nholes;
+  sep_K_ = dev_.alloc<double>(static_cast<size_t>(batches * nholes) * sep_rows_);
+  sep_C_ = dev_.alloc<double>(static_cast<size_t>(nholes) * sep_rows_);
+  Hole2DArgs A{};
+  A.m0 = m0;
+  A.m1 = m1;
+  A.n0 = mesh_.n[0];
+  A.n1 = mesh_.n[1];
+  A.nf0 = mesh_.nf[0];
+  A.nf1 = mesh_.nf[1];
+  A.nbox0 = mesh_.nc[0] + 1;
+  A.nbox1 = mesh_.nc[1] + 1;
+  A.st = st_fine_;
+  A.line_left = H.line_left;
+  A.line_right = H.line_right;
+  const Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
+  double* modes = static_cast<double*>(scratch0_);
+  hole2d_prepare(113 * 1024);  // kernel attributes (dynamic shared memory) of the hole kernels
+  std::vector<double> unit(static_cast<size_t>(nholes) * sep_cols_);
+  cudaStream_t s = nullptr;
+  launch_state_init(state_, 1, 1, s);
+  for (i64 b = 0; b < batches; ++b) {
+    std::fill(unit.begin(), unit.end(), 0.0);
+    for (i64 h = 0; h < nholes && b * nholes + h < sep_cols_; ++h) unit[static_cast<size_t>(h * sep_cols_ + b * nholes + h)] = 1.0;
+    ASDSM_CUDA_CHECK(cudaMemcpy(hole_ring_, unit.data(), unit.size() * sizeof(double), cudaMemcpyHostToDevice));
+    launch_hole2d_part(modes, A, P, state_, s);
+    launch_hole2d_sep_rows(modes, H.V[0], nullptr, A, strip_p_, state_, s, sep_K_ + b * nholes * sep_rows_);
+  }
+  ASDSM_CUDA_CHECK(cudaDeviceSynchronize());
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+  blas_ = h;
+  const size_t ws = 32u << 20;
+  ASDSM_CUDA_CHECK(cudaMalloc(&blas_ws_, ws));
+  if (cublasSetWorkspace(h, blas_ws_, ws) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetWorkspace failed");
+}
+
 Solver::~Solver() {
+  if (blas_) cublasDestroy(static_cast<cublasHandle_t>(blas_));
+  if (blas_ws_) cudaFree(blas_ws_);
   if (host_state_) cudaFreeHost(host_state_);
   if (host_hist_) cudaFreeHost(host_hist_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -586,15 +639,28 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
     const bool strips = part && strip_p_ > 0;
     const SepSolver& T = strips ? sep_strip_ : H;
     if (stage & kFillLines) {
+      const bool gemm = strips && sep_K_ != nullptr;
       if (part) {
         Hole2DPartArgs P{H.W[0], H.part, H.part_stride, H.part_seg, H.part_P, H.part_last, hole_ring_};
         launch_hole2d_ring(e, A, P, state_, s);
-        launch_hole2d_part(modes, A, P, state_, s);
+        if (!gemm) launch_hole2d_part(modes, A, P, state_, s);
       } else {
         launch_hole2d_fwd_thomas(e, modes, A, state_, s);
       }
-      if (strips) {
+      if (gemm) {
+        // separators = K ring for every hole at once (cuBLAS DGEMM, captured into the graph)
+        cublasHandle_t h = static_cast<cublasHandle_t>(blas_);
+        if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream failed");
+        const double one = 1.0, zero = 0.0;
+        const int nh = A.nbox0 * A.nbox1;
+        if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, sep_rows_, nh, sep_cols_, &one, sep_K_, sep_rows_, hole_ring_,
+                        sep_cols_, &zero, sep_C_, sep_rows_) != CUBLAS_STATUS_SUCCESS)
+          throw CudaError("cublasDgemm (hole separators) failed");
+        launch_hole2d_sep_scatter(sep_C_, e, A, strip_p_, state_, s);
+      } else if (strips) {
         launch_hole2d_sep_rows(modes, H.V[0], e, A, strip_p_, state_, s);
+      }
+      if (strips) {
         const int w = T.ext[0];
         A.m0 = w;
         A.n0 = w + 1;

@@ -177,6 +177,14 @@ class Solver {
   int strip_p_ = 0;
   SepSolver sep_strip_{};
   double* strip_ring_ = nullptr;
+  // the separators from one GEMM with the separator response matrix K ((p-1) m1 x (2 m1 + 2 m0),
+  // column-major, built at plan creation; holes2d.cuh): sep = K ring, on cuBLAS
+  double* sep_K_ = nullptr;
+  double* sep_C_ = nullptr;  // [hole][(p-1) m1]
+  int sep_rows_ = 0, sep_cols_ = 0;
+  void* blas_ = nullptr;     // cublasHandle_t
+  void* blas_ws_ = nullptr;  // its workspace (set explicitly: no allocation during stream capture)
+  void build_separator_matrix();
   bool dots_update_ok_ = false;                 // kMarchDotsUpdate on (ASDSM_DOTS_UPDATE=1) and applicable
   // optimal-step dot products over the skeleton rows only (ASDSM_FULL_DOTS=1: every row)
   bool skel_dots_ = std::getenv("ASDSM_FULL_DOTS") == nullptr;                          // one-launch slab step (slabstep2d.cu) eligible

@@ -405,7 +405,7 @@ def test_hole_strip_split_agrees(spec, nf, nc, iters, monkeypatch):
     opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=4)
     ctx, _, _ = _ctx(spec, nf, nc)
     st_s = ctx.iterate(opts)
-    assert any("hole2d_sep_rows_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
+    assert any("hole2d_sep_scatter_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
     monkeypatch.setenv("ASDSM_STRIPS", "0")
     ctx1, _, _ = _ctx(spec, nf, nc)
     st_w = ctx1.iterate(opts)
@@ -416,3 +416,23 @@ def test_hole_strip_split_agrees(spec, nf, nc, iters, monkeypatch):
     assert len(a) == len(b)
     assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
     assert np.max(np.abs(st_s.u - st_w.u)) <= 1e-8 * np.max(np.abs(st_w.u))
+
+
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])
+def test_separator_gemm_agrees(spec, nf, nc, iters, monkeypatch):
+    """The strip split's separators from one GEMM with the separator response matrix K (default;
+    K built at plan creation from the iteration's own mode-line and separator kernels on unit
+    rings) against the per-iteration mode lines + separator product (ASDSM_SEP_MODES=1)."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=4)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_g = ctx.iterate(opts)
+    monkeypatch.setenv("ASDSM_SEP_MODES", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_m = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    assert any("hole2d_sep_rows_kernel" in k for k in ctx1.kernels()), sorted(ctx1.kernels())
+    a = np.array([h.res_l2 for h in st_g.history])
+    b = np.array([h.res_l2 for h in st_m.history])
+    k = np.arange(len(b))
+    assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
+    assert np.max(np.abs(st_g.u - st_m.u)) <= 1e-8 * np.max(np.abs(st_m.u))
