@@ -400,7 +400,9 @@ void launch_variant(const MarchArgs& A, const S3Geo& G, const S3Maps& M, size_t 
 }  // namespace
 
 // ASDSM_STREAM3D=1 (read at launch / capture) selects this pass; the default is the axpy +
-// z-coarsened residual passes (march.cu).
+// z-coarsened residual passes (march.cu), measured faster for the update: config 4 1.83 vs
+// 1.43 ms per update (2.9 vs 3.7 TB/s of the algorithmic 40 B/point) -- the residual mode alone
+// matches the default (0.81 vs 0.83 ms, 3.9 TB/s).  See DESIGN.md "Measured and not kept".
 bool stream3d_supported(const MarchArgs& A) {
   if (A.g.dim != 3 || A.coef != nullptr || A.g.stride[1] != A.g.ext[0] || !std::getenv("ASDSM_STREAM3D")) return false;
   S3Geo G = s3_geo(A.g);

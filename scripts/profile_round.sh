@@ -1,36 +1,32 @@
 #!/bin/bash
-# One profiling pass of the current build (run under gpurun from the repo root):
-#   bench (all configs) + reference arm, ncu launch lists of one solve per config, and one
-#   `ncu --set full` capture per top kernel.  Writes gpurun_out/prof_<tag>/...
+# Profiling pass of the current build (run under gpurun from the repo root).
+#   bash scripts/profile_round.sh TAG bench   : bench (all configs) + reference arm + ncu launch lists
+#   bash scripts/profile_round.sh TAG full    : one `ncu --set full` capture per top kernel
+# Writes gpurun_out/prof_<tag>/...  (gpurun's ncu wrapper runs each command once without ncu first)
 tag=${1:-r2}
+what=${2:-bench}
 out=gpurun_out/prof_$tag
 mkdir -p $out
-python bench.py > $out/bench.json 2> $out/bench.err
-python bench.py --impl reference > $out/bench_ref.json 2> $out/bench_ref.err
-for c in 1 2 3 4; do
-  python scripts/one_solve.py $c 1 > $out/plain_c$c.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $out/launches_c$c.csv \
-      python scripts/one_solve.py $c 1 > $out/ncu_launch_c$c.log 2>&1
-done
-full() {  # config, kernel regex, skip, name
-  python scripts/one_solve.py $1 1 > $out/plain_full.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 1 -o $out/full_c$1_$4 \
-      python scripts/one_solve.py $1 1 > $out/ncu_full_c$1_$4.log 2>&1
-}
-full 1 "stencil2d_yc_kernel" 5 update
-full 1 "hole2d_fused_kernel" 5 hole
-full 1 "slabstep2d_kernel" 5 slabstep
-full 1 "skel2d_dots_kernel" 5 dots
-full 2 "stencil2d_yc_kernel" 5 update
-full 2 "dmma_eo2_kernel" 5 back
-full 2 "hole2d_part_kernel" 6 lines
-full 2 "hole2d_sep_rows_kernel" 3 seprows
-full 2 "slab2d_fwd_kernel" 3 slabfwd
-full 3 "hole3d_fused_kernel" 3 hole
-full 3 "stencil3d_zc_kernel" 3 cand
-full 3 "axpy_update_kernel" 3 axpy
-full 3 "part_line_kernel" 3 slablines
-full 4 "hole3d_fused_kernel" 3 hole
-full 4 "stencil3d_zc_kernel" 3 cand
-full 4 "axpy_update_kernel" 3 axpy
-echo done > $out/DONE
+if [ "$what" = bench ]; then
+  python bench.py > $out/bench.json 2> $out/bench.err
+  python bench.py --impl reference > $out/bench_ref.json 2> $out/bench_ref.err
+  for c in 1 2 3 4; do
+    ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $out/launches_c$c.csv \
+        python scripts/one_solve.py $c 1 > $out/ncu_launch_c$c.log 2>&1
+  done
+else
+  full() {  # config, kernel regex, skip, name
+    ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 1 -o $out/full_c$1_$4 \
+        python scripts/one_solve.py $1 1 > $out/ncu_full_c$1_$4.log 2>&1
+  }
+  full 1 "hole2d_fused_kernel" 5 hole
+  full 1 "stencil2d_yc_kernel" 5 update
+  full 2 "dmma_eo2_kernel" 5 back
+  full 2 "stencil2d_yc_kernel" 5 update
+  full 2 "hole2d_part_kernel" 5 lines
+  full 3 "hole3d_fused_kernel" 3 hole
+  full 4 "hole3d_fused_kernel" 3 hole
+  full 4 "stencil3d_zc_kernel" 3 cand
+  full 4 "axpy_update_kernel" 3 axpy
+fi
+echo done > $out/DONE_$what
