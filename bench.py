@@ -56,19 +56,24 @@ def config_dict(cid, world):
             "l2": "GPU arm: flushed between steps (256 MB write)",
             "parallelism": f"replicas x{world}" if world > 1 else "1gpu"}
 # Bounded CPU samples of the reference per config: (nf, nc, iterations run, what).  Full solves
-# where they take seconds; the full mesh with 1 iteration for configs 2 and 3 (the rate of a
-# K-iteration solve is extrapolated from the measured initial-guess and iteration times); for
-# config 4 (509^3 does not fit a bounded sample: ~1000 hole solves of 50^3 per iteration) the
-# reference on 101^3 at N_c = 1, i.e. the same 50^3 space-time holes and the same ratio of hole,
-# skeleton and fine work per DOF.
+# where they take seconds; the full mesh with 1 iteration for config 2 (the rate of a K-iteration
+# solve is extrapolated from the measured initial-guess and iteration times).  The 3D meshes do
+# not fit a bounded sample on the host (the reference factors three 9 x 259 x 259 slabs and a
+# 25^3 / 50^3 hole block with a band LU: hours), so config 3 is sampled on 103^3 at N_c = 3 (the
+# config's 25^3 holes) and config 4 on 81^3 at N_c = 1 (40^3 space-time holes; the config's 50^3
+# block alone takes minutes to factor): the same ratio of hole, skeleton and fine work per DOF,
+# with the rate per DOF extrapolated.  Measured wall times incl. setup on 8 cores: 0.1 / 3 / 40 /
+# 8 / 29 s.
 CPU_SAMPLE = [
     (0, 0, 10, "full solve (initial guess + 10 iterations) at the config's mesh"),
     (0, 0, 20, "full solve (initial guess + 20 iterations) at the config's mesh"),
     (0, 0, 1, "the config's full 4099^2 mesh: initial guess + 1 iteration timed, the 20-iteration rate extrapolated"),
-    (0, 0, 1, "the config's full 259^3 mesh: initial guess + 1 iteration timed, the 10-iteration rate extrapolated"),
-    (101, 1, 1, "101^3 at N_c=1 (the config's 50^3 space-time holes): initial guess + 1 iteration timed, "
-                "the 10-iteration rate per DOF extrapolated"),
+    (103, 3, 1, "103^3 at N_c=3 (the config's 25^3 holes; the full 259^3 slabs take hours to factor on the host): "
+                "initial guess + 1 iteration timed, the 10-iteration rate per DOF extrapolated"),
+    (81, 1, 1, "81^3 at N_c=1 (40^3 space-time holes; the config's 50^3 hole block takes minutes to factor on the "
+               "host): initial guess + 1 iteration timed, the 10-iteration rate per DOF extrapolated"),
 ]
+CPU_SAMPLE_TIMEOUT_S = 240  # a sample that overruns is reported as unavailable, never waited for
 FP64_PEAK_TFLOPS = 37.0  # measured on this pool's B200 (scripts/probe_fp64.cu: DMMA 37.0, DFMA 36.6)
 REF_DUMP = os.path.join(ROOT, "oracle", "_ref", "ref_dump")
 
@@ -100,8 +105,8 @@ def reference_sample(cid, seed):
     with tempfile.TemporaryDirectory() as d:
         prefix = os.path.join(d, "r")
         t0 = time.time()
-        subprocess.check_call([REF_DUMP, "iterate", f"cfg:{cid}:{seed}", str(nf), str(nc), str(it), "0", prefix],
-                              stdout=subprocess.DEVNULL)
+        subprocess.run([REF_DUMP, "iterate", f"cfg:{cid}:{seed}", str(nf), str(nc), str(it), "0", prefix],
+                       stdout=subprocess.DEVNULL, check=True, timeout=CPU_SAMPLE_TIMEOUT_S)
         wall = time.time() - t0
         rows = np.array([[float(x) for x in line.split()] for line in open(prefix + ".hist.txt")
                          if not line.startswith("#")])
@@ -490,15 +495,24 @@ def main():
     if args.per_config and world == 1:
         only = [int(x) for x in args.only.split(",")] if args.only else range(len(CONFIG_NAMES))
         for c in only:
+            t0 = time.time()
             per[c] = head if c == cid else measure_config(c, args, world, rank, local, flush,
                                                           max(3, min(args.steps, 5)), max(args.warmup, 3))
+            print(f"[bench] config {c}: {per[c]['ms_per_step']:.3f} ms/solve, setup {per[c]['setup_s']:.1f} s, "
+                  f"measured in {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
 
     # ---- CPU baseline: the compiled reference on this box's host cores (rank 0, N=1), after
     # every GPU measurement (nothing else runs on the host while it is timed)
     cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_DUMP):
         for c in ([cid] + [c for c in per if c != cid]):
-            v, det = reference_sample(c, args.seed)
+            t0 = time.time()
+            try:
+                v, det = reference_sample(c, args.seed)
+            except subprocess.TimeoutExpired:
+                cpu[c] = {"unavailable": f"reference sample exceeded {CPU_SAMPLE_TIMEOUT_S} s on this host"}
+                continue
+            print(f"[bench] cpu sample config {c}: {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
             cpu[c] = {"value": v, "unit": "DOF-iter/s", "cores": os.cpu_count(), "kind": "reference",
                       "sample": CPU_SAMPLE[c][3] + "; the reference's own C++ (oracle/_ref, Eigen SparseLU stand-in: "
                                 "RCM + band LU), hole solves threaded, context setup excluded", "detail": det}
