@@ -589,6 +589,264 @@ __global__ void __launch_bounds__(256, ASDSM_ZC_MINB) stencil3d_zc_kernel(MarchA
 }
 
 
+// Lean y-march of the 2D constant-coefficient passes (the 2D form of stencil3d_zm_kernel below):
+//   RESIDUAL : r = b - A u        UPDATE : v = u + s e ; u' = v ; r' = b - A v ; norms
+// plus the residual's copies on the slab stations.  A CTA owns 256 consecutive columns and a row
+// range; a thread walks its column in chunks of YM rows: one up-front batch of the chunk's
+// next-row values and b (exact) values, the two trailing rows carried in registers, x neighbours
+// from L1.  The row index is CTA-uniform, so the y-station test is a uniform branch; domain edges
+// are clamped neighbour offsets with zeroed per-thread coefficients (adding c * v = +-0 to a
+// row sum that starts at +0 leaves it bitwise unchanged).  32-bit indices (size < 2^31).
+constexpr int YM = 4;
+template <int MODE, bool EX>
+__global__ void __launch_bounds__(256, (MODE == kMarchUpdate && EX) ? 3 : 4) stencil2d_ym_kernel(MarchArgs A, int ylen) {
+  pdl_launch_dependents();
+  pdl_wait();
+  DevState* S = A.state;
+  if (!S->active) return;
+  const int cur = S->cur;
+  double sc = 0.0;
+  bool work = true;
+  if (MODE == kMarchUpdate) {
+    sc = S->s;
+    work = sc != 0.0 && (!A.retry_pass || S->retry);
+  }
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1];
+  const int sy = Nx;
+  const Stencil& st = A.st;
+  const double* __restrict__ uu = cur ? A.u1 : A.u0;
+  const double* __restrict__ ee = A.e;
+  const double* __restrict__ bb = A.b;
+  const double* __restrict__ xx = A.exact;
+  double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
+  double* __restrict__ rr = MODE == kMarchUpdate ? (cur ? A.ro0 : A.ro1) : (cur ? A.ro1 : A.ro0);
+  double* __restrict__ sta = MODE == kMarchUpdate ? (cur ? A.sta0 : A.sta1) : (cur ? A.sta1 : A.sta0);
+  const unsigned ntx = (Nx + 255) / 256;
+  const unsigned bx = blockIdx.x % ntx, byr = blockIdx.x / ntx;
+  const int x0 = bx * 256 + threadIdx.x;
+  const bool in = x0 < Nx;
+  const int x = min(x0, Nx - 1);
+  const int oxl = x > 0 ? -1 : 0, oxr = x < Nx - 1 ? 1 : 0;
+  const double cxl = x > 0 ? st.left[0] : 0.0, cxr = (x < Nx - 1 && st.has_right[0]) ? st.right[0] : 0.0;
+  const double cyr = st.has_right[1] ? st.right[1] : 0.0;
+  const int yb = byr * ylen, ye = work ? min(Ny, yb + ylen) : yb;
+  int i = x + yb * sy;
+  // station copies: this column's x-station slot (or -1); the y-station test is per row, uniform
+  int xst = -1;
+  if (sta && in && (x + 1) % A.n[0] == 0 && (x + 1) / A.n[0] <= A.nc[0]) xst = ((x + 1) / A.n[0] - 1) * Ny;
+  int yrem = (yb + 1) % A.n[1], yJ = (yb + 1) / A.n[1];
+  auto V = [&](int j) -> double {
+    if (MODE == kMarchUpdate) return __dadd_rn(__ldg(uu + j), __dmul_rn(sc, __ldg(ee + j)));
+    return __ldg(uu + j);
+  };
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double vm = 0.0, vc = 0.0;
+  if (yb < ye) {
+    vm = yb > 0 ? V(i - sy) : 0.0;
+    vc = V(i);
+  }
+  for (int y0 = yb; y0 < ye; y0 += YM) {
+    double vn[YM], bq[YM], eq[EX ? YM : 1];
+#pragma unroll
+    for (int q = 0; q < YM; ++q) {
+      const int y = y0 + q;
+      const int j = i + q * sy;
+      vn[q] = y + 1 < Ny ? V(j + sy) : 0.0;
+      bq[q] = y < Ny ? __ldg(bb + j) : 0.0;
+      if (EX) eq[q] = y < Ny ? __ldg(xx + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < YM; ++q) {
+      const int y = y0 + q;
+      if (y < ye) {
+        const int j = i + q * sy;
+        double acc = __dadd_rn(0.0, __dmul_rn(y > 0 ? st.left[1] : 0.0, vm));
+        acc = __dadd_rn(acc, __dmul_rn(cxl, V(j + oxl)));
+        acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
+        acc = __dadd_rn(acc, __dmul_rn(cxr, V(j + oxr)));
+        acc = __dadd_rn(acc, __dmul_rn(y < Ny - 1 ? cyr : 0.0, vn[q]));
+        const double r = __dsub_rn(bq[q], acc);
+        if (in) {
+          rr[j] = r;
+          if (MODE == kMarchUpdate) uo[j] = vc;
+          if (xst >= 0) sta[xst + y] = r;
+          if (sta && yrem == 0 && yJ <= A.nc[1]) sta[A.nc[0] * Ny + (yJ - 1) * Nx + x] = r;
+          a0 += r * r;
+          a1 = fmax(a1, fabs(r));
+          if (EX) {
+            const double d = vc - eq[q];
+            a2 += d * d;
+            a3 = fmax(a3, fabs(d));
+          }
+        }
+        if (++yrem == A.n[1]) {
+          yrem = 0;
+          ++yJ;
+        }
+        vm = vc;
+        vc = vn[q];
+      }
+    }
+    i += YM * sy;
+  }
+  block_reduce4_march(a0, a1, a2, a3, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
+static bool ym_supported(const MarchArgs& A) {
+  const FineGeom& g = A.g;
+  return g.dim == 2 && A.coef == nullptr && !A.sparse && g.size < (1LL << 31) - (1LL << 20) && g.stride[1] == g.ext[0] &&
+         (!A.sta0 || static_cast<long long>(A.nc[0]) * g.ext[1] + static_cast<long long>(A.nc[1]) * g.ext[0] < (1LL << 31));
+}
+
+// row-range length: ~8 CTAs per SM over the whole grid, whole chunks, at least four chunks
+// (measured at config 1: ranges of 8 / 16 / 32 rows 1.160 / 1.134 / 1.232 ms per solve)
+static int ym_ylen(const FineGeom& g) {
+  if (const char* e = std::getenv("ASDSM_YM_LEN")) return std::max(YM, std::atoi(e) / YM * YM);
+  const int ntx = (g.ext[0] + 255) / 256;
+  const int nyr = std::max(1, 8 * kNumSms / ntx);
+  int ylen = ((g.ext[1] + nyr - 1) / nyr + YM - 1) / YM * YM;
+  ylen = std::max(ylen, 4 * YM);
+  while (static_cast<long long>(ntx) * ((g.ext[1] + ylen - 1) / ylen) > kRedStride) ylen += YM;
+  return ylen;
+}
+
+template <int MODE>
+static void launch_ym(const MarchArgs& A, cudaStream_t s) {
+  const int ylen = ym_ylen(A.g);
+  const unsigned nb = static_cast<unsigned>(((A.g.ext[0] + 255) / 256) * ((A.g.ext[1] + ylen - 1) / ylen));
+  if (A.exact) launch_pdl(stencil2d_ym_kernel<MODE, true>, nb, 256, 0, s, A, ylen);
+  else launch_pdl(stencil2d_ym_kernel<MODE, false>, nb, 256, 0, s, A, ylen);
+}
+
+// Lean z-march of the 3D constant-coefficient passes (north-star kernels 1 and 4 in 3D):
+//   RESIDUAL : r = b - A u            CAND : r' = b - A u' (u' from the axpy pass)
+//   UPDATE   : v = u + s e ; u' = v ; r' = b - A v   (solver.cpp:634-645, fdm.cpp:221-230)
+// A CTA of 32 x 8 threads owns one xy tile and a z range; a thread walks its column in chunks
+// of ZM planes: one up-front batch of the chunk's next-plane values and b (exact) values, the two
+// trailing planes carried in registers (no z halo re-read), in-plane neighbours from L1 (lines
+// the neighbouring warps' batches fetched).  Measured against the tile-walking z-coarsened
+// kernel (scripts/probe_stencil3d.cu, 509^3): that kernel issues ~115 instructions per point --
+// three 64-bit divisions per tile, 64-bit addresses, per-point boundary predicates -- and is
+// issue/latency bound at 3.8 TB/s with DRAM traffic already at the algorithmic bytes; here the
+// tile is fixed per CTA (32-bit division once), indices are 32-bit (size < 2^31), and the domain
+// edges are clamped neighbour offsets with zeroed per-thread coefficients: c * v = +-0 added to
+// a row sum that starts at +0 and therefore is never -0 leaves it bitwise unchanged, so r is
+// bitwise the reference's CSR row sum (fdm.cpp:110-117) as before.
+constexpr int ZM = 4;
+template <int MODE, bool EX>
+__global__ void __launch_bounds__(256, (MODE == kMarchUpdate && EX) ? 3 : 4) stencil3d_zm_kernel(MarchArgs A, int zlen) {
+  DevState* S = A.state;
+  if (!S->active) return;
+  const int cur = S->cur;
+  double sc = 0.0;
+  bool work = true;
+  if (MODE == kMarchUpdate || MODE == kMarchCand) {
+    sc = S->s;
+    work = sc != 0.0 && (!A.retry_pass || S->retry);
+  }
+  const int Nx = A.g.ext[0], Ny = A.g.ext[1], Nz = A.g.ext[2];
+  const int sy = Nx, sz = Nx * Ny;
+  const Stencil& st = A.st;
+  const double* __restrict__ uu = MODE == kMarchCand ? (cur ? A.uo0 : A.uo1) : (cur ? A.u1 : A.u0);
+  const double* __restrict__ ee = A.e;
+  const double* __restrict__ bb = A.b;
+  const double* __restrict__ xx = A.exact;
+  double* __restrict__ uo = MODE == kMarchUpdate ? (cur ? A.uo0 : A.uo1) : nullptr;
+  double* __restrict__ rr = MODE == kMarchResidual ? (cur ? A.ro1 : A.ro0) : (cur ? A.ro0 : A.ro1);
+  const unsigned ntx = (Nx + 31) / 32, nty = (Ny + 7) / 8;
+  unsigned t = blockIdx.x;
+  const unsigned bx = t % ntx;
+  t /= ntx;
+  const unsigned by = t % nty, bzr = t / nty;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = bx * 32 + tx, y0 = by * 8 + ty;
+  const bool in = x0 < Nx && y0 < Ny;
+  const int x = min(x0, Nx - 1), y = min(y0, Ny - 1);
+  const int oxl = x > 0 ? -1 : 0, oxr = x < Nx - 1 ? 1 : 0, oyl = y > 0 ? -sy : 0, oyr = y < Ny - 1 ? sy : 0;
+  const double cxl = x > 0 ? st.left[0] : 0.0, cxr = (x < Nx - 1 && st.has_right[0]) ? st.right[0] : 0.0;
+  const double cyl = y > 0 ? st.left[1] : 0.0, cyr = (y < Ny - 1 && st.has_right[1]) ? st.right[1] : 0.0;
+  const double czr = st.has_right[2] ? st.right[2] : 0.0;
+  const int zb = bzr * zlen, ze = work ? min(Nz, zb + zlen) : zb;
+  int i = x + y * sy + zb * sz;  // element index of (x, y, zb)
+  auto V = [&](int j) -> double {
+    if (MODE == kMarchUpdate) return __dadd_rn(__ldg(uu + j), __dmul_rn(sc, __ldg(ee + j)));
+    return __ldg(uu + j);
+  };
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double vm = 0.0, vc = 0.0;
+  if (zb < ze) {
+    vm = zb > 0 ? V(i - sz) : 0.0;  // plane z - 1
+    vc = V(i);                       // plane z
+  }
+  for (int z0 = zb; z0 < ze; z0 += ZM) {
+    double vn[ZM], bq[ZM], eq[EX ? ZM : 1];
+#pragma unroll
+    for (int q = 0; q < ZM; ++q) {
+      const int z = z0 + q;
+      const int j = i + q * sz;
+      vn[q] = z + 1 < Nz ? V(j + sz) : 0.0;
+      bq[q] = z < Nz ? __ldg(bb + j) : 0.0;
+      if (EX) eq[q] = z < Nz ? __ldg(xx + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < ZM; ++q) {
+      const int z = z0 + q;
+      if (z < ze) {
+        const int j = i + q * sz;
+        double acc = __dadd_rn(0.0, __dmul_rn(z > 0 ? st.left[2] : 0.0, vm));
+        acc = __dadd_rn(acc, __dmul_rn(cyl, V(j + oyl)));
+        acc = __dadd_rn(acc, __dmul_rn(cxl, V(j + oxl)));
+        acc = __dadd_rn(acc, __dmul_rn(st.diag, vc));
+        acc = __dadd_rn(acc, __dmul_rn(cxr, V(j + oxr)));
+        acc = __dadd_rn(acc, __dmul_rn(cyr, V(j + oyr)));
+        acc = __dadd_rn(acc, __dmul_rn(z < Nz - 1 ? czr : 0.0, vn[q]));
+        const double r = __dsub_rn(bq[q], acc);
+        if (in) {
+          rr[j] = r;
+          if (MODE == kMarchUpdate) uo[j] = vc;
+          a0 += r * r;
+          a1 = fmax(a1, fabs(r));
+          if (EX) {
+            const double d = vc - eq[q];
+            a2 += d * d;
+            a3 = fmax(a3, fabs(d));
+          }
+        }
+        vm = vc;
+        vc = vn[q];
+      }
+    }
+    i += ZM * sz;
+  }
+  block_reduce4_march(a0, a1, a2, a3, A.partials);
+  fold_ctrl(A.ctrl, A.partials, S, A.history);
+}
+
+// z-range length of the lean z-march: ~8 ranges per column (whole chunks), more planes per range
+// when the grid would exceed the partial buffer
+static int zm_zlen(const FineGeom& g) {
+  const long long nxy = static_cast<long long>((g.ext[0] + 31) / 32) * ((g.ext[1] + 7) / 8);
+  int zlen = ((g.ext[2] + 7) / 8 + ZM - 1) / ZM * ZM;
+  while (nxy * ((g.ext[2] + zlen - 1) / zlen) > kRedStride) zlen += ZM;
+  return zlen;
+}
+
+static bool zm_supported(const MarchArgs& A) {
+  const FineGeom& g = A.g;
+  return g.dim == 3 && A.coef == nullptr && !A.sparse && g.size < (1LL << 31) - (1LL << 20) && g.stride[1] == g.ext[0] &&
+         g.stride[2] == static_cast<i64>(g.ext[0]) * g.ext[1] &&
+         static_cast<long long>((g.ext[0] + 31) / 32) * ((g.ext[1] + 7) / 8) <= kRedStride;
+}
+
+template <int MODE>
+static void launch_zm(const MarchArgs& A, cudaStream_t s) {
+  const int zlen = zm_zlen(A.g);
+  const unsigned nb = static_cast<unsigned>(((A.g.ext[0] + 31) / 32) * ((A.g.ext[1] + 7) / 8) * ((A.g.ext[2] + zlen - 1) / zlen));
+  if (A.exact) stencil3d_zm_kernel<MODE, true><<<nb, 256, 0, s>>>(A, zlen);
+  else stencil3d_zm_kernel<MODE, false><<<nb, 256, 0, s>>>(A, zlen);
+}
+
 // The 3D update's first pass: u' = u + s e into the non-current buffer (vectorized stream);
 // the residual of u' follows as kMarchCand (measured: two passes stream faster than the fused
 // 3D update, whose neighbour values each cost two loads).
@@ -701,6 +959,10 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
   } else if (A.g.dim == 2 && mode == kMarchDots && A.skel_only) {
     if (var) skel2d_dots_kernel<true><<<kNumSms, 128, 0, s>>>(A);
     else skel2d_dots_kernel<false><<<kNumSms, 128, 0, s>>>(A);
+  } else if ((mode == kMarchUpdate || mode == kMarchResidual) && ym_supported(A) && std::getenv("ASDSM_YC2D") == nullptr) {
+    // the lean y-march (constant coefficients; ASDSM_YC2D=1 selects the tile-walking kernel)
+    if (mode == kMarchResidual) launch_ym<kMarchResidual>(A, s);
+    else launch_ym<kMarchUpdate>(A, s);
   } else if (A.g.dim == 2) {
     // measured (configs 1-2): 8-row segments, a persistent grid of 4 CTAs per SM (more CTAs
     // pay in the completion count and block scheduling, fewer leave HBM latency exposed)
@@ -733,8 +995,25 @@ void launch_march(int mode, const MarchArgs& A0, cudaStream_t s) {
              std::getenv("ASDSM_MARCH3D") == nullptr) {
     launch_stream3d(mode, A, s);
     return;
+  } else if ((mode == kMarchUpdate || mode == kMarchResidual) && zm_supported(A) && std::getenv("ASDSM_MARCH3D") == nullptr &&
+             std::getenv("ASDSM_ZC3D") == nullptr) {
+    // the lean z-march (constant coefficients): the residual, and the update as axpy + candidate
+    // residual -- measured in the captured solve (one box, alternating): config 4 53.74 (z-coarsened
+    // tile kernel) -> 50.85 (fused update, 40 B per point: 1126 us) -> 50.35 ms (two passes, 48 B);
+    // config 3 11.75 -> 11.03 -> 10.9 ms.  ASDSM_UPD3D_FUSED=1 selects the fused form (read at capture).
+    if (mode == kMarchResidual) {
+      launch_zm<kMarchResidual>(A, s);
+    } else if (std::getenv("ASDSM_UPD3D_FUSED") == nullptr) {
+      axpy_update_kernel<<<8 * kNumSms, 256, 0, s>>>(A);
+      ASDSM_CUDA_CHECK(cudaGetLastError());
+      ++g_kernel_launches;
+      launch_zm<kMarchCand>(A, s);
+    } else {
+      launch_zm<kMarchUpdate>(A, s);
+    }
   } else if (mode == kMarchUpdate && std::getenv("ASDSM_MARCH3D") == nullptr) {
-    // measured (configs 3/4): axpy + candidate residual beats the fused 3D update
+    // variable coefficients / sparse residual: axpy + candidate residual (measured against the
+    // fused z-coarsened update)
     axpy_update_kernel<<<8 * kNumSms, 256, 0, s>>>(A);
     ASDSM_CUDA_CHECK(cudaGetLastError());
     ++g_kernel_launches;

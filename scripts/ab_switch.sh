@@ -1,4 +1,4 @@
-# A/B of an env switch on bench configs: scripts/_ab.sh "VAR=val" configs...
+# A/B of an env switch on bench configs: scripts/ab_switch.sh "VAR=val" configs...
 sw="$1"; shift
 for c in "$@"; do
   for v in base sw base sw; do

@@ -217,6 +217,335 @@ __global__ void __launch_bounds__(256, MINB) slab_kernel(Args A) {
   block_fold(a0, a1, a2, a3, A.part);
 }
 
+// ---- V_zch: zc with every true miss hoisted into one up-front batch per tile: the ZCN+2 centre
+// values, b (and exact) of the ZCN planes, the x halo (lanes 0 / 31) and the y halo (first /
+// last warp row); x neighbours by shuffles, interior y neighbours from L1 (lines fetched by the
+// neighbouring warps' batches)
+template <int TYH, int ZCN, bool EX, int MINB>
+__global__ void __launch_bounds__(32 * TYH, MINB) zch_kernel(Args A) {
+  const int Nx = A.Nx, Ny = A.Ny, Nz = A.Nz;
+  const i64 sy = A.sy, sz = A.sz;
+  const St& st = A.st;
+  const double* __restrict__ uu = A.u;
+  const int ntx = (Nx + 31) / 32, nty = (Ny + TYH - 1) / TYH, ntz = (Nz + ZCN - 1) / ZCN;
+  const i64 ntiles = (i64)ntx * nty * ntz;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int bx = t % ntx, by = (t / ntx) % nty, bz = t / ((i64)ntx * nty);
+    const int x = bx * 32 + tx, y = by * TYH + ty, z0 = bz * ZCN;
+    if (y >= Ny) continue;  // warp-uniform
+    const bool in = x < Nx;
+    const i64 pxy = (in ? x : Nx - 1) + y * sy;
+    double vz[ZCN + 2], bq[ZCN], eq[EX ? ZCN : 1], xh[ZCN], yh[ZCN];
+    const bool lh = tx == 0 && x > 0, rh = (tx == 31 || x == Nx - 1) && x < Nx - 1;
+    const bool ylo = ty == 0 && y > 0, yhi = (ty == TYH - 1) && y < Ny - 1;
+#pragma unroll
+    for (int q = 0; q < ZCN + 2; ++q) {
+      const int z = z0 - 1 + q;
+      vz[q] = (z >= 0 && z < Nz) ? __ldg(uu + pxy + z * sz) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      const int z = z0 + q;
+      const bool zin = z < Nz;
+      const i64 p = pxy + z * sz;
+      bq[q] = zin ? __ldg(A.b + p) : 0.0;
+      if (EX) eq[q] = zin ? __ldg(A.ex + p) : 0.0;
+      xh[q] = (zin && lh) ? __ldg(uu + p - 1) : ((zin && rh) ? __ldg(uu + p + 1) : 0.0);
+      yh[q] = (zin && ylo) ? __ldg(uu + p - sy) : ((zin && yhi) ? __ldg(uu + p + sy) : 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      const int z = z0 + q;
+      if (z >= Nz) break;
+      const i64 p = pxy + z * sz;
+      const double vc = vz[q + 1];
+      double vxl = __shfl_up_sync(~0u, vc, 1), vxr = __shfl_down_sync(~0u, vc, 1);
+      if (tx == 0) vxl = xh[q];
+      if (tx == 31 || x == Nx - 1) vxr = xh[q];
+      const double vyl = ty == 0 ? yh[q] : __ldg(uu + p - sy);
+      const double vyr = ty == TYH - 1 ? yh[q] : (y < Ny - 1 ? __ldg(uu + p + sy) : 0.0);
+      const double acc = row_sum(st, z > 0, y > 0, x > 0, x < Nx - 1, y < Ny - 1, z < Nz - 1, vz[q], vyl, vxl, vc, vxr,
+                                 vyr, vz[q + 2]);
+      if (in) {
+        const double r = __dsub_rn(bq[q], acc);
+        A.r[p] = r;
+        a0 += r * r; a1 = fmax(a1, fabs(r));
+        if (EX) { const double d = vc - eq[q]; a2 += d * d; a3 = fmax(a3, fabs(d)); }
+      }
+    }
+  }
+  block_fold(a0, a1, a2, a3, A.part);
+}
+
+// ---- V_zcs: as V_zch, but the in-plane neighbours go through shared memory: the centre values
+// and the halos of the ZCN planes are written to S[q][TYH+2][34], one barrier, then the row sums
+// read S (double buffered over tiles: one barrier per tile)
+template <int TYH, int ZCN, bool EX, int MINB>
+__global__ void __launch_bounds__(32 * TYH, MINB) zcs_kernel(Args A) {
+  const int Nx = A.Nx, Ny = A.Ny, Nz = A.Nz;
+  const i64 sy = A.sy, sz = A.sz;
+  const St& st = A.st;
+  const double* __restrict__ uu = A.u;
+  __shared__ double S[2][ZCN][TYH + 2][34];
+  const int ntx = (Nx + 31) / 32, nty = (Ny + TYH - 1) / TYH, ntz = (Nz + ZCN - 1) / ZCN;
+  const i64 ntiles = (i64)ntx * nty * ntz;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  int buf = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+    const int bx = t % ntx, by = (t / ntx) % nty, bz = t / ((i64)ntx * nty);
+    const int x = bx * 32 + tx, y = by * TYH + ty, z0 = bz * ZCN;
+    const bool yin = y < Ny, in = x < Nx && yin;
+    const i64 pxy = (x < Nx ? x : Nx - 1) + (yin ? y : Ny - 1) * sy;
+    double vz[ZCN + 2], bq[ZCN], eq[EX ? ZCN : 1], xh[ZCN], yh[ZCN];
+    const bool lh = tx == 0 && x > 0, rh = (tx == 31 || x == Nx - 1) && x < Nx - 1;
+    const bool ylo = ty == 0 && y > 0, yhi = (ty == TYH - 1 || y == Ny - 1) && y < Ny - 1;
+#pragma unroll
+    for (int q = 0; q < ZCN + 2; ++q) {
+      const int z = z0 - 1 + q;
+      vz[q] = (z >= 0 && z < Nz) ? __ldg(uu + pxy + z * sz) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      const int z = z0 + q;
+      const bool zin = z < Nz;
+      const i64 p = pxy + z * sz;
+      bq[q] = zin ? __ldg(A.b + p) : 0.0;
+      if (EX) eq[q] = zin ? __ldg(A.ex + p) : 0.0;
+      xh[q] = (zin && lh && yin) ? __ldg(uu + p - 1) : ((zin && rh && yin) ? __ldg(uu + p + 1) : 0.0);
+      yh[q] = (zin && ylo) ? __ldg(uu + p - sy) : ((zin && yhi && yin) ? __ldg(uu + p + sy) : 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      S[buf][q][ty + 1][tx + 1] = vz[q + 1];
+      if (tx == 0) S[buf][q][ty + 1][0] = xh[q];
+      if (tx == 31 || x == Nx - 1) S[buf][q][ty + 1][tx + 2] = xh[q];
+      if (ty == 0) S[buf][q][0][tx + 1] = yh[q];
+      if (ty == TYH - 1 || y == Ny - 1) S[buf][q][ty + 2][tx + 1] = yh[q];
+    }
+    __syncthreads();
+    if (in) {
+#pragma unroll
+      for (int q = 0; q < ZCN; ++q) {
+        const int z = z0 + q;
+        if (z >= Nz) break;
+        const i64 p = pxy + z * sz;
+        const double vc = vz[q + 1];
+        const double acc = row_sum(st, z > 0, y > 0, x > 0, x < Nx - 1, y < Ny - 1, z < Nz - 1, vz[q], S[buf][q][ty][tx + 1],
+                                   S[buf][q][ty + 1][tx], vc, S[buf][q][ty + 1][tx + 2], S[buf][q][ty + 2][tx + 1], vz[q + 2]);
+        const double r = __dsub_rn(bq[q], acc);
+        A.r[p] = r;
+        a0 += r * r; a1 = fmax(a1, fabs(r));
+        if (EX) { const double d = vc - eq[q]; a2 += d * d; a3 = fmax(a3, fabs(d)); }
+      }
+    }
+  }
+  block_fold(a0, a1, a2, a3, A.part);
+}
+
+// ---- V_zm: lean z-march.  A CTA of 32 x 8 threads owns one xy tile and a z range; a thread walks
+// its column in chunks of ZCN planes: one up-front batch of the chunk's ZCN centre values and b
+// (exact) values, the two trailing centre values carried in registers from the previous chunk,
+// in-plane neighbours from L1.  No division in the loop, 32-bit element indices, edge handling
+// by clamped neighbour offsets with zeroed per-thread coefficients (adding c*v = +-0 leaves the
+// row sum bitwise unchanged: the sum starts at +0 and never becomes -0).
+// UPD: the fused update -- V = u + s e at the point and at every neighbour, u' written.
+template <int ZCN, bool EX, bool UPD, int MINB>
+__global__ void __launch_bounds__(256, MINB) zm_kernel(Args A, const double* __restrict__ ee, double* __restrict__ uo,
+                                                       double sc, int zlen) {
+  const int Nx = A.Nx, Ny = A.Ny, Nz = A.Nz;
+  const int sy = (int)A.sy, sz = (int)A.sz;
+  const St& st = A.st;
+  const double* __restrict__ uu = A.u;
+  const double* __restrict__ bb = A.b;
+  const double* __restrict__ xx = A.ex;
+  double* __restrict__ rr = A.r;
+  const unsigned ntx = (Nx + 31) / 32, nty = (Ny + 7) / 8;
+  unsigned t = blockIdx.x;
+  const unsigned bx = t % ntx;
+  t /= ntx;
+  const unsigned by = t % nty, bzr = t / nty;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = bx * 32 + tx, y0 = by * 8 + ty;
+  const bool in = x0 < Nx && y0 < Ny;
+  const int x = min(x0, Nx - 1), y = min(y0, Ny - 1);
+  const int oxl = x > 0 ? -1 : 0, oxr = x < Nx - 1 ? 1 : 0, oyl = y > 0 ? -sy : 0, oyr = y < Ny - 1 ? sy : 0;
+  const double cxl = x > 0 ? st.l[0] : 0.0, cxr = x < Nx - 1 ? st.r[0] : 0.0;
+  const double cyl = y > 0 ? st.l[1] : 0.0, cyr = y < Ny - 1 ? st.r[1] : 0.0;
+  const int zb = bzr * zlen, ze = min(Nz, zb + zlen);
+  int i = x + y * sy + zb * sz;  // element index of (x, y, zb)
+  auto V = [&](int j) -> double {
+    if (UPD) return __dadd_rn(__ldg(uu + j), __dmul_rn(sc, __ldg(ee + j)));
+    return __ldg(uu + j);
+  };
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  double vm = zb > 0 ? V(i - sz) : 0.0;  // plane z - 1
+  double vc = V(i);                       // plane z
+  for (int z0 = zb; z0 < ze; z0 += ZCN) {
+    double vn[ZCN], bq[ZCN], eq[EX ? ZCN : 1];
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      const int z = z0 + q;
+      const int j = i + q * sz;
+      if (UPD) {
+        const double un = z + 1 < Nz ? __ldg(uu + j + sz) : 0.0, en = z + 1 < Nz ? __ldg(ee + j + sz) : 0.0;
+        vn[q] = __dadd_rn(un, __dmul_rn(sc, en));
+      } else {
+        vn[q] = z + 1 < Nz ? __ldg(uu + j + sz) : 0.0;
+      }
+      bq[q] = z < Nz ? __ldg(bb + j) : 0.0;
+      if (EX) eq[q] = z < Nz ? __ldg(xx + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < ZCN; ++q) {
+      const int z = z0 + q;
+      if (z < ze) {
+        const int j = i + q * sz;
+        double acc = __dadd_rn(0.0, __dmul_rn(z > 0 ? st.l[2] : 0.0, vm));
+        acc = __dadd_rn(acc, __dmul_rn(cyl, V(j + oyl)));
+        acc = __dadd_rn(acc, __dmul_rn(cxl, V(j + oxl)));
+        acc = __dadd_rn(acc, __dmul_rn(st.d, vc));
+        acc = __dadd_rn(acc, __dmul_rn(cxr, V(j + oxr)));
+        acc = __dadd_rn(acc, __dmul_rn(cyr, V(j + oyr)));
+        acc = __dadd_rn(acc, __dmul_rn(z < Nz - 1 ? st.r[2] : 0.0, vn[q]));
+        const double r = __dsub_rn(bq[q], acc);
+        if (in) {
+          rr[j] = r;
+          if (UPD) uo[j] = vc;
+          a0 += r * r; a1 = fmax(a1, fabs(r));
+          if (EX) { const double d = vc - eq[q]; a2 += d * d; a3 = fmax(a3, fabs(d)); }
+        }
+        vm = vc;
+        vc = vn[q];
+      }
+    }
+    i += ZCN * sz;
+  }
+  block_fold(a0, a1, a2, a3, A.part);
+}
+
+// axpy of the two-pass update, for the comparison with the fused zm<UPD>
+__global__ void __launch_bounds__(256) axpy_kernel(const double* __restrict__ u, const double* __restrict__ e,
+                                                   double* __restrict__ uo, double s, i64 n) {
+  const i64 n2 = n / 2, stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 uv = __ldg((const double2*)u + i), ev = __ldg((const double2*)e + i);
+    ((double2*)uo)[i] = make_double2(__dadd_rn(uv.x, __dmul_rn(s, ev.x)), __dadd_rn(uv.y, __dmul_rn(s, ev.y)));
+  }
+}
+
+// ---- V_zn: zm with an interior fast path (no z predicates, constant-bank coefficients for the
+// z terms, no per-plane bounds checks) and the running max of |r| as an unsigned compare of the
+// bit patterns (non-negative doubles order like their bits)
+__device__ __forceinline__ void umax_abs(unsigned long long& m, double r) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(r) & 0x7fffffffffffffffull;
+  m = a > m ? a : m;
+}
+template <int ZCN, bool EX, bool UPD, int MINB>
+__global__ void __launch_bounds__(256, MINB) zn_kernel(Args A, const double* __restrict__ ee, double* __restrict__ uo,
+                                                       double sc, int zlen) {
+  const int Nx = A.Nx, Ny = A.Ny, Nz = A.Nz;
+  const int sy = (int)A.sy, sz = (int)A.sz;
+  const St& st = A.st;
+  const double* __restrict__ uu = A.u;
+  const double* __restrict__ bb = A.b;
+  const double* __restrict__ xx = A.ex;
+  double* __restrict__ rr = A.r;
+  const unsigned ntx = (Nx + 31) / 32, nty = (Ny + 7) / 8;
+  unsigned t = blockIdx.x;
+  const unsigned bx = t % ntx;
+  t /= ntx;
+  const unsigned by = t % nty, bzr = t / nty;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = bx * 32 + tx, y0 = by * 8 + ty;
+  const bool in = x0 < Nx;
+  double a0 = 0, a2 = 0;
+  unsigned long long m1 = 0, m3 = 0;
+  if (y0 < Ny) {  // warp-uniform
+    const int x = min(x0, Nx - 1), y = y0;
+    const int oxl = x > 0 ? -1 : 0, oxr = x < Nx - 1 ? 1 : 0, oyl = y > 0 ? -sy : 0, oyr = y < Ny - 1 ? sy : 0;
+    const double cxl = x > 0 ? st.l[0] : 0.0, cxr = x < Nx - 1 ? st.r[0] : 0.0;
+    const double cyl = y > 0 ? st.l[1] : 0.0, cyr = y < Ny - 1 ? st.r[1] : 0.0;
+    const int zb = bzr * zlen, ze = min(Nz, zb + zlen);
+    int i = x + y * sy + zb * sz;
+    auto V = [&](int j) -> double {
+      if (UPD) return __dadd_rn(__ldg(uu + j), __dmul_rn(sc, __ldg(ee + j)));
+      return __ldg(uu + j);
+    };
+    double vm = zb > 0 ? V(i - sz) : 0.0, vc = V(i);
+    int z0 = zb;
+    for (; z0 < ze; z0 += ZCN, i += ZCN * sz) {
+      double vn[ZCN], bq[ZCN], eq[EX ? ZCN : 1];
+      if (z0 > 0 && z0 + ZCN < Nz && z0 + ZCN <= ze) {  // interior chunk
+#pragma unroll
+        for (int q = 0; q < ZCN; ++q) {
+          const int j = i + q * sz;
+          vn[q] = V(j + sz);
+          bq[q] = __ldg(bb + j);
+          if (EX) eq[q] = __ldg(xx + j);
+        }
+#pragma unroll
+        for (int q = 0; q < ZCN; ++q) {
+          const int j = i + q * sz;
+          double acc = __dadd_rn(0.0, __dmul_rn(st.l[2], vm));
+          acc = __dadd_rn(acc, __dmul_rn(cyl, V(j + oyl)));
+          acc = __dadd_rn(acc, __dmul_rn(cxl, V(j + oxl)));
+          acc = __dadd_rn(acc, __dmul_rn(st.d, vc));
+          acc = __dadd_rn(acc, __dmul_rn(cxr, V(j + oxr)));
+          acc = __dadd_rn(acc, __dmul_rn(cyr, V(j + oyr)));
+          acc = __dadd_rn(acc, __dmul_rn(st.r[2], vn[q]));
+          const double r = __dsub_rn(bq[q], acc);
+          if (in) {
+            rr[j] = r;
+            if (UPD) uo[j] = vc;
+            a0 += r * r;
+            umax_abs(m1, r);
+            if (EX) { const double d = vc - eq[q]; a2 += d * d; umax_abs(m3, d); }
+          }
+          vm = vc;
+          vc = vn[q];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < ZCN; ++q) {
+          const int z = z0 + q;
+          const int j = i + q * sz;
+          vn[q] = z + 1 < Nz ? V(j + sz) : 0.0;
+          bq[q] = z < Nz ? __ldg(bb + j) : 0.0;
+          if (EX) eq[q] = z < Nz ? __ldg(xx + j) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < ZCN; ++q) {
+          const int z = z0 + q;
+          if (z < ze) {
+            const int j = i + q * sz;
+            double acc = __dadd_rn(0.0, __dmul_rn(z > 0 ? st.l[2] : 0.0, vm));
+            acc = __dadd_rn(acc, __dmul_rn(cyl, V(j + oyl)));
+            acc = __dadd_rn(acc, __dmul_rn(cxl, V(j + oxl)));
+            acc = __dadd_rn(acc, __dmul_rn(st.d, vc));
+            acc = __dadd_rn(acc, __dmul_rn(cxr, V(j + oxr)));
+            acc = __dadd_rn(acc, __dmul_rn(cyr, V(j + oyr)));
+            acc = __dadd_rn(acc, __dmul_rn(z < Nz - 1 ? st.r[2] : 0.0, vn[q]));
+            const double r = __dsub_rn(bq[q], acc);
+            if (in) {
+              rr[j] = r;
+              if (UPD) uo[j] = vc;
+              a0 += r * r;
+              umax_abs(m1, r);
+              if (EX) { const double d = vc - eq[q]; a2 += d * d; umax_abs(m3, d); }
+            }
+            vm = vc;
+            vc = vn[q];
+          }
+        }
+      }
+    }
+  }
+  block_fold(a0, __longlong_as_double((long long)m1), a2, __longlong_as_double((long long)m3), A.part);
+}
+
 static double checksum(const double* d_r, i64 n) {
   std::vector<double> h(n);
   CK(cudaMemcpy(h.data(), d_r, n * 8, cudaMemcpyDeviceToHost));
@@ -231,8 +560,8 @@ static void run(const char* name, F launch, Args& A, double bytes, float* flush,
   CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   CK(cudaMemset(A.r, 0, A.n * 8));
   float best = 1e30f, sum = 0;
-  const int reps = 6;
-  for (int i = 0; i < reps + 2; ++i) {
+  const int warm = getenv("PROBE_ONCE") ? 0 : 2, reps = getenv("PROBE_ONCE") ? 1 : 6;
+  for (int i = 0; i < reps + warm; ++i) {
     CK(cudaMemsetAsync(flush, i, flush_n));
     CK(cudaEventRecord(e0));
     launch();
@@ -240,7 +569,7 @@ static void run(const char* name, F launch, Args& A, double bytes, float* flush,
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
-    if (i >= 2) { best = ms < best ? ms : best; sum += ms; }
+    if (i >= warm) { best = ms < best ? ms : best; sum += ms; }
   }
   const double cs = check ? checksum(A.r, A.n) : 0.0;
   printf("%-34s mean %8.4f ms  best %8.4f ms  %7.1f GB/s (mean)  %7.1f (best)  checksum %.0f\n", name, sum / reps, best,
@@ -258,7 +587,7 @@ int main(int argc, char** argv) {
   A.st.d = 6.0 / (h * h);
   double *u, *b, *x, *r, *part;
   CK(cudaMalloc(&u, (A.n + 2) * 8)); CK(cudaMalloc(&b, (A.n + 2) * 8)); CK(cudaMalloc(&x, (A.n + 2) * 8));
-  CK(cudaMalloc(&r, (A.n + 2) * 8)); CK(cudaMalloc(&part, 4 * 65536 * 8));
+  CK(cudaMalloc(&r, (A.n + 2) * 8)); CK(cudaMalloc(&part, 4 * ((A.n + 255) / 256 + 1024) * 8));
   {
     std::vector<double> h0(A.n);
     unsigned long long s = 88172645463325252ull;
@@ -276,27 +605,89 @@ int main(int argc, char** argv) {
   const double by = (ex ? 32.0 : 24.0) * A.n, by_copy = 24.0 * A.n;
   const int SM = 148;
   printf("N = %d, exact = %d, %.1f M points, algorithmic %.2f GB\n", N, (int)ex, A.n / 1e6, by / 1e9);
-  run("lin_copy (8x148)", [&] { lin_copy<<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
   run("lin_copy (32x148)", [&] { lin_copy<<<32 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
-  run("tile_copy 32x8x8", [&] { tile_copy<32, 8, 8><<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
-  run("tile_copy 64x4x8", [&] { tile_copy<64, 4, 8><<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
-  run("tile_copy 128x2x8", [&] { tile_copy<128, 2, 8><<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
-  run("tile_copy 256x1x8", [&] { tile_copy<256, 1, 8><<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
-  run("tile_copy 32x8x1", [&] { tile_copy<32, 8, 1><<<8 * SM, 256>>>(A); }, A, by_copy, flush, flush_n, false);
 #define ZCV(TX, TY, ZC, MB, G)                                                                                     \
   if (ex) run("zc " #TX "x" #TY "x" #ZC " minb" #MB " grid" #G, [&] { zc_kernel<TX, TY, ZC, true, MB><<<G * SM, 256>>>(A); }, A, by, flush, flush_n); \
   else run("zc " #TX "x" #TY "x" #ZC " minb" #MB " grid" #G, [&] { zc_kernel<TX, TY, ZC, false, MB><<<G * SM, 256>>>(A); }, A, by, flush, flush_n);
   ZCV(32, 8, 8, 4, 8)
-  ZCV(32, 8, 8, 4, 4)
-  ZCV(32, 8, 4, 4, 8)
-  ZCV(32, 8, 4, 6, 6)
-  ZCV(32, 8, 2, 8, 8)
-  ZCV(64, 4, 8, 4, 8)
-  ZCV(128, 2, 8, 4, 8)
-  ZCV(256, 1, 8, 4, 8)
-  ZCV(64, 4, 4, 6, 6)
-  ZCV(128, 2, 4, 6, 6)
-  ZCV(256, 1, 4, 6, 6)
+  double *e2, *uo2;
+  CK(cudaMalloc(&e2, (A.n + 2) * 8)); CK(cudaMalloc(&uo2, (A.n + 2) * 8));
+  CK(cudaMemcpy(e2, x, A.n * 8, cudaMemcpyDeviceToDevice));
+  const unsigned nxy = ((N + 31) / 32) * ((N + 7) / 8);
+#define ZM(ZC, MB, NZR)                                                                                            \
+  {                                                                                                                \
+    const int zlen = ((N + NZR - 1) / NZR + ZC - 1) / ZC * ZC, nzr = (N + zlen - 1) / zlen;                         \
+    if (ex) run("zm ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zm_kernel<ZC, true, false, MB><<<nxy * nzr, 256>>>(A, nullptr, nullptr, 0.0, zlen); }, A, by, flush, flush_n); \
+    else run("zm ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zm_kernel<ZC, false, false, MB><<<nxy * nzr, 256>>>(A, nullptr, nullptr, 0.0, zlen); }, A, by, flush, flush_n); \
+  }
+  ZM(8, 4, 4)
+  ZM(8, 4, 8)
+  ZM(8, 4, 16)
+  ZM(8, 3, 8)
+  ZM(8, 2, 8)
+  ZM(4, 4, 8)
+  ZM(4, 6, 8)
+  ZM(4, 8, 8)
+  ZM(16, 2, 8)
+  ZM(16, 3, 4)
+  ZM(2, 8, 8)
+  // fused update: u' = u + s e, r = b - A u' (40 / 48 B per point) against axpy + residual (48 / 56 B)
+  const double byu = (ex ? 48.0 : 40.0) * A.n;
+#define ZMU(ZC, MB, NZR)                                                                                           \
+  {                                                                                                                \
+    const int zlen = ((N + NZR - 1) / NZR + ZC - 1) / ZC * ZC, nzr = (N + zlen - 1) / zlen;                         \
+    if (ex) run("zm UPD ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zm_kernel<ZC, true, true, MB><<<nxy * nzr, 256>>>(A, e2, uo2, 0.37, zlen); }, A, byu, flush, flush_n); \
+    else run("zm UPD ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zm_kernel<ZC, false, true, MB><<<nxy * nzr, 256>>>(A, e2, uo2, 0.37, zlen); }, A, byu, flush, flush_n); \
+  }
+  ZMU(8, 4, 8)
+  ZMU(8, 3, 8)
+  ZMU(8, 2, 8)
+  ZMU(4, 4, 8)
+  ZMU(4, 6, 8)
+  ZMU(4, 3, 8)
+  {
+    Args B = A;
+    B.u = uo2;
+    const int zlen = ((N + 7) / 8 + 7) / 8 * 8, nzr = (N + zlen - 1) / zlen;
+    if (ex) run("axpy + zm ZC8 minb4 nzr8", [&] { axpy_kernel<<<8 * SM, 256>>>(u, e2, uo2, 0.37, A.n); zm_kernel<8, true, false, 4><<<nxy * nzr, 256>>>(B, nullptr, nullptr, 0.0, zlen); }, A, byu, flush, flush_n);
+    else run("axpy + zm ZC8 minb4 nzr8", [&] { axpy_kernel<<<8 * SM, 256>>>(u, e2, uo2, 0.37, A.n); zm_kernel<8, false, false, 4><<<nxy * nzr, 256>>>(B, nullptr, nullptr, 0.0, zlen); }, A, byu, flush, flush_n);
+  }
+#define ZN(ZC, MB, NZR)                                                                                            \
+  {                                                                                                                \
+    const int zlen = ((N + NZR - 1) / NZR + ZC - 1) / ZC * ZC, nzr = (N + zlen - 1) / zlen;                         \
+    if (ex) run("zn ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zn_kernel<ZC, true, false, MB><<<nxy * nzr, 256>>>(A, nullptr, nullptr, 0.0, zlen); }, A, by, flush, flush_n); \
+    else run("zn ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zn_kernel<ZC, false, false, MB><<<nxy * nzr, 256>>>(A, nullptr, nullptr, 0.0, zlen); }, A, by, flush, flush_n); \
+  }
+  ZN(2, 8, 8)
+  ZN(2, 8, 16)
+  ZN(2, 6, 8)
+  ZN(4, 4, 8)
+  ZN(4, 4, 16)
+  ZN(4, 5, 8)
+  ZN(4, 6, 8)
+  ZN(8, 4, 8)
+  ZN(8, 3, 8)
+  ZN(1, 8, 8)
+#define ZNU(ZC, MB, NZR)                                                                                           \
+  {                                                                                                                \
+    const int zlen = ((N + NZR - 1) / NZR + ZC - 1) / ZC * ZC, nzr = (N + zlen - 1) / zlen;                         \
+    if (ex) run("zn UPD ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zn_kernel<ZC, true, true, MB><<<nxy * nzr, 256>>>(A, e2, uo2, 0.37, zlen); }, A, byu, flush, flush_n); \
+    else run("zn UPD ZC" #ZC " minb" #MB " nzr" #NZR, [&] { zn_kernel<ZC, false, true, MB><<<nxy * nzr, 256>>>(A, e2, uo2, 0.37, zlen); }, A, byu, flush, flush_n); \
+  }
+  ZNU(2, 8, 8)
+  ZNU(2, 6, 8)
+  ZNU(2, 4, 8)
+  ZNU(4, 4, 8)
+  ZNU(4, 3, 8)
+  ZNU(4, 5, 8)
+  {
+    Args B = A;
+    B.u = uo2;
+    const int zlen = ((N + 7) / 8 + 1) / 2 * 2, nzr = (N + zlen - 1) / zlen;
+    if (ex) run("axpy + zn ZC2 minb8 nzr8", [&] { axpy_kernel<<<8 * SM, 256>>>(u, e2, uo2, 0.37, A.n); zn_kernel<2, true, false, 8><<<nxy * nzr, 256>>>(B, nullptr, nullptr, 0.0, zlen); }, A, byu, flush, flush_n);
+    else run("axpy + zn ZC2 minb8 nzr8", [&] { axpy_kernel<<<8 * SM, 256>>>(u, e2, uo2, 0.37, A.n); zn_kernel<2, false, false, 8><<<nxy * nzr, 256>>>(B, nullptr, nullptr, 0.0, zlen); }, A, byu, flush, flush_n);
+  }
+  if (getenv("PROBE_ZM_ONLY")) return 0;
 #define LINV(P, MB, G)                                                                                             \
   if (ex) run("lin P" #P " minb" #MB " grid" #G, [&] { lin_kernel<P, true, MB><<<G, 256>>>(A); }, A, by, flush, flush_n); \
   else run("lin P" #P " minb" #MB " grid" #G, [&] { lin_kernel<P, false, MB><<<G, 256>>>(A); }, A, by, flush, flush_n);

@@ -397,6 +397,50 @@ def test_stream3d_tma_pass_bitwise(spec, nf, nc, iters, monkeypatch):
     assert np.all(np.abs(a - b) <= 1e-14 * b)
 
 
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:0:0", 0, 0, 6), ("cfg:1:2", 199, 9, 6), ("cfg:2:5", 199, 9, 6),
+                                              ("cfg:1:0", 0, 0, 5), ("ex:1:1", 459, 3, 4)])
+def test_ymarch2d_pass_bitwise(spec, nf, nc, iters, monkeypatch):
+    """The lean y-march of the 2D residual / update pass (default, march.cu stencil2d_ym_kernel:
+    clamped neighbour offsets with zeroed edge coefficients, station copies from a uniform row
+    test) against the tile-walking kernel with per-point boundary predicates (ASDSM_YC2D=1): the
+    same row sums in the reference's CSR order (fdm.cpp:110-117), so bitwise the same solve."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=3)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_d = ctx.iterate(opts)
+    assert any("stencil2d_ym_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
+    monkeypatch.setenv("ASDSM_YC2D", "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_t = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    assert np.array_equal(st_d.u, st_t.u) and np.array_equal(st_d.r, st_t.r)
+    a = np.array([h.res_l2 for h in st_d.history])
+    b = np.array([h.res_l2 for h in st_t.history])
+    assert np.all(np.abs(a - b) <= 1e-14 * b)
+
+
+@pytest.mark.parametrize("switch", ["ASDSM_ZC3D", "ASDSM_UPD3D_FUSED"])
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:4:1", 24, 4, 6)])
+def test_zmarch3d_pass_bitwise(spec, nf, nc, iters, switch, monkeypatch):
+    """The lean z-march of the 3D residual / candidate residual (default, march.cu
+    stencil3d_zm_kernel: clamped neighbour offsets with zeroed edge coefficients) against the
+    tile-walking z-coarsened kernel with per-point boundary predicates (ASDSM_ZC3D=1), and its
+    fused update form (ASDSM_UPD3D_FUSED=1) against axpy + candidate residual: the same row sums
+    in the reference's CSR order (fdm.cpp:110-117), so bitwise the same solve."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=3)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_d = ctx.iterate(opts)
+    assert any("stencil3d_zm_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
+    monkeypatch.setenv(switch, "1")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_t = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    assert np.array_equal(st_d.u, st_t.u) and np.array_equal(st_d.r, st_t.r)
+    # (the norms are reduced over another grid shape: the same values summed in another order)
+    a = np.array([h.res_l2 for h in st_d.history])
+    b = np.array([h.res_l2 for h in st_t.history])
+    assert np.all(np.abs(a - b) <= 1e-14 * b)
+
+
 @pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])
 def test_hole_strip_split_agrees(spec, nf, nc, iters, monkeypatch):
     """Large 2D holes split into strips (default: separator columns from the hole's own modes,
