@@ -172,8 +172,13 @@ def ncu_traffic(cid, component, kernels):
         return (int(m.group(1)), m.group(2) or "") if m else (0, "")
     paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic*.json")), key=order, reverse=True)
 
+    def norm(n):  # `stencil2d_ym_kernel<1,0>` from either demangler's spelling
+        n = n.replace("(anonymous namespace)::", "").replace("asdsm_b200::", "")
+        n = re.sub(r"\((?:int|bool)\)", "", n)
+        return n.replace(" ", "").replace("false", "0").replace("true", "1")
+
     def launched(name):
-        return any(name == n or n.endswith("::" + name) or name.endswith("::" + n) for n in kernels)
+        return any(norm(name) == norm(n) for n in kernels)
     for path in paths:
         try:
             k = json.load(open(path))["kernels"].get(f"{cid}/{component}")

@@ -4,11 +4,18 @@
 #pragma once
 #include "plan.hpp"
 
+#include <cstdlib>
+
 namespace asdsm_b200 {
 
 // the even/odd kernel is used for axes of at least this many modes (below, the dense kernel's
 // rounding is kept: the split's savings do not matter there)
 constexpr int kEoMinModes = 64;
+// (ASDSM_EO_MIN overrides; read when a transform is launched / captured)
+inline int eo_min_modes() {
+  const char* e = std::getenv("ASDSM_EO_MIN");
+  return e ? std::atoi(e) : kEoMinModes;
+}
 
 struct GemmLines {
   int o_ext[2];

@@ -436,7 +436,7 @@ void launch_transform(const SepSolver& S, int axis, const BoxArray& in, const Bo
       }
       G.nlines = M.nlines;
       const bool dense = std::getenv("ASDSM_DENSE_GEMM") != nullptr;  // (read at capture time)
-      if (eo != 0 && S.half[axis] != nullptr && m >= kEoMinModes && !dense) {
+      if (eo != 0 && S.half[axis] != nullptr && m >= eo_min_modes() && !dense) {
         launch_dmma_eo_transform(eo == 1, ip, op, S.half[axis], m, in.stride[axis], out.stride[axis], G, st);
         return;
       }

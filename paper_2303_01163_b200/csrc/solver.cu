@@ -695,7 +695,7 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
     const i64 in_es = part ? A.m1 : 1;  // [hole][k][j] from the partition solve, else [hole][j][k]
-    if (A.m0 >= kEoMinModes && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
+    if (A.m0 >= eo_min_modes() && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
       launch_dmma_eo_transform(true, modes, e, T.half[0], A.m0, in_es, 1, G, s);
     else launch_dmma_transform(modes, e, T.V[0], A.m0, in_es, 1, G, s);
     return;
@@ -1364,13 +1364,13 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     // the hole fill exactly as the solve launches it (Solver::fill): one fused kernel per hole,
     // or (large holes) the mode-line solves and the DMMA back transform timed apart
     if (hole2d_fused_fits(H.ext[0], H.ext[1]) && std::getenv("ASDSM_HOLE_UNFUSED") == nullptr) {
-      const double eo = H.ext[0] >= kEoMinModes ? 0.5 : 1.0;  // even/odd split executes half the MACs
+      const double eo = H.ext[0] >= eo_min_modes() ? 0.5 : 1.0;  // even/odd split executes half the MACs
       timed("hole2d_fused_dmma", 8.0 * NH, 2.0 * H.ext[0] * eo * static_cast<double>(NH), iters,
             [&] { fill(e_, nullptr, s); });
     } else {
       // (strip split: the back transform runs over the strips' w-point transforms)
       const int mt = strip_p_ ? sep_strip_.ext[0] : H.ext[0];
-      const double eot = mt >= kEoMinModes ? 0.5 : 1.0;
+      const double eot = mt >= eo_min_modes() ? 0.5 : 1.0;
       timed(strip_p_ ? "hole2d_mode_lines_separators_strip_lines" : "hole2d_mode_lines", 8.0 * NH * 2.0, 0.0, iters,
             [&] { fill(e_, nullptr, s, kFillLines); });
       timed("hole_backtransform_dmma", 8.0 * NH * 2.0, 2.0 * mt * eot * static_cast<double>(NH), iters,
@@ -1381,7 +1381,10 @@ std::vector<Solver::Component> Solver::profile(cudaStream_t s, int reps) {
     if (!variable_)
       for (int i = 0; i < H.nd; ++i) hflops += 2.0 * H.ext[H.dax[i]] * static_cast<double>(NH);
     if (h3f_ok_ && std::getenv("ASDSM_HOLE3D_UNFUSED") == nullptr) hflops *= 0.5;  // even/odd on both axes
-    timed("hole_fill", 8.0 * NH * 3.0, hflops, iters, [&] { fill(e_, nullptr, s); });
+    // algorithmic bytes: the fused kernel writes every hole value once (the ring it reads is
+    // O(m^2) per hole); the unfused path also writes and reads the mode buffer
+    const bool h3_fused = h3f_ok_ && std::getenv("ASDSM_HOLE3D_UNFUSED") == nullptr;
+    timed("hole_fill", 8.0 * NH * (h3_fused ? 1.0 : 3.0), hflops, iters, [&] { fill(e_, nullptr, s); });
     timed("slab_solves", 8.0 * slab_pts * 4.0, 0.0, iters, [&] {
       for (int a = 0; a < mesh_.dim; ++a) {
         launch_gather(r_[0], r_[1], rhs_slab_[a], md_, 1u << a, g_slab_[a].size, state_, s);

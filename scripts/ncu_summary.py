@@ -20,13 +20,17 @@ METRICS = [
 ]
 
 
-def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def main(path, header=True):
+    if path.endswith(".csv"):  # a raw page exported on the GPU box (profile_round.sh)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued")]
-    print("| kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls |")
-    print("|---" * (len(METRICS) + 2) + "|")
+    if header:
+        print("| kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls |")
+        print("|---" * (len(METRICS) + 2) + "|")
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("(anonymous namespace)::", "")[-48:]
         cells = []
@@ -43,4 +47,5 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    for i, p in enumerate(sys.argv[1:]):
+        main(p, header=i == 0)

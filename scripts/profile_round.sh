@@ -15,18 +15,30 @@ if [ "$what" = bench ]; then
         python scripts/one_solve.py $c 1 > $out/ncu_launch_c$c.log 2>&1
   done
 else
+  # reports stay on the box (/tmp); the raw metric pages come back as CSV (gpurun_out/ is capped
+  # at 64 MiB), plus the .ncu-rep of the kernels listed in KEEP for the source page
+  KEEP=${KEEP:-"c4_hole"}
+  mkdir -p /tmp/prof_$tag
   full() {  # config, kernel regex, skip, name
-    ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 1 -o $out/full_c$1_$4 \
+    ncu -f --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 1 -o /tmp/prof_$tag/full_c$1_$4 \
         python scripts/one_solve.py $1 1 > $out/ncu_full_c$1_$4.log 2>&1
+    ncu -i /tmp/prof_$tag/full_c$1_$4.ncu-rep --page raw --csv > $out/full_c$1_$4.csv 2>/dev/null
+    for k in $KEEP; do [ "$k" = "c$1_$4" ] && cp /tmp/prof_$tag/full_c$1_$4.ncu-rep $out/; done
   }
   full 1 "hole2d_fused_kernel" 5 hole
-  full 1 "stencil2d_yc_kernel" 5 update
+  full 1 "stencil2d_ym_kernel" 5 update
+  full 1 "slabstep2d_kernel" 5 slabstep
   full 2 "dmma_eo2_kernel" 5 back
-  full 2 "stencil2d_yc_kernel" 5 update
+  full 2 "stencil2d_ym_kernel" 5 update
   full 2 "hole2d_part_kernel" 5 lines
   full 3 "hole3d_fused_kernel" 3 hole
+  full 3 "stencil3d_zm_kernel" 3 cand
   full 4 "hole3d_fused_kernel" 3 hole
-  full 4 "stencil3d_zc_kernel" 3 cand
+  full 4 "stencil3d_zm_kernel" 3 cand
   full 4 "axpy_update_kernel" 3 axpy
+  full 4 "m3_apply_kernel" 3 m3apply
+  full 4 "m4_kernel" 3 m4
+  full 4 "skel3d_dots_rows_kernel" 3 dots
+  full 4 "dmma_eo2_kernel" 6 slabtransform
 fi
 echo done > $out/DONE_$what

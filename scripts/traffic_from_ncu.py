@@ -1,7 +1,8 @@
 """DRAM traffic per launch of the bench components from `ncu --set full` reports:
 python scripts/traffic_from_ncu.py PROFDIR OUT.json
 
-PROFDIR holds full_c<config>_<name>.ncu-rep (scripts/profile_round.sh).  Each bench component
+PROFDIR holds full_c<config>_<name>.csv (the raw page, exported by scripts/profile_round.sh) or
+.ncu-rep.  Each bench component
 (Solver::profile names) maps to the kernels one launch of it runs; its traffic is the sum of
 their dram__bytes_read.sum + dram__bytes_write.sum.  bench.py reads OUT.json (profiles/
 r*_traffic*.json) and reports a component's traffic only when every listed kernel is in the
@@ -17,13 +18,18 @@ COMPONENTS = {  # (config, component): [report names]
     (1, "update_residual"): ["update"], (1, "hole2d_fused_dmma"): ["hole"], (1, "slabstep2d"): ["slabstep"],
     (1, "step_dots_skeleton"): ["dots"],
     (2, "update_residual"): ["update"], (2, "hole_backtransform_dmma"): ["back"], (2, "slab2d_fwd_pcr"): ["slabfwd"],
-    (3, "update_residual"): ["axpy", "cand"], (3, "hole_fill"): ["hole"],
-    (4, "update_residual"): ["axpy", "cand"], (4, "hole_fill"): ["hole"],
+    (2, "hole2d_mode_lines_separators_strip_lines"): ["lines"],
+    (3, "update_residual"): ["axpy", "cand"], (3, "hole_fill"): ["hole"], (3, "residual"): ["cand"],
+    (4, "update_residual"): ["axpy", "cand"], (4, "hole_fill"): ["hole"], (4, "residual"): ["cand"],
 }
 
 
 def kernel_name(raw):
+    """`stencil2d_ym_kernel<1,0>` from ncu's `void unnamed>::stencil2d_ym_kernel<1, 0>(MarchArgs, int)`
+    (bench.py normalizes the library's own demangled names the same way)."""
     n = raw.replace("(anonymous namespace)::", "")
+    if "unnamed>::" in n:
+        n = n.split("unnamed>::", 1)[1]
     if n.startswith("void "):
         n = n[5:]
     depth = 0
@@ -33,12 +39,16 @@ def kernel_name(raw):
         elif ch == ">":
             depth -= 1
         elif ch == "(" and depth == 0:
-            return n[:i]
-    return n
+            n = n[:i]
+            break
+    return n.replace(" ", "").replace("false", "0").replace("true", "1")
 
 
 def read(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # the raw page already exported on the GPU box (profile_round.sh)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, r = rows[0], rows[1], rows[2]
 
@@ -55,7 +65,9 @@ def main(d, out_path):
     for (cid, comp), names in COMPONENTS.items():
         parts = []
         for n in names:
-            p = os.path.join(d, f"full_c{cid}_{n}.ncu-rep")
+            p = os.path.join(d, f"full_c{cid}_{n}.csv")
+            if not os.path.exists(p):
+                p = os.path.join(d, f"full_c{cid}_{n}.ncu-rep")
             if not os.path.exists(p):
                 break
             parts.append(read(p))
