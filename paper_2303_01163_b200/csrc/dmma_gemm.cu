@@ -4,6 +4,9 @@
 // the scalar register-tiled kernel is limited by shared-memory bandwidth instead.
 #include "dmma_gemm.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace asdsm_b200 {
 
 namespace {
@@ -327,6 +330,171 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
   }
 }
 
+
+// Back transform of a batch of hole strips with the half sine table resident in shared memory
+// (config 2: 500 strips of w = 81 columns x 409 rows per iteration).  The generic even/odd kernel
+// above re-stages the table for every 64 x 64 x 16 step and pads the 41 outputs of a strip's
+// half transform to a 64-wide tile; here a CTA takes one (strip, row tile) work item:
+//   modes [strip][k][j] (j contiguous) -> A tile [k in even/odd order][TR rows] by 8-byte cp.async
+//   (the whole K extent at once: no K loop over global memory), the table once per CTA,
+//   a warp pair 16 rows x every output (each warp half of the n tiles): E and O accumulators of the same (j, q) live in the same
+//   thread, so out(q) = sc_q (E + O), out(m-1-q) = sc_{m-1-q} (E - O) needs no exchange and is
+//   written straight from the accumulators.  One persistent CTA per SM walks the work items with
+//   two A tiles in flight (the next tile's cp.async group is issued before this tile's MMAs).
+//   The last row tile of a strip is shifted up to end at the strip's last row (it recomputes a
+//   few rows of its neighbour -- the same values), so every tile is full.
+struct StripBackArgs {
+  int m, m1, kh, mh, ne, no4;  // modes, rows, padded half width, ceil(m/2), even modes, odd modes padded to 4
+  int tiles;                   // row tiles per strip
+  int nbox0, nboxes;
+  i64 out_bs0, out_bs1, out_stride;
+};
+
+template <int NTW>  // n tiles of 8 outputs per warp: a warp pair covers 2 NTW >= ceil(mh / 8) tiles
+__global__ void __launch_bounds__(512) strip_back_kernel(const double* __restrict__ modes, double* __restrict__ e,
+                                                         const double* __restrict__ half, StripBackArgs P) {
+  extern __shared__ __align__(16) double ssm[];
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
+  const int TR = nth >> 2;  // 16 rows per warp pair
+  const int LDA = TR + 4, LDB = 2 * P.kh + 4;
+  const int m = P.m, m1 = P.m1, kh = P.kh, KA = kh + P.no4;
+  double* Bs = ssm;                      // [16 NTW][LDB]: table row q, column half * kh + kappa
+  double* Ss = Bs + 16 * NTW * LDB;      // sc[m]
+  double* Ab = Ss + ((m + 1) & ~1);      // two A tiles [KA][LDA]: even modes, then odd modes
+  const int ntile = P.tiles * P.nboxes;
+  // the tile's modes, every k at once, by 8-byte cp.async: this warp's share is rows k = warp,
+  // warp + nwarp, ... in chunks of 32 rows-of-j; item i = (row i / nch, chunk i % nch)
+  const int nch = (TR + 31) >> 5, nitem = ((m - warp + nwarp - 1) / nwarp) * nch;
+  auto issue_item = [&](const double* __restrict__ src, double* As, int i) {
+    const int k = warp + nwarp * (i / nch), j = 32 * (i % nch) + lane;
+    const int row = (k & 1) ? kh + (k >> 1) : (k >> 1);
+    if (j < TR) cp_async8(As + row * LDA + j, src + static_cast<i64>(k) * m1 + j);
+  };
+  auto tile_src = [&](int tile) {
+    const int box = tile / P.tiles, t = tile - box * P.tiles;
+    return modes + static_cast<i64>(box) * m * m1 + min(t * TR, m1 - TR);
+  };
+  const double* __restrict__ sc = half + static_cast<i64>(half_sine_rows(m)) * 2 * kh;
+  for (int r = warp; r < 16 * NTW; r += nwarp) {
+    const bool have = r < half_sine_rows(m);  // table rows beyond the half table: zeros
+    for (int c = lane; c < 2 * kh; c += 32) {
+      if (have) cp_async8(Bs + r * LDB + c, half + static_cast<i64>(r) * 2 * kh + c);
+      else Bs[r * LDB + c] = 0.0;
+    }
+  }
+  for (int i = tid; i < m; i += nth) cp_async8(Ss + i, sc + i);
+  // padding rows of both A tiles, never overwritten (the table's padding columns are zero, but
+  // 0 * garbage may be NaN)
+  for (int buf = 0; buf < 2; ++buf) {
+    double* As = Ab + buf * KA * LDA;
+    for (int idx = tid; idx < (kh - P.ne) * TR; idx += nth) As[(P.ne + idx / TR) * LDA + idx % TR] = 0.0;
+    for (int idx = tid; idx < (P.no4 - m / 2) * TR; idx += nth) As[(kh + m / 2 + idx / TR) * LDA + idx % TR] = 0.0;
+  }
+  int tile = blockIdx.x;
+  if (tile < ntile) {
+    const double* __restrict__ src = tile_src(tile);
+    for (int i = 0; i < nitem; ++i) issue_item(src, Ab, i);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  const int r8 = lane >> 2, c4 = lane & 3, r0 = 16 * (warp >> 1), nb0 = (warp & 1) * NTW;
+  for (int it = 0; tile < ntile; tile += gridDim.x, ++it) {
+    // this tile's group was committed a round ago; the next tile's loads are issued between
+    // the MMA steps below (one item per step) and committed after them
+    const int buf = it & 1, next = tile + gridDim.x;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const double* __restrict__ nsrc = next < ntile ? tile_src(next) : nullptr;
+    double* An = Ab + (buf ^ 1) * KA * LDA;
+    int ni = 0;
+    const double* As = Ab + buf * KA * LDA + r0 + r8;
+    const double* Bw = Bs + (8 * nb0 + r8) * LDB + c4;
+    double E[2][NTW][2], O[2][NTW][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < NTW; ++b) E[a][b][0] = E[a][b][1] = O[a][b][0] = O[a][b][1] = 0.0;
+#pragma unroll 2
+    for (int ks = 0; ks < kh; ks += 4) {
+      const double a0 = As[(ks + c4) * LDA], a1 = As[(ks + c4) * LDA + 8];
+      if (nsrc && ni < nitem) issue_item(nsrc, An, ni++);
+#pragma unroll
+      for (int b = 0; b < NTW; ++b) {
+        const double fb = Bw[8 * b * LDB + ks];
+        dmma(E[0][b], a0, fb);
+        dmma(E[1][b], a1, fb);
+      }
+    }
+#pragma unroll 2
+    for (int ks = 0; ks < P.no4; ks += 4) {
+      const double a0 = As[(kh + ks + c4) * LDA], a1 = As[(kh + ks + c4) * LDA + 8];
+      if (nsrc && ni < nitem) issue_item(nsrc, An, ni++);
+#pragma unroll
+      for (int b = 0; b < NTW; ++b) {
+        const double fb = Bw[8 * b * LDB + kh + ks];
+        dmma(O[0][b], a0, fb);
+        dmma(O[1][b], a1, fb);
+      }
+    }
+    if (nsrc)
+      for (; ni < nitem; ++ni) issue_item(nsrc, An, ni);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    // out(q) = sc_q (E + O), out(m-1-q) = sc_{m-1-q} (E - O) straight from the accumulators
+    const int box = tile / P.tiles, t = tile - box * P.tiles;
+    const int j0 = min(t * TR, m1 - TR);
+    const int bx = box % P.nbox0, by = box / P.nbox0;
+    const int qb = 8 * nb0 + 2 * c4;  // this thread's first output of n tile 0
+    double* __restrict__ dst = e + bx * P.out_bs0 + by * P.out_bs1 + static_cast<i64>(j0 + r0 + r8) * P.out_stride;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      double* __restrict__ pq = dst + static_cast<i64>(8 * a) * P.out_stride + qb;
+      double* __restrict__ pm = dst + static_cast<i64>(8 * a) * P.out_stride + (m - 1 - qb);
+#pragma unroll
+      for (int b = 0; b < NTW; ++b) {
+        if (8 * (nb0 + b) + 7 < P.mh - 1) {  // warp-uniform: every output of the tile and its mirror exist
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            pq[8 * b + h] = Ss[qb + 8 * b + h] * (E[a][b][h] + O[a][b][h]);
+            pm[-(8 * b + h)] = Ss[m - 1 - qb - 8 * b - h] * (E[a][b][h] - O[a][b][h]);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = qb + 8 * b + h;
+            if (q < P.mh) {
+              pq[8 * b + h] = Ss[q] * (E[a][b][h] + O[a][b][h]);
+              if (m - 1 - q != q) pm[-(8 * b + h)] = Ss[m - 1 - q] * (E[a][b][h] - O[a][b][h]);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with this A tile before the next round refills it
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+int strip_back_warps(int m1) {
+  if (const char* ev = std::getenv("ASDSM_STRIP_BACK_NW")) return std::max(2, std::min(8, std::atoi(ev)));
+  // rows per tile = 16 x warps: the fewest padded rows over 4..7 warps (ties to more warps)
+  int best = 6;
+  double waste = 1e30;
+  for (int nw = 3; nw <= 7; ++nw) {
+    const int tr = 16 * nw;
+    if (m1 < tr) continue;
+    const double w = static_cast<double>((m1 + tr - 1) / tr * tr) / m1;
+    if (w <= waste) {
+      waste = w;
+      best = nw;
+    }
+  }
+  return best;
+}
+
+size_t strip_back_smem(int m, int nw) {
+  const int kh = half_sine_kh(m), no4 = ((m / 2) + 3) & ~3, ntw = (((m + 1) / 2 + 7) / 8 + 1) / 2;
+  return sizeof(double) * (static_cast<size_t>(16 * ntw) * (2 * kh + 4) + ((m + 1) & ~1) +
+                           2 * static_cast<size_t>(kh + no4) * (16 * nw + 4));
+}
 }  // namespace
 
 void dmma_prepare() {  // (a 3-stage cp.async variant of the dense kernel measured slower on both
@@ -334,6 +502,8 @@ void dmma_prepare() {  // (a 3-stage cp.async variant of the dense kernel measur
   static bool done = false;
   if (done) return;
   done = true;
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(strip_back_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(strip_back_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
@@ -372,6 +542,45 @@ void launch_dmma_transform(const double* in, double* out, const double* M, int m
   else if (ci) dmma_transform_kernel<true, false><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
   else if (co) dmma_transform_kernel<false, true><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
   else dmma_transform_kernel<false, false><<<grid, NTH, 0, s>>>(in, out, M, m, in_es, out_es, L);
+  ASDSM_CUDA_CHECK(cudaGetLastError());
+  ++g_kernel_launches;
+}
+
+bool strip_back_supported(int m, int m1) {
+  const int nt = ((m + 1) / 2 + 7) / 8;
+  if (m < 56 || nt < 4 || nt > 6 || m1 < 64) return false;
+  const int nw = strip_back_warps(m1);
+  return m1 >= 16 * nw && strip_back_smem(m, nw) <= 220 * 1024;
+}
+
+void launch_strip_back(const double* modes, double* e, const double* half, int m, int m1, int nbox0, int nbox1,
+                       i64 out_bs0, i64 out_bs1, i64 out_stride, cudaStream_t s) {
+  const int nw = strip_back_warps(m1), tr = 16 * nw;
+  StripBackArgs P{};
+  P.m = m;
+  P.m1 = m1;
+  P.kh = half_sine_kh(m);
+  P.mh = (m + 1) / 2;
+  P.ne = (m + 1) / 2;
+  P.no4 = ((m / 2) + 3) & ~3;
+  P.tiles = (m1 + tr - 1) / tr;
+  P.nbox0 = nbox0;
+  P.nboxes = nbox0 * nbox1;
+  P.out_bs0 = out_bs0;
+  P.out_bs1 = out_bs1;
+  P.out_stride = out_stride;
+  const long long ntile = static_cast<long long>(nbox0) * nbox1 * P.tiles;
+  if (ntile > 0x7fffffffLL) throw AsdsmError(kUnsupported, "strip back transform: too many tiles");
+  // persistent: as many CTAs as are resident at once walk the tiles
+  const size_t smem_q = strip_back_smem(m, nw);
+  int per_sm = 1;
+  if ((P.mh + 7) / 8 <= 4) ASDSM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, strip_back_kernel<2>, 64 * nw, smem_q));
+  else ASDSM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, strip_back_kernel<3>, 64 * nw, smem_q));
+  const long long grid = std::min<long long>(ntile, static_cast<long long>(kNumSms) * std::max(per_sm, 1));
+  const size_t smem = strip_back_smem(m, nw);
+  const int nt = (P.mh + 7) / 8;  // 4..6 (strip_back_supported): a warp pair covers 2 x 2 or 2 x 3 n tiles
+  if (nt <= 4) strip_back_kernel<2><<<static_cast<unsigned>(grid), 64 * nw, smem, s>>>(modes, e, half, P);
+  else strip_back_kernel<3><<<static_cast<unsigned>(grid), 64 * nw, smem, s>>>(modes, e, half, P);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }

@@ -33,5 +33,10 @@ void launch_dmma_eo_transform(bool back, const double* in, double* out, const do
                               i64 out_es, const GemmLines& L, cudaStream_t s);
 void launch_dmma_transform(const double* in, double* out, const double* M, int m, i64 in_es, i64 out_es,
                            const GemmLines& L, cudaStream_t s);
+// Back transform of hole strips with the half table resident in shared memory: modes
+// [box = bx + nbox0 by][k < m][j < m1] -> e[bx out_bs0 + by out_bs1 + j out_stride + i], i < m.
+bool strip_back_supported(int m, int m1);
+void launch_strip_back(const double* modes, double* e, const double* half, int m, int m1, int nbox0, int nbox1,
+                       i64 out_bs0, i64 out_bs1, i64 out_stride, cudaStream_t s);
 
 }  // namespace asdsm_b200

@@ -695,6 +695,14 @@ void Solver::fill(double* e, const double* b, cudaStream_t s, int stage) {
     G.out_bs[1] = static_cast<i64>(A.n1) * g_fine_.stride[1];
     G.nlines = static_cast<i64>(A.m1) * A.nbox0 * A.nbox1;
     const i64 in_es = part ? A.m1 : 1;  // [hole][k][j] from the partition solve, else [hole][j][k]
+    // strips: the table-resident back transform (ASDSM_STRIP_BACK=0: the generic even/odd GEMM;
+    // read at capture time)
+    const char* sb = std::getenv("ASDSM_STRIP_BACK");
+    if (strips && part && strip_back_supported(A.m0, A.m1) && !(sb && sb[0] == '0') &&
+        std::getenv("ASDSM_DENSE_GEMM") == nullptr) {
+      launch_strip_back(modes, e, T.half[0], A.m0, A.m1, A.nbox0, A.nbox1, G.out_bs[0], G.out_bs[1], g_fine_.stride[1], s);
+      return;
+    }
     if (A.m0 >= eo_min_modes() && std::getenv("ASDSM_DENSE_GEMM") == nullptr)
       launch_dmma_eo_transform(true, modes, e, T.half[0], A.m0, in_es, 1, G, s);
     else launch_dmma_transform(modes, e, T.V[0], A.m0, in_es, 1, G, s);

@@ -418,6 +418,27 @@ def test_ymarch2d_pass_bitwise(spec, nf, nc, iters, monkeypatch):
     assert np.all(np.abs(a - b) <= 1e-14 * b)
 
 
+@pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:2:5", 0, 0, 4), ("ex:1:1", 2049, 4, 4)])
+def test_strip_back_resident_agrees(spec, nf, nc, iters, monkeypatch):
+    """Strip back transform with the half sine table resident in shared memory (default,
+    dmma_gemm.cu strip_back_kernel: whole-K tiles, E and O in one thread) against the generic
+    even/odd DMMA GEMM (ASDSM_STRIP_BACK=0): the same sums in the same k order."""
+    opts = pb.IterateOptions(tol=0.0, max_iter=iters, stagnation_window=0, rng_seed=4)
+    ctx, _, _ = _ctx(spec, nf, nc)
+    st_s = ctx.iterate(opts)
+    assert any("strip_back_kernel" in k for k in ctx.kernels()), sorted(ctx.kernels())
+    monkeypatch.setenv("ASDSM_STRIP_BACK", "0")
+    ctx1, _, _ = _ctx(spec, nf, nc)
+    st_w = ctx1.iterate(opts)
+    assert_variant_ran(ctx, ctx1)
+    a = np.array([h.res_l2 for h in st_s.history])
+    b = np.array([h.res_l2 for h in st_w.history])
+    k = np.arange(len(b))
+    assert len(a) == len(b)
+    assert np.all(np.abs(a - b) <= b * 1e-11 * 10.0 ** (k / 4.0) + 1e-14 * b[0])
+    assert np.max(np.abs(st_s.u - st_w.u)) <= 1e-8 * np.max(np.abs(st_w.u))
+
+
 @pytest.mark.parametrize("switch", ["ASDSM_ZC3D", "ASDSM_UPD3D_FUSED"])
 @pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 5), ("cfg:4:1", 99, 9, 4), ("ex:4:1", 24, 4, 6)])
 def test_zmarch3d_pass_bitwise(spec, nf, nc, iters, switch, monkeypatch):
