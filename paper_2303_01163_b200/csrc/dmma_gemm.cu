@@ -180,29 +180,48 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
   constexpr int PB = (EQ * 2 * EK) / ENT2;  // 8
   double ra[PA], rb[PB];
   auto load = [&](int k0) {
+    if (kBack) {
 #pragma unroll
-    for (int r = 0; r < PA; ++r) {
-      const int e = tid + r * ENT2;
-      int pl, c;  // c in [0, 2 EK): back: mode 2 k0 + c; forward: (j = k0 + c/2, parity = mirror)
-      if (kContigIn) {
-        pl = e / (2 * EK);
-        c = e % (2 * EK);
-      } else {
-        pl = e % EP;
-        c = e / EP;
-      }
-      double v = 0.0;
-      if (p0 + pl < L.nlines) {
-        if (kBack) {
+      for (int r = 0; r < PA; ++r) {
+        const int e = tid + r * ENT2;
+        int pl, c;  // c in [0, 2 EK): mode 2 k0 + c
+        if (kContigIn) {
+          pl = e / (2 * EK);
+          c = e % (2 * EK);
+        } else {
+          pl = e % EP;
+          c = e / EP;
+        }
+        double v = 0.0;
+        if (p0 + pl < L.nlines) {
           const int k = 2 * k0 + c;
           if (k < m) v = __ldg(in + s_ib[pl] + static_cast<i64>(k) * in_es);
-        } else {
-          const int j = k0 + (c >> 1);
-          const int jj = (c & 1) ? m - 1 - j : j;
-          if (j < mh) v = __ldg(in + s_ib[pl] + static_cast<i64>(jj) * in_es) * __ldg(ci + jj);
         }
+        ra[r] = v;
       }
-      ra[r] = v;
+    } else {
+      // forward: a thread loads the pair g_j = ci_j in(j), g_{m-1-j} of its (line, j) elements, so
+      // h+ / h- are formed in registers when the tile is stored (no combine pass over the tile)
+#pragma unroll
+      for (int r = 0; r < PA / 2; ++r) {
+        const int e = tid + r * ENT2;
+        int pl, jl;
+        if (kContigIn) {
+          pl = e / EK;
+          jl = e % EK;
+        } else {
+          pl = e % EP;
+          jl = e / EP;
+        }
+        const int j = k0 + jl, jm = m - 1 - j;
+        double g = 0.0, gm = 0.0;
+        if (p0 + pl < L.nlines && j < mh) {
+          g = __ldg(in + s_ib[pl] + static_cast<i64>(j) * in_es) * __ldg(ci + j);
+          gm = jm == j ? 0.0 : __ldg(in + s_ib[pl] + static_cast<i64>(jm) * in_es) * __ldg(ci + jm);
+        }
+        ra[2 * r] = g;
+        ra[2 * r + 1] = gm;
+      }
     }
 #pragma unroll
     for (int r = 0; r < PB; ++r) {
@@ -219,19 +238,38 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
     }
   };
   auto store = [&]() {
+    if (kBack) {
 #pragma unroll
-    for (int r = 0; r < PA; ++r) {
-      const int e = tid + r * ENT2;
-      int pl, c;
-      if (kContigIn) {
-        pl = e / (2 * EK);
-        c = e % (2 * EK);
-      } else {
-        pl = e % EP;
-        c = e / EP;
+      for (int r = 0; r < PA; ++r) {
+        const int e = tid + r * ENT2;
+        int pl, c;
+        if (kContigIn) {
+          pl = e / (2 * EK);
+          c = e % (2 * EK);
+        } else {
+          pl = e % EP;
+          c = e / EP;
+        }
+        if (c & 1) AO[pl][c >> 1] = ra[r];
+        else AE[pl][c >> 1] = ra[r];
       }
-      if (c & 1) AO[pl][c >> 1] = ra[r];
-      else AE[pl][c >> 1] = ra[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < PA / 2; ++r) {
+        const int e = tid + r * ENT2;
+        int pl, jl;
+        if (kContigIn) {
+          pl = e / EK;
+          jl = e % EK;
+        } else {
+          pl = e % EP;
+          jl = e / EP;
+        }
+        // h+ = g_j + g_{m-1-j}, h- = g_j - g_{m-1-j}; the middle row alone (its mirror loaded as
+        // 0: g + 0 and g - 0 are g); beyond the half (g = gm = 0) both are 0
+        AE[pl][jl] = ra[2 * r] + ra[2 * r + 1];
+        AO[pl][jl] = ra[2 * r] - ra[2 * r + 1];
+      }
     }
 #pragma unroll
     for (int r = 0; r < PB; ++r) {
@@ -254,17 +292,6 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
   for (int k0 = 0; k0 < K; k0 += EK) {
     store();
     __syncthreads();
-    if (!kBack) {
-      // forward: AE/AO hold g_j / g_{m-1-j}; make them h+ / h- (g_j alone at the middle row)
-      for (int t = tid; t < EP * EK; t += ENT2) {
-        const int pl = t / EK, jl = t % EK, j = k0 + jl;
-        const double g = AE[pl][jl], gm = AO[pl][jl];
-        const bool mid = (m - 1 - j) == j;
-        AE[pl][jl] = mid ? g : g + gm;
-        AO[pl][jl] = mid ? g : g - gm;
-      }
-      __syncthreads();
-    }
     if (k0 + EK < K) load(k0 + EK);
 #pragma unroll
     for (int kk = 0; kk < EK; kk += 4) {
