@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NTH, ASDSM_DENSE_MINB) dmma_transform_kernel(c
 constexpr int EP = 64, EQ = 64, EK = 16, ELD2 = EK + 4, ENT2 = 256;
 constexpr size_t kEo2Smem = sizeof(double) * 4 * EP * ELD2 + 2 * EP * sizeof(i64);
 
-template <bool kBack, bool kContigIn>
+template <bool kBack, bool kContigIn, int EQT>
 __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                            const double* __restrict__ SH, const double* __restrict__ sc,
                                                            int m, int kh, i64 in_es, i64 out_es, GemmLines L) {
@@ -158,10 +158,11 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
   i64* s_ob = s_ib + EP;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp >> 2, wl = warp & 3;  // grp 0: E, 1: O
-  const int wp = (wl >> 1) * 32, wq = (wl & 1) * 32;
+  constexpr int NB = EQT / 16;  // 8-wide n tiles per warp (the warp tile is 32 x EQT / 2)
+  const int wp = (wl >> 1) * 32, wq = (wl & 1) * (EQT / 2);
   const int mh = (m + 1) >> 1;
   const i64 p0 = static_cast<i64>(blockIdx.y) * EP;
-  const int q0 = blockIdx.x * EQ;
+  const int q0 = blockIdx.x * EQT;
   const double* __restrict__ ci = sc + m;
   for (int t = tid; t < EP; t += ENT2) {
     i64 ib = 0, ob = 0;
@@ -170,14 +171,14 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
     s_ob[t] = ob;
   }
   __syncthreads();
-  double acc[4][4][2];
+  double acc[4][NB][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int K = kBack ? kh : mh;
   constexpr int PA = (EP * 2 * EK) / ENT2;  // 8
-  constexpr int PB = (EQ * 2 * EK) / ENT2;  // 8
+  constexpr int PB = (EQT * 2 * EK) / ENT2;  // 8 (6)
   double ra[PA], rb[PB];
   auto load = [&](int k0) {
     if (kBack) {
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
         const int ql = e / (2 * EK), c = e % (2 * EK), half = c / EK, kl = c % EK;
         if (q0 + ql < mh && k0 + kl < kh) v = __ldg(SH + static_cast<i64>(q0 + ql) * 2 * kh + half * kh + k0 + kl);
       } else {  // B(n = kappa, k = j): SH[j][half kh + kappa], kappa contiguous
-        const int nl = e % EQ, c = e / EQ, half = c / EK, jl = c % EK;
+        const int nl = e % EQT, c = e / EQT, half = c / EK, jl = c % EK;
         if (q0 + nl < kh && k0 + jl < mh) v = __ldg(SH + static_cast<i64>(k0 + jl) * 2 * kh + half * kh + q0 + nl);
       }
       rb[r] = v;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
         if (c < EK) BE[ql][c] = rb[r];
         else BO[ql][c - EK] = rb[r];
       } else {
-        const int nl = e % EQ, c = e / EQ;
+        const int nl = e % EQT, c = e / EQT;
         if (c < EK) BE[nl][c] = rb[r];
         else BO[nl][c - EK] = rb[r];
       }
@@ -295,26 +296,26 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
     if (k0 + EK < K) load(k0 + EK);
 #pragma unroll
     for (int kk = 0; kk < EK; kk += 4) {
-      double fa[4], fb[4];
+      double fa[4], fb[NB];
 #pragma unroll
       for (int a = 0; a < 4; ++a) fa[a] = As[wp + a * 8 + r8][kk + c4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = Bs[wq + b * 8 + r8][kk + c4];
+      for (int b = 0; b < NB; ++b) fb[b] = Bs[wq + b * 8 + r8][kk + c4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(acc[a][b], fa[a], fb[b]);
+        for (int b = 0; b < NB; ++b) dmma(acc[a][b], fa[a], fb[b]);
     }
     __syncthreads();
   }
   if (kBack) {
     // E -> shared (over the A tiles), then the O warps combine: out(q), out(m-1-q)
-    double(*Ex)[EQ + 4] = reinterpret_cast<double(*)[EQ + 4]>(esm);
+    double(*Ex)[EQT + 4] = reinterpret_cast<double(*)[EQT + 4]>(esm);
     if (grp == 0) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NB; ++b) {
           Ex[wp + a * 8 + r8][wq + b * 8 + 2 * c4] = acc[a][b][0];
           Ex[wp + a * 8 + r8][wq + b * 8 + 2 * c4 + 1] = acc[a][b][1];
         }
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
         if (p0 + pl >= L.nlines) continue;
         const i64 ob = s_ob[pl];
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < NB; ++b)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int ql = wq + b * 8 + 2 * c4 + h, q = q0 + ql;
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
       if (p0 + pl >= L.nlines) continue;
       const i64 ob = s_ob[pl];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int kap = q0 + wq + b * 8 + 2 * c4 + h;
@@ -531,10 +532,14 @@ void dmma_prepare() {  // (a 3-stage cp.async variant of the dense kernel measur
   done = true;
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(strip_back_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(strip_back_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
-  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+#define ASDSM_EO2_ATTR(B, C)                                                                                      \
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<B, C, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem))); \
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(dmma_eo2_kernel<B, C, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEo2Smem)));
+  ASDSM_EO2_ATTR(true, true)
+  ASDSM_EO2_ATTR(true, false)
+  ASDSM_EO2_ATTR(false, true)
+  ASDSM_EO2_ATTR(false, false)
+#undef ASDSM_EO2_ATTR
 }
 
 void launch_dmma_eo_transform(bool back, const double* in, double* out, const double* half, int m, i64 in_es,
@@ -544,15 +549,25 @@ void launch_dmma_eo_transform(bool back, const double* in, double* out, const do
   const i64 pb = (L.nlines + EP - 1) / EP;
   if (pb > 65535) throw AsdsmError(kUnsupported, "transform batch too large for the grid");
   const int nq = back ? mh : kh;
-  dim3 grid(static_cast<unsigned>((nq + EQ - 1) / EQ), static_cast<unsigned>(pb));
+  // output tile width: 64, or 48 when that pads the nq outputs less (259-point slab axes: 130
+  // outputs are 3 tiles either way, 144 against 192 columns of MMAs; ASDSM_EO2_Q=64 forces 64)
+  const bool q48 = ((nq + 47) / 48) * 48 < ((nq + 63) / 64) * 64 && std::getenv("ASDSM_EO2_Q") == nullptr;
+  const int eq = q48 ? 48 : 64;
+  dim3 grid(static_cast<unsigned>((nq + eq - 1) / eq), static_cast<unsigned>(pb));
   const bool ci = in_es == 1;
+#define ASDSM_EO2_LAUNCH(B, C)                                                                                   \
+  do {                                                                                                           \
+    if (q48) dmma_eo2_kernel<B, C, 48><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);  \
+    else dmma_eo2_kernel<B, C, 64><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);      \
+  } while (0)
   if (back) {
-    if (ci) dmma_eo2_kernel<true, true><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
-    else dmma_eo2_kernel<true, false><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+    if (ci) ASDSM_EO2_LAUNCH(true, true);
+    else ASDSM_EO2_LAUNCH(true, false);
   } else {
-    if (ci) dmma_eo2_kernel<false, true><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
-    else dmma_eo2_kernel<false, false><<<grid, ENT2, kEo2Smem, s>>>(in, out, half, sc, m, kh, in_es, out_es, L);
+    if (ci) ASDSM_EO2_LAUNCH(false, true);
+    else ASDSM_EO2_LAUNCH(false, false);
   }
+#undef ASDSM_EO2_LAUNCH
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
 }
