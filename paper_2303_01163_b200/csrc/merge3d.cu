@@ -233,7 +233,7 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
       for (int C = 0; C < nc1; ++C) y[C + 1] = fam1_y(m, c, I, k2, C);
       double* mm = A.mF1[a] + static_cast<i64>(t) * (nc1 + 2);
       spline_second_derivs(m, c.f1, y, mm, dg, up, rh);
-      spline_segments(m, c.f1, yl, mm, A.sF1[a] + static_cast<i64>(t) * 4 * (nc1 + 1));
+      spline_segments(m, c.f1, yl, mm, A.sF1[a] + 4 * static_cast<i64>(t), 4 * static_cast<i64>(n1));
     } else if (t < n1 + n2) {
       const int l = t - n1;
       const int I = l % ncA, k1 = l / ncA;
@@ -242,7 +242,7 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
       for (int C = 0; C < nc2; ++C) y[C + 1] = fam2_y(m, c, I, k1, C);
       double* mm = A.mF2[a] + static_cast<i64>(l) * (nc2 + 2);
       spline_second_derivs(m, c.f2, y, mm, dg, up, rh);
-      spline_segments(m, c.f2, yl, mm, A.sF2[a] + static_cast<i64>(l) * 4 * (nc2 + 1));
+      spline_segments(m, c.f2, yl, mm, A.sF2[a] + 4 * static_cast<i64>(l), 4 * static_cast<i64>(n2));
     } else if (t < n1 + n2 + n3) {
       const int l = t - n1 - n2;
       const int I = l % ncA, C2 = l / ncA;
@@ -251,7 +251,7 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
       for (int C = 0; C < nc1; ++C) y[C + 1] = fam3_y(A, c, I, C2, C);
       double* mm = A.mF3a[a] + static_cast<i64>(l) * (nc1 + 2);
       spline_second_derivs(m, c.f1, y, mm, dg, up, rh);
-      spline_segments(m, c.f1, yl, mm, A.sF3a[a] + static_cast<i64>(l) * 4 * (nc1 + 1));
+      spline_segments(m, c.f1, yl, mm, A.sF3a[a] + 4 * static_cast<i64>(l), 4 * static_cast<i64>(n3));
     }
   } else {
     // fam3b: (I, k1), y = g(I, k1, C2) = fam3a spline (I, C2) at k1
@@ -261,10 +261,10 @@ __global__ void m3_derivs_kernel(Merge3DArgs A, int stage, const DevState* st) {
     y[0] = 0.0;
     y[nc2 + 1] = 0.0;
     for (int C2 = 0; C2 < nc2; ++C2)
-      y[C2 + 1] = spline_eval_seg(m, c.f1, A.sF3a[a] + static_cast<i64>(I + ncA * C2) * 4 * (nc1 + 1), k1 + 1);
+      y[C2 + 1] = spline_eval_seg(m, c.f1, A.sF3a[a] + 4 * static_cast<i64>(I + ncA * C2), 4 * static_cast<i64>(ncA) * nc2, k1 + 1);
     double* mm = A.mF3b[a] + static_cast<i64>(t) * (nc2 + 2);
     spline_second_derivs(m, c.f2, y, mm, dg, up, rh);
-    spline_segments(m, c.f2, yl, mm, A.sF3b[a] + static_cast<i64>(t) * 4 * (nc2 + 1));
+    spline_segments(m, c.f2, yl, mm, A.sF3b[a] + 4 * static_cast<i64>(t), 4 * static_cast<i64>(n));
   }
   (void)nf2;
 }
@@ -278,7 +278,7 @@ constexpr int kDerivWarps = 4;
 constexpr int kWarpKnots = 32;
 
 __device__ __forceinline__ void spline_warp(const MeshDev& m, int axis, double* ys, double* dg, double* up, double* rh,
-                                            double* mmS, double* mm, double* seg) {
+                                            double* mmS, double* mm, double* seg, i64 ss) {
   const int lane = threadIdx.x & 31;
   const int nc = m.nc[axis], n = nc + 2, ni = n - 2;
   __syncwarp();
@@ -315,7 +315,7 @@ __device__ __forceinline__ void spline_warp(const MeshDev& m, int axis, double* 
     c.y = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m0), m1)) / 6.0);
     c.z = m0 / 2.0;
     c.w = __dsub_rn(m1, m0) / __dmul_rn(6.0, h);
-    *reinterpret_cast<double4*>(seg + 4 * i) = c;
+    *reinterpret_cast<double4*>(seg + ss * i) = c;
   }
 }
 
@@ -339,19 +339,19 @@ __global__ void __launch_bounds__(32 * kDerivWarps) m3_derivs_warp_kernel(Merge3
       const int I = t % ncA, k2 = t / ncA;
       if (lane < nc1 + 2) ys[lane] = (lane == 0 || lane == nc1 + 1) ? 0.0 : fam1_y(m, c, I, k2, lane - 1);
       spline_warp(m, c.f1, ys, dg, up, rh, mmS, A.mF1[a] + static_cast<i64>(t) * (nc1 + 2),
-                  A.sF1[a] + static_cast<i64>(t) * 4 * (nc1 + 1));
+                  A.sF1[a] + 4 * static_cast<i64>(t), 4 * static_cast<i64>(n1));
     } else if (t < n1 + n2) {
       const int l = t - n1;
       const int I = l % ncA, k1 = l / ncA;
       if (lane < nc2 + 2) ys[lane] = (lane == 0 || lane == nc2 + 1) ? 0.0 : fam2_y(m, c, I, k1, lane - 1);
       spline_warp(m, c.f2, ys, dg, up, rh, mmS, A.mF2[a] + static_cast<i64>(l) * (nc2 + 2),
-                  A.sF2[a] + static_cast<i64>(l) * 4 * (nc2 + 1));
+                  A.sF2[a] + 4 * static_cast<i64>(l), 4 * static_cast<i64>(n2));
     } else if (t < n1 + n2 + n3) {
       const int l = t - n1 - n2;
       const int I = l % ncA, C2 = l / ncA;
       if (lane < nc1 + 2) ys[lane] = (lane == 0 || lane == nc1 + 1) ? 0.0 : fam3_y(A, c, I, C2, lane - 1);
       spline_warp(m, c.f1, ys, dg, up, rh, mmS, A.mF3a[a] + static_cast<i64>(l) * (nc1 + 2),
-                  A.sF3a[a] + static_cast<i64>(l) * 4 * (nc1 + 1));
+                  A.sF3a[a] + 4 * static_cast<i64>(l), 4 * static_cast<i64>(n3));
     }
   } else {
     const int n = ncA * nf1;
@@ -360,9 +360,10 @@ __global__ void __launch_bounds__(32 * kDerivWarps) m3_derivs_warp_kernel(Merge3
     if (lane < nc2 + 2)
       ys[lane] = (lane == 0 || lane == nc2 + 1)
                      ? 0.0
-                     : spline_eval_seg(m, c.f1, A.sF3a[a] + static_cast<i64>(I + ncA * (lane - 1)) * 4 * (nc1 + 1), k1 + 1);
+                     : spline_eval_seg(m, c.f1, A.sF3a[a] + 4 * static_cast<i64>(I + ncA * (lane - 1)),
+                                       4 * static_cast<i64>(ncA) * nc2, k1 + 1);
     spline_warp(m, c.f2, ys, dg, up, rh, mmS, A.mF3b[a] + static_cast<i64>(t) * (nc2 + 2),
-                A.sF3b[a] + static_cast<i64>(t) * 4 * (nc2 + 1));
+                A.sF3b[a] + 4 * static_cast<i64>(t), 4 * static_cast<i64>(n));
   }
   (void)nf2;
 }
@@ -374,21 +375,23 @@ __global__ void m3_apply_kernel(Merge3DArgs A, const DevState* st) {
   const int a = blockIdx.y;  // slab
   const MeshDev& m = A.m;
   const PlaneCtx c = plane_ctx(A, a);
-  const int ncA = m.nc[a], nc1 = m.nc[c.f1], nc2 = m.nc[c.f2];
-  const int e0 = c.se.e[0], e1 = c.se.e[1];
-  const i64 total = static_cast<i64>(c.se.e[0]) * c.se.e[1] * c.se.e[2];
-  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+  const int ncA = m.nc[a];
+  const unsigned e0 = c.se.e[0], e1 = c.se.e[1];
+  const unsigned total = e0 * e1 * static_cast<unsigned>(c.se.e[2]);  // < 2^31: checked at launch
+  const i64 ss1 = 4 * static_cast<i64>(ncA) * m.nf[c.f2], ss2 = 4 * static_cast<i64>(ncA) * m.nf[c.f1];
+  const double* __restrict__ slab = c.slab;
+  double* __restrict__ outp = A.corrected[a];
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     int q[3];
-    const i64 r = t / e0;
+    const unsigned r = t / e0;
     q[0] = static_cast<int>(t - r * e0);
-    q[1] = static_cast<int>(r % e1);
     q[2] = static_cast<int>(r / e1);
+    q[1] = static_cast<int>(r - static_cast<unsigned>(q[2]) * e1);
     const int I = q[a], k1 = q[c.f1], k2 = q[c.f2];
-    const double s1 = spline_eval_seg(m, c.f1, A.sF1[a] + static_cast<i64>(I + ncA * k2) * 4 * (nc1 + 1), k1 + 1);
-    const double s2 = spline_eval_seg(m, c.f2, A.sF2[a] + static_cast<i64>(I + ncA * k1) * 4 * (nc2 + 1), k2 + 1);
-    const double s3 = spline_eval_seg(m, c.f2, A.sF3b[a] + static_cast<i64>(I + ncA * k1) * 4 * (nc2 + 1), k2 + 1);
-    A.corrected[a][t] = __dadd_rn(c.slab[t], __dsub_rn(__dadd_rn(s1, s2), s3));
+    const double s1 = spline_eval_seg(m, c.f1, A.sF1[a] + 4 * static_cast<i64>(I + ncA * k2), ss1, k1 + 1);
+    const double s2 = spline_eval_seg(m, c.f2, A.sF2[a] + 4 * static_cast<i64>(I + ncA * k1), ss2, k2 + 1);
+    const double s3 = spline_eval_seg(m, c.f2, A.sF3b[a] + 4 * static_cast<i64>(I + ncA * k1), ss2, k2 + 1);
+    outp[t] = __dadd_rn(slab[t], __dsub_rn(__dadd_rn(s1, s2), s3));
   }
 }
 
@@ -399,32 +402,31 @@ __global__ void m3_apply_kernel(Merge3DArgs A, const DevState* st) {
 __global__ void m4_kernel(Merge3DArgs A, double* out, const DevState* st) {
   if (!st->active || !st->have_e) return;
   const MeshDev& m = A.m;
-  const i64 nf0 = m.nf[0], nf1 = m.nf[1], nf2 = m.nf[2];
-  const i64 fx = nf0 - m.nc[0], fy = nf1 - m.nc[1];  // non-coarse counts per axis
-  const i64 n0 = static_cast<i64>(m.nc[0]) * nf1 * nf2;
-  const i64 n1 = fx * m.nc[1] * nf2;
-  const i64 n2 = fx * fy * m.nc[2];
-  for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < n0 + n1 + n2;
-       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+  const i64 nf0 = m.nf[0], nf1 = m.nf[1];
+  // 32-bit point counts (checked at launch): 64-bit divisions were the kernel's cost
+  const unsigned unf1 = m.nf[1], unf2 = m.nf[2], nc0 = m.nc[0], nc1 = m.nc[1], nc2 = m.nc[2];
+  const unsigned fx = m.nf[0] - m.nc[0], fy = m.nf[1] - m.nc[1];  // non-coarse counts per axis
+  const unsigned n0 = nc0 * unf1 * unf2;
+  const unsigned n1 = fx * nc1 * unf2;
+  const unsigned n2 = fx * fy * nc2;
+  const unsigned s0 = m.n[0] - 1, s1 = m.n[1] - 1;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n0 + n1 + n2; t += gridDim.x * blockDim.x) {
     int f[3];
-    auto noncoarse = [&](int a, i64 q) {  // q-th non-coarse fine index along axis a
-      return static_cast<int>(q + q / (m.n[a] - 1));
-    };
     if (t < n0) {
-      const i64 q = t;
-      f[0] = (static_cast<int>(q % m.nc[0]) + 1) * m.n[0] - 1;
-      f[1] = static_cast<int>((q / m.nc[0]) % nf1);
-      f[2] = static_cast<int>(q / (m.nc[0] * nf1));
+      const unsigned q = t, r = q / nc0, z = r / unf1;
+      f[0] = static_cast<int>((q - r * nc0 + 1) * m.n[0] - 1);
+      f[1] = static_cast<int>(r - z * unf1);
+      f[2] = static_cast<int>(z);
     } else if (t < n0 + n1) {
-      const i64 q = t - n0;
-      f[0] = noncoarse(0, q % fx);
-      f[1] = (static_cast<int>((q / fx) % m.nc[1]) + 1) * m.n[1] - 1;
-      f[2] = static_cast<int>(q / (fx * m.nc[1]));
+      const unsigned q = t - n0, r = q / fx, z = r / nc1, x = q - r * fx;
+      f[0] = static_cast<int>(x + x / s0);  // x-th non-coarse fine index
+      f[1] = static_cast<int>((r - z * nc1 + 1) * m.n[1] - 1);
+      f[2] = static_cast<int>(z);
     } else {
-      const i64 q = t - n0 - n1;
-      f[0] = noncoarse(0, q % fx);
-      f[1] = noncoarse(1, (q / fx) % fy);
-      f[2] = (static_cast<int>(q / (fx * fy)) + 1) * m.n[2] - 1;
+      const unsigned q = t - n0 - n1, r = q / fx, c = r / fy, x = q - r * fx, y = r - c * fy;
+      f[0] = static_cast<int>(x + x / s0);
+      f[1] = static_cast<int>(y + y / s1);
+      f[2] = static_cast<int>((c + 1) * m.n[2] - 1);
     }
     bool on[3];
     int cc[3];
@@ -497,11 +499,13 @@ void launch_merge3d(const Merge3DArgs& A, double* out, DevState* st, cudaStream_
     m3_derivs_kernel<<<dim3((nl + 31) / 32, 3), 32, 0, s>>>(A, 0, st);
     m3_derivs_kernel<<<dim3((nl3 + 31) / 32, 3), 32, 0, s>>>(A, 1, st);
   }
+  if (ns >= (i64{1} << 31)) throw AsdsmError(kUnsupported, "3D merge: slab arrays of 2^31 points or more");
   m3_apply_kernel<<<dim3(nblk(ns, 256, 3 * kNumSms), 3), 256, 0, s>>>(A, st);
   g_kernel_launches += 3;
   const i64 nskel = static_cast<i64>(m.nc[0]) * m.nf[1] * m.nf[2] +
                    static_cast<i64>(m.nf[0] - m.nc[0]) * m.nc[1] * m.nf[2] +
                    static_cast<i64>(m.nf[0] - m.nc[0]) * (m.nf[1] - m.nc[1]) * m.nc[2];
+  if (nskel >= (i64{1} << 31)) throw AsdsmError(kUnsupported, "3D merge: 2^31 skeleton points or more");
   m4_kernel<<<nblk(nskel, 256, 32 * kNumSms), 256, 0, s>>>(A, out, st);
   ++g_kernel_launches;
   ASDSM_CUDA_CHECK(cudaGetLastError());

@@ -55,28 +55,31 @@ __device__ __forceinline__ double spline_eval(const MeshDev& m, int axis, Y y, c
 }
 
 // The per-interval coefficients spline_eval forms, (y_i, c1, c2, c3) for i = 0..nc, so that a
-// line evaluated at many points pays the divisions once (bitwise the same values).
+// line evaluated at many points pays the divisions once (bitwise the same values).  Tables are
+// interval-major: interval i of a line sits at seg + i * ss (ss = 4 x the family's line count),
+// so the lines of neighbouring points read neighbouring 32-byte entries.
 template <typename Y>
-__device__ inline void spline_segments(const MeshDev& m, int axis, Y y, const double* mm, double* seg) {
+__device__ inline void spline_segments(const MeshDev& m, int axis, Y y, const double* mm, double* seg, i64 ss) {
   const int nc = m.nc[axis];
   for (int i = 0; i <= nc; ++i) {
     const double xi = knot(m, axis, i), xi1 = knot(m, axis, i + 1);
     const double y0 = y(i), y1 = y(i + 1), m0 = mm[i], m1 = mm[i + 1];
     const double h = __dsub_rn(xi1, xi);
-    seg[4 * i] = y0;
-    seg[4 * i + 1] = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m0), m1)) / 6.0);
-    seg[4 * i + 2] = m0 / 2.0;
-    seg[4 * i + 3] = __dsub_rn(m1, m0) / __dmul_rn(6.0, h);
+    seg[ss * i] = y0;
+    seg[ss * i + 1] = __dsub_rn(__dsub_rn(y1, y0) / h, __dmul_rn(h, __dadd_rn(__dmul_rn(2.0, m0), m1)) / 6.0);
+    seg[ss * i + 2] = m0 / 2.0;
+    seg[ss * i + 3] = __dsub_rn(m1, m0) / __dmul_rn(6.0, h);
   }
 }
 
 // spline_eval from the segment table of the line
-__device__ __forceinline__ double spline_eval_seg(const MeshDev& m, int axis, const double* __restrict__ seg, int fi) {
+__device__ __forceinline__ double spline_eval_seg(const MeshDev& m, int axis, const double* __restrict__ seg, i64 ss,
+                                                  int fi) {
   const double x = static_cast<double>(fi) * m.h[axis];
   int i = fi / m.n[axis];
   if (i > m.nc[axis]) i = m.nc[axis];
   const double t = __dsub_rn(x, knot(m, axis, i));
-  const double4 c = *reinterpret_cast<const double4*>(seg + 4 * i);
+  const double4 c = *reinterpret_cast<const double4*>(seg + ss * i);
   return __dadd_rn(c.x, __dmul_rn(t, __dadd_rn(c.y, __dmul_rn(t, __dadd_rn(c.z, __dmul_rn(t, c.w))))));
 }
 
