@@ -45,6 +45,7 @@ struct H3Layout {  // shared memory, in doubles
   int rp, skx;     // plane rows (even/odd l order, zero gaps), row stride
   int kxo, kyo;    // padded odd mode counts
   int tc;          // planes resident at once (SYM: all)
+  int lg, lu;      // CAUSAL: thread (k, l0) owns the lines (k, l0 + lg u), u < lu
   size_t bytes;
 };
 struct Hole3DFusedArgs {

@@ -97,7 +97,8 @@ __device__ __forceinline__ HalfTab half_tab(const double* base, const H3Axis& a)
 // Forward transforms of a batch of nv vectors (length T.m; value i of vector v = in(v, i)) on
 // one axis: out(v, k) = sum_i W[k][i] v_i = sum_{i < he} S[i][k] h_{k&1}(i) with the pair sums
 // h+/-(i) = ci_i v_i +/- ci_{m-1-i} v_{m-1-i} (i < ho; the middle point alone), built in Hb
-// ([nv][2][he]) first.  Phase 1 and 2 are separated by a barrier; the caller syncs after.
+// ([nv][2][he]) first (fwd_pairs), then the dots (fwd_dots_mma).  The two phases are separated
+// by a barrier; the caller syncs after.
 template <typename In>
 __device__ __forceinline__ void fwd_pairs(const HalfTab& T, int nv, In in, double* Hb) {
   const int he = T.he, m = T.m;
@@ -114,22 +115,42 @@ __device__ __forceinline__ void fwd_pairs(const HalfTab& T, int nv, In in, doubl
     Hb[v * 2 * he + he + i] = hm;
   }
 }
+// The dots of the forward transforms on the DMMA pipe: per parity class the [modes x he] x [he x nv] product
+// out(v, k) = sum_i S[i][c(k)] h_{k&1}(v, i), one (parity, 8 modes, 8 vectors) tile per task
+// (tasks are dealt to warps by the caller: fwd_mma_tasks of them).  Rows i >= he of S are zero
+// in the table and the h operand is masked there, so the padded K steps add exact zeros.
+__device__ __forceinline__ int fwd_mma_tasks(const HalfTab& T, int nv) { return 2 * ((T.he + 7) >> 3) * ((nv + 7) >> 3); }
 template <typename Out>
-__device__ __forceinline__ void fwd_dots(const HalfTab& T, int nv, const double* Hb, Out out) {
-  const int he = T.he, m = T.m;
-  for (int q = threadIdx.x; q < nv * m; q += kH3Threads) {
-    const int v = q / m, k = q - v * m;
-    const double* hv = Hb + v * 2 * he + (k & 1) * he;
-    const double* sc = T.S + T.col(k);
-    double a0 = 0.0, a1 = 0.0;
-    int i = 0;
-    for (; i + 1 < he; i += 2) {
-      a0 = fma(sc[i * T.sh], hv[i], a0);
-      a1 = fma(sc[(i + 1) * T.sh], hv[i + 1], a1);
-    }
-    if (i < he) a0 = fma(sc[i * T.sh], hv[i], a0);
-    out(v, k, a0 + a1);
+__device__ __forceinline__ void fwd_dots_mma(const HalfTab& T, int nv, const double* Hb, int task, Out out) {
+  const int lane = threadIdx.x & 31, ar = lane >> 2, ak = lane & 3;
+  const int he = T.he;
+  const int nmt = (he + 7) >> 3, nnt = (nv + 7) >> 3;
+  const int par = task / (nmt * nnt), rem = task - par * nmt * nnt, mt = rem / nnt, nt = rem - mt * nnt;
+  const int v = 8 * nt + ar;  // this lane's B column (vector)
+  const bool vok = v < nv;
+  const double* hv = Hb + (vok ? (v * 2 + par) * he : 0);
+  const double* sa = T.S + (par ? T.khe : 0) + 8 * mt + ar;
+  double acc[2] = {0.0, 0.0};
+  const int ksteps = (he + 3) >> 2;
+  for (int kk = 0; kk < ksteps; ++kk) {
+    const int i = 4 * kk + ak;
+    const double a = sa[i * T.sh];
+    const double b = (vok && i < he) ? hv[i] : 0.0;
+    dmma884(acc, a, b);
   }
+  const int k = 2 * (8 * mt + ar) + par;  // mode of this lane's accumulator row
+  if (k < T.m) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int v2 = 8 * nt + 2 * ak + hh;
+      if (v2 < nv) out(v2, k, acc[hh]);
+    }
+  }
+}
+template <typename Out>
+__device__ __forceinline__ void fwd_dots_all(const HalfTab& T, int nv, const double* Hb, Out out) {
+  const int nt = fwd_mma_tasks(T, nv);
+  for (int task = threadIdx.x >> 5; task < nt; task += kH3Warps) fwd_dots_mma(T, nv, Hb, task, out);
 }
 
 // Back transform of `np` consecutive planes held in X (plane stride rp*skx; row r(l), column
@@ -248,11 +269,11 @@ __device__ void zface_transform(const double* __restrict__ e, const Hole3DFusedA
   __syncthreads();
   fwd_pairs(Tx, my, [&](int v, int i) { return F[v * mx + i]; }, Hb);  // rows C(., j)
   __syncthreads();
-  fwd_dots(Tx, my, Hb, [&](int v, int k, double x) { G[v * mx + k] = x; });
+  fwd_dots_all(Tx, my, Hb, [&](int v, int k, double x) { G[v * mx + k] = x; });
   __syncthreads();
   fwd_pairs(Ty, mx, [&](int v, int j) { return G[j * mx + v]; }, Hb);  // columns G(., k)
   __syncthreads();
-  fwd_dots(Ty, mx, Hb, [&](int v, int l, double x) { CH[l * mx + v] = x; });
+  fwd_dots_all(Ty, mx, Hb, [&](int v, int l, double x) { CH[l * mx + v] = x; });
   __syncthreads();
 }
 
@@ -334,8 +355,8 @@ __global__ void __launch_bounds__(kH3Threads, 1)
       return sg ? b0 - b1 : b0 + b1;
     }, H2);
     __syncthreads();
-    fwd_dots(Ty, 2 * mt, H1, [&](int v, int l, double x) { YA[v * my + l] = x; });
-    fwd_dots(Tx, 2 * mt, H2, [&](int v, int k, double x) { XB[v * mx + k] = x; });
+    fwd_dots_all(Ty, 2 * mt, H1, [&](int v, int l, double x) { YA[v * my + l] = x; });
+    fwd_dots_all(Tx, 2 * mt, H2, [&](int v, int k, double x) { XB[v * mx + k] = x; });
     __syncthreads();
     double* G = X + mx * my;
     double* HZ = G + mx * my;
@@ -460,15 +481,16 @@ __global__ void __launch_bounds__(kH3Threads, 1)
   face_weights(cx0, cx1, cy0, cy1);
   zface_transform(e, A, h, 0, X, X + mx * my, X + 2 * mx * my, CH0, Tx, Ty);
   for (int q = tid; q < L.xsize; q += kH3Threads) X[q] = 0.0;
-  // line state: lines c = tid + u * threads, mode (k, l) packed as k | l << 16
+  // line state: thread (k, l0) = (tid % mx, tid / mx) owns the lines (k, l0 + G u), u < U, G even:
+  // its lines share k, the l parity, the x-face term's address and sit G/2 plane rows apart, so a
+  // line step is two loads, three flops and a store at constant offsets
+  const int LG = L.lg;
+  const int tk = tid % mx, tl0 = tid / mx;
+  int nlines = 0;
+  if (tl0 < LG && tl0 < my) nlines = min(L.lu, (my - tl0 + LG - 1) / LG);
   double yv[kCausalLines];
-  int kl[kCausalLines];
 #pragma unroll
-  for (int u = 0; u < kCausalLines; ++u) {
-    const int c = tid + u * kH3Threads;
-    yv[u] = 0.0;
-    kl[u] = c < ncombo ? (c % mx) | ((c / mx) << 16) : -1;
-  }
+  for (int u = 0; u < kCausalLines; ++u) yv[u] = 0.0;
   // Ring values from raw skeleton values staged through shared memory one chunk ahead
   // (cp.async: no registers wait on the loads).  Per plane: XL[j] = e(ox-1, oy+j), XR[j] =
   // e(ox+mx, oy+j), YL[i] = e(ox+i, oy-1), YR[i] = e(ox+i, oy+my); plane 0 also needs the
@@ -562,30 +584,47 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     }, HBx);
     __syncthreads();
     stage_raw(ci + 2);  // this chunk's raw values are consumed (pair sums formed)
-    fwd_dots(Ty, 2 * np, HB, [&](int v, int l, double x) { V[(v >> 1) * nring + (v & 1) * my + l] = x; });
-    fwd_dots(Tx, 2 * np, HBx, [&](int v, int k, double x) { V[(v >> 1) * nring + 2 * my + (v & 1) * mx + k] = x; });
+    {  // both axes' dots as one task list over the warps (16 tiles at config 4: one per warp)
+      const int nty_ = fwd_mma_tasks(Ty, 2 * np), ntx_ = fwd_mma_tasks(Tx, 2 * np);
+      for (int task = tid >> 5; task < nty_ + ntx_; task += kH3Warps) {
+        if (task < nty_)
+          fwd_dots_mma(Ty, 2 * np, HB, task, [&](int v, int l, double x) { V[(v >> 1) * nring + (v & 1) * my + l] = x; });
+        else
+          fwd_dots_mma(Tx, 2 * np, HBx, task - nty_,
+                       [&](int v, int k, double x) { V[(v >> 1) * nring + 2 * my + (v & 1) * mx + k] = x; });
+      }
+    }
     __syncthreads();
 #ifdef ASDSM_H3_TRACE
     c1 = clock64();
     ph[0] += c1 - c0;
 #endif
-    double iv[kCausalLines];  // bidiagonal: one pivot per line for every t (L1-resident table)
-#pragma unroll
-    for (int u = 0; u < kCausalLines; ++u) iv[u] = kl[u] >= 0 ? __ldg(A.ipiv + tid + u * kH3Threads) : 0.0;
-    for (int tt = 0; tt < np; ++tt) {
-      const int t = t0 + tt;
-      const double* Vp = V + tt * nring;
-      double* Xp = X + tt * ps;
+    if (nlines > 0) {
+      double iv[kCausalLines], s0y[kCausalLines];  // bidiagonal: one pivot per line for every t (L1-resident table)
 #pragma unroll
       for (int u = 0; u < kCausalLines; ++u) {
-        if (kl[u] < 0) continue;
-        const int k = kl[u] & 0xffff, l = kl[u] >> 16;
-        double f = Tx.s0(k) * Vp[(k & 1) * my + l];
-        f = fma(Ty.s0(l), Vp[2 * my + (l & 1) * mx + k], f);
-        if (t == 0) f += CH0[l * mx + k];
-        const double y = (t == 0) ? f * iv[u] : (f - lft * yv[u]) * iv[u];
-        yv[u] = y;
-        Xp[rowof(l) * skx + Tx.col(k)] = y;
+        const int l = tl0 + LG * u;
+        iv[u] = u < nlines ? __ldg(A.ipiv + tk + mx * l) : 0.0;
+        s0y[u] = u < nlines ? Ty.s0(l) : 0.0;
+      }
+      const double s0x = Tx.s0(tk);
+      const int v1 = (tk & 1) * my + tl0, v2 = 2 * my + (tl0 & 1) * mx + tk;
+      const int xo = rowof(tl0) * skx + Tx.col(tk), xs = (LG >> 1) * skx;
+      for (int tt = 0; tt < np; ++tt) {
+        const int t = t0 + tt;
+        const double* Vp = V + tt * nring;
+        double* Xp = X + tt * ps + xo;
+        const double xb = Vp[v2];
+#pragma unroll
+        for (int u = 0; u < kCausalLines; ++u) {
+          if (u >= nlines) break;
+          double f = s0x * Vp[v1 + LG * u];
+          f = fma(s0y[u], xb, f);
+          if (t == 0) f += CH0[(tl0 + LG * u) * mx + tk];
+          const double y = (t == 0) ? f * iv[u] : (f - lft * yv[u]) * iv[u];
+          yv[u] = y;
+          Xp[u * xs] = y;
+        }
       }
     }
     __syncthreads();
@@ -662,6 +701,10 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     if (off > kMax) return false;
   } else {
     if (mx * my > kCausalLines * kH3Threads) return false;
+    // line ownership: thread (k, l0) takes l = l0 + lg u; lg even (one l parity per thread)
+    L.lg = std::max(2, std::min(kH3Threads / mx, (my + 1) & ~1) & ~1);
+    L.lu = (my + L.lg - 1) / L.lg;
+    if (L.lu > kCausalLines || mx * std::min(L.lg, my) > kH3Threads) return false;
     const int nring = 2 * (mx + my);
     L.faces = static_cast<int>(off);
     int tc = 0;
