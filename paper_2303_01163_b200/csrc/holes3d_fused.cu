@@ -153,6 +153,44 @@ __device__ __forceinline__ void fwd_dots_all(const HalfTab& T, int nv, const dou
   for (int task = threadIdx.x >> 5; task < nt; task += kH3Warps) fwd_dots_mma(T, nv, Hb, task, out);
 }
 
+// The MMA loops of the back transform with the tile count as a compile-time constant: a runtime
+// `if (j < n)` around each mma.sync costs a predicate, its own address arithmetic and a
+// WARPSYNC per MMA (8 instructions per DMMA in the profile); these are one LDS per operand.
+// step A: a = this lane's row of X (even then odd mode columns), b = rows of the half table
+template <int NT>
+__device__ __forceinline__ void step_a_mma(const double* Ar, const double* Sb, int sh, int khe, int kev, int kod,
+                                           double (&ae)[4][2], double (&ao)[4][2]) {
+  for (int kk = 0; kk < kev; ++kk) {
+    const double a = Ar[4 * kk];
+    const double* b = Sb + 4 * kk;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma884(ae[j], a, b[8 * j * sh]);
+  }
+  for (int kk = 0; kk < kod; ++kk) {
+    const double a = Ar[khe + 4 * kk];
+    const double* b = Sb + khe + 4 * kk;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma884(ao[j], a, b[8 * j * sh]);
+  }
+}
+// step B: a = rows of the y half table, b = rows of the plane (8-column tiles)
+template <int NT>
+__device__ __forceinline__ void step_b_mma(const double* Ay, const double* Pk0, int skx, int khe, int kev, int kod,
+                                           double (&ae)[4][2], double (&ao)[4][2]) {
+  for (int kk = 0; kk < kev; ++kk) {
+    const double a = Ay[4 * kk];
+    const double* Pk = Pk0 + 4 * kk * skx;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma884(ae[j], a, Pk[8 * j]);
+  }
+  for (int kk = 0; kk < kod; ++kk) {
+    const double a = Ay[khe + 4 * kk];
+    const double* Pk = Pk0 + (khe + 4 * kk) * skx;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma884(ao[j], a, Pk[8 * j]);
+  }
+}
+
 // Back transform of `np` consecutive planes held in X (plane stride rp*skx; row r(l), column
 // c(k); finite everywhere, zero where no mode lives), planes t0.. of the hole.
 __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const HalfTab& Ty, const Hole3DFusedArgs& A,
@@ -172,19 +210,14 @@ __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const 
       double ae[4][2], ao[4][2];
 #pragma unroll
       for (int j = 0; j < 4; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
-      for (int kk = 0; kk < kev; ++kk) {
-        const double a = Ar[4 * kk + ak];
-        const double* b = Tx.S + ar * Tx.sh + 4 * kk + ak;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < ntx) dmma884(ae[j], a, b[8 * j * Tx.sh]);
-      }
-      for (int kk = 0; kk < kod; ++kk) {
-        const double a = Ar[Tx.khe + 4 * kk + ak];
-        const double* b = Tx.S + ar * Tx.sh + Tx.khe + 4 * kk + ak;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < ntx) dmma884(ao[j], a, b[8 * j * Tx.sh]);
+      {
+        const double* Sb = Tx.S + ar * Tx.sh + ak;
+        switch (ntx) {
+          case 4: step_a_mma<4>(Ar + ak, Sb, Tx.sh, Tx.khe, kev, kod, ae, ao); break;
+          case 3: step_a_mma<3>(Ar + ak, Sb, Tx.sh, Tx.khe, kev, kod, ae, ao); break;
+          case 2: step_a_mma<2>(Ar + ak, Sb, Tx.sh, Tx.khe, kev, kod, ae, ao); break;
+          default: step_a_mma<1>(Ar + ak, Sb, Tx.sh, Tx.khe, kev, kod, ae, ao); break;
+        }
       }
       __syncwarp();
       if (rb * 8 + ar < rows) {
@@ -221,19 +254,11 @@ __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const 
     double ae[4][2], ao[4][2];
 #pragma unroll
     for (int j = 0; j < 4; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
-    for (int kk = 0; kk < kev; ++kk) {
-      const double a = Ay[4 * kk];
-      const double* Pk = P + (4 * kk + ak) * skx;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nn) dmma884(ae[j], a, Pk[8 * j]);
-    }
-    for (int kk = 0; kk < kod; ++kk) {
-      const double a = Ay[Ty.khe + 4 * kk];
-      const double* Pk = P + (Ty.khe + 4 * kk + ak) * skx;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < nn) dmma884(ao[j], a, Pk[8 * j]);
+    switch (nn) {
+      case 4: step_b_mma<4>(Ay, P + ak * skx, skx, Ty.khe, kev, kod, ae, ao); break;
+      case 3: step_b_mma<3>(Ay, P + ak * skx, skx, Ty.khe, kev, kod, ae, ao); break;
+      case 2: step_b_mma<2>(Ay, P + ak * skx, skx, Ty.khe, kev, kod, ae, ao); break;
+      default: step_b_mma<1>(Ay, P + ak * skx, skx, Ty.khe, kev, kod, ae, ao); break;
     }
     const int jr = 8 * jt + ar;
     if (jr < Ty.he) {
@@ -556,13 +581,12 @@ __global__ void __launch_bounds__(kH3Threads, 1)
 #ifdef ASDSM_H3_TRACE
   long long ph[4] = {0, 0, 0, 0}, c0 = clock64(), c1, c2, c3, c4;
 #endif
-  for (int t0 = 0; t0 < mt; t0 += TC) {
+  // pair sums of chunk ci from its staged raw ring values: (plane, sign) -> y transform of
+  // cx0 A0 +/- cx1 A1, x transform of cy0 B0 +/- cy1 B1
+  auto pairs_chunk = [&](int ci) {
+    const int t0 = ci * TC;
     const int np = min(TC, mt - t0);
-    const int ci = t0 / TC;
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();
     const double* RW = RAW + (ci & 1) * TC * nring;
-    // vectors: (plane, sign) -> y transform of cx0 A0 +/- cx1 A1, x transform of cy0 B0 +/- cy1 B1
     fwd_pairs(Ty, 2 * np, [&](int v, int j) {
       const int tt = v >> 1;
       const double* rp = RW + tt * nring;
@@ -582,7 +606,21 @@ __global__ void __launch_bounds__(kH3Threads, 1)
       const double b0 = cy0 * r0, b1 = cy1 * r1;
       return (v & 1) ? b0 - b1 : b0 + b1;
     }, HBx);
-    __syncthreads();
+  };
+  // Chunk schedule (4 CTA barriers per chunk): [top barrier] stage raw(ci+2), dots(ci) -> V |
+  // line steps -> X | step A | step B, then -- with no barrier -- the pair sums of chunk ci+1:
+  // they read RAW(ci+1) (landed before step A's barrier: the wait below) and write HB, which
+  // the dots of chunk ci released two barriers ago, so they fill the tail of step B.
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  __syncthreads();
+  for (int t0 = -TC; t0 < mt; t0 += TC) {  // the first pass only forms the pair sums of chunk 0
+    const int np = min(TC, mt - t0);
+    const int ci = t0 / TC;
+    if (t0 < 0) {
+      pairs_chunk(0);
+      continue;
+    }
+    __syncthreads();  // pair sums complete, RAW(ci) consumed, X free (step B of chunk ci-1 done)
     stage_raw(ci + 2);  // this chunk's raw values are consumed (pair sums formed)
     {  // both axes' dots as one task list over the warps (16 tiles at config 4: one per warp)
       const int nty_ = fwd_mma_tasks(Ty, 2 * np), ntx_ = fwd_mma_tasks(Tx, 2 * np);
@@ -628,18 +666,19 @@ __global__ void __launch_bounds__(kH3Threads, 1)
       }
     }
     __syncthreads();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // RAW(ci+1): visible after step A's barrier
 #ifdef ASDSM_H3_TRACE
     c2 = clock64();
     back_planes(X, np, t0, Tx, Ty, A, h, e, &c3);
-    __syncthreads();
     c4 = clock64();
+    if (t0 + TC < mt) pairs_chunk(ci + 1);
     ph[1] += c2 - c1;
     ph[2] += c3 - c2;
     ph[3] += c4 - c3;
     c0 = c4;
 #else
     back_planes(X, np, t0, Tx, Ty, A, h, e);
-    __syncthreads();
+    if (t0 + TC < mt) pairs_chunk(ci + 1);
 #endif
   }
 #ifdef ASDSM_H3_TRACE
