@@ -28,11 +28,13 @@ else
   full 1 "hole2d_fused_kernel" 5 hole
   full 1 "stencil2d_ym_kernel" 5 update
   full 1 "slabstep2d_kernel" 5 slabstep
-  full 2 "dmma_eo2_kernel" 5 back
+  full 2 "strip_back_kernel" 5 back
   full 2 "stencil2d_ym_kernel" 5 update
   full 2 "hole2d_part_kernel" 5 lines
+  full 2 "slab2d_fwd_kernel" 5 slabfwd
   full 3 "hole3d_fused_kernel" 3 hole
   full 3 "stencil3d_zm_kernel" 3 cand
+  full 3 "dmma_eo2_kernel" 6 slabtransform
   full 4 "hole3d_fused_kernel" 3 hole
   full 4 "stencil3d_zm_kernel" 3 cand
   full 4 "axpy_update_kernel" 3 axpy
@@ -40,5 +42,6 @@ else
   full 4 "m4_kernel" 3 m4
   full 4 "skel3d_dots_rows_kernel" 3 dots
   full 4 "dmma_eo2_kernel" 6 slabtransform
+  full 4 "gather_kernel" 6 gather
 fi
 echo done > $out/DONE_$what
