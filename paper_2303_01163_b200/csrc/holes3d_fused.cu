@@ -224,9 +224,18 @@ __device__ void back_planes(double* X, int np, int t0, const HalfTab& Tx, const 
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j >= ntx) break;
+          const int i0 = 8 * j + 2 * ak;
+          if (i0 + 1 < Tx.he && !(mx & 1)) {  // both points and both mirrors: two 16-byte stores
+            const int im1 = mx - 2 - i0;
+            *reinterpret_cast<double2*>(Ar + i0) =
+                make_double2(Tx.sc[i0] * (ae[j][0] + ao[j][0]), Tx.sc[i0 + 1] * (ae[j][1] + ao[j][1]));
+            *reinterpret_cast<double2*>(Ar + im1) =
+                make_double2(Tx.sc[im1] * (ae[j][1] - ao[j][1]), Tx.sc[im1 + 1] * (ae[j][0] - ao[j][0]));
+            continue;
+          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const int i = 8 * j + 2 * ak + hh;
+            const int i = i0 + hh;
             if (i < Tx.he) {
               const int im = mx - 1 - i;
               Ar[i] = Tx.sc[i] * (ae[j][hh] + ao[j][hh]);
@@ -302,7 +311,9 @@ __device__ void zface_transform(const double* __restrict__ e, const Hole3DFusedA
   __syncthreads();
 }
 
-template <bool CAUSAL>
+// NL: CAUSAL line slots per thread (5 covers config 4's 50 x 50 modes on 500 threads; the line
+// values live in registers across the GEMM phases, so unused slots cost spills)
+template <bool CAUSAL, int NL = kCausalLines>
 __global__ void __launch_bounds__(kH3Threads, 1)
     hole3d_fused_kernel(double* __restrict__ e, Hole3DFusedArgs A, const DevState* S) {
   if (!S->active || !S->have_e) return;
@@ -513,9 +524,9 @@ __global__ void __launch_bounds__(kH3Threads, 1)
   const int tk = tid % mx, tl0 = tid / mx;
   int nlines = 0;
   if (tl0 < LG && tl0 < my) nlines = min(L.lu, (my - tl0 + LG - 1) / LG);
-  double yv[kCausalLines];
+  double yv[NL];
 #pragma unroll
-  for (int u = 0; u < kCausalLines; ++u) yv[u] = 0.0;
+  for (int u = 0; u < NL; ++u) yv[u] = 0.0;
   // Ring values from raw skeleton values staged through shared memory one chunk ahead
   // (cp.async: no registers wait on the loads).  Per plane: XL[j] = e(ox-1, oy+j), XR[j] =
   // e(ox+mx, oy+j), YL[i] = e(ox+i, oy-1), YR[i] = e(ox+i, oy+my); plane 0 also needs the
@@ -527,27 +538,31 @@ __global__ void __launch_bounds__(kH3Threads, 1)
   const i64 esy = A.nf[0], esz = static_cast<i64>(A.nf[0]) * A.nf[1];
   const bool hxl = h.ox > 0, hxr = h.ox + mx < A.nf[0] && stn.has_right[0];
   const bool hyl = h.oy > 0, hyr = h.oy + my < A.nf[1] && stn.has_right[1];
+  // thread r < nring owns ring position r of every plane: its source offset within a plane and
+  // whether the neighbour exists are fixed for the kernel, a chunk is TC copies a plane apart
+  i64 rsrc = 0;
+  bool rok = false;
+  if (tid < nring) {
+    if (tid < 2 * my) {
+      const int f = tid / my, j = tid - f * my;
+      rok = f == 0 ? hxl : hxr;
+      rsrc = (f == 0 ? h.ox - 1 : h.ox + mx) + (h.oy + j) * esy;
+    } else {
+      const int r2 = tid - 2 * my, f = r2 / mx, i = r2 - f * mx;
+      rok = f == 0 ? hyl : hyr;
+      rsrc = (h.ox + i) + (f == 0 ? h.oy - 1 : h.oy + my) * esy;
+    }
+    rsrc += h.oz * esz;
+  }
   auto stage_raw = [&](int c) {
     const int t0c = c * TC;
-    if (t0c < mt) {
-      double* dst = RAW + (c & 1) * TC * nring;
+    if (t0c < mt && tid < nring) {
+      double* dst = RAW + (c & 1) * TC * nring + tid;
       const int npc = min(TC, mt - t0c);
-      for (int q = tid; q < npc * nring; q += kH3Threads) {
-        const int tt = q / nring, r = q - tt * nring;
-        const i64 zo = (h.oz + t0c + tt) * esz;
-        bool ok;
-        i64 p;
-        if (r < 2 * my) {
-          const int f = r / my, j = r - f * my;
-          ok = f == 0 ? hxl : hxr;
-          p = (f == 0 ? h.ox - 1 : h.ox + mx) + (h.oy + j) * esy + zo;
-        } else {
-          const int r2 = r - 2 * my, f = r2 / mx, i = r2 - f * mx;
-          ok = f == 0 ? hyl : hyr;
-          p = (h.ox + i) + (f == 0 ? h.oy - 1 : h.oy + my) * esy + zo;
-        }
-        if (ok) cp_async8(dst + q, e + p);
-        else dst[q] = 0.0;
+      const double* src = e + rsrc + t0c * esz;
+      for (int tt = 0; tt < npc; ++tt) {
+        if (rok) cp_async8(dst + tt * nring, src + tt * esz);
+        else dst[tt * nring] = 0.0;
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -638,9 +653,9 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     ph[0] += c1 - c0;
 #endif
     if (nlines > 0) {
-      double iv[kCausalLines], s0y[kCausalLines];  // bidiagonal: one pivot per line for every t (L1-resident table)
+      double iv[NL], s0y[NL];  // bidiagonal: one pivot per line for every t (L1-resident table)
 #pragma unroll
-      for (int u = 0; u < kCausalLines; ++u) {
+      for (int u = 0; u < NL; ++u) {
         const int l = tl0 + LG * u;
         iv[u] = u < nlines ? __ldg(A.ipiv + tk + mx * l) : 0.0;
         s0y[u] = u < nlines ? Ty.s0(l) : 0.0;
@@ -654,7 +669,7 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         double* Xp = X + tt * ps + xo;
         const double xb = Vp[v2];
 #pragma unroll
-        for (int u = 0; u < kCausalLines; ++u) {
+        for (int u = 0; u < NL; ++u) {
           if (u >= nlines) break;
           double f = s0x * Vp[v1 + LG * u];
           f = fma(s0y[u], xb, f);
@@ -800,7 +815,8 @@ std::vector<double> hole3d_half_table(const H3Axis& a, const std::vector<double>
 
 void launch_hole3d_fused(double* e, const Hole3DFusedArgs& A, bool causal, DevState* st, cudaStream_t s) {
   const unsigned nh = static_cast<unsigned>(A.nbox[0] * A.nbox[1] * A.nbox[2]);
-  if (causal) hole3d_fused_kernel<true><<<nh, kH3Threads, A.lay.bytes, s>>>(e, A, st);
+  if (causal && A.lay.lu <= 5) hole3d_fused_kernel<true, 5><<<nh, kH3Threads, A.lay.bytes, s>>>(e, A, st);
+  else if (causal) hole3d_fused_kernel<true><<<nh, kH3Threads, A.lay.bytes, s>>>(e, A, st);
   else hole3d_fused_kernel<false><<<nh, kH3Threads, A.lay.bytes, s>>>(e, A, st);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
@@ -812,6 +828,7 @@ void hole3d_fused_prepare() {  // outside any stream capture: the dynamic shared
   done = true;
   const int mx = 227 * 1024;
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole3d_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole3d_fused_kernel<true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ASDSM_CUDA_CHECK(cudaFuncSetAttribute(hole3d_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 }
 

@@ -203,7 +203,10 @@ def test_even_odd_transforms_agree(spec, nf, nc, iters, monkeypatch):
 
 
 @pytest.mark.parametrize("spec,nf,nc,iters", [("cfg:3:0", 129, 4, 6), ("cfg:3:0", 79, 4, 4),
-                                              ("cfg:4:1", 99, 4, 5), ("cfg:4:1", 254, 4, 3)])
+                                              ("cfg:4:1", 99, 4, 5), ("cfg:4:1", 254, 4, 3),
+                                              # m = 63 / 35: CAUSAL line ownership with 8 / 3 lines per
+                                              # thread (the 8-slot kernel; config 4's m = 50 takes 5)
+                                              ("cfg:4:1", 127, 1, 2), ("cfg:4:1", 71, 1, 2)])
 def test_fused_hole3d_fill_agrees(spec, nf, nc, iters, monkeypatch):
     """The one-kernel 3D hole fill (holes3d_fused.cu: faces, line solves and both DMMA back
     transforms per hole in shared memory; SYM schedule for the steady configs, CAUSAL plane

@@ -53,11 +53,11 @@ def test_config2_full_mesh_m409():
 def test_config3_hole_extent_m25_sym(nf, nc, seed):
     ctx = _run("cfg:3:0", nf, nc, 10, seed)
     assert ctx.config.factors == [26, 26, 26]
-    assert _has(ctx.kernels(), "hole3d_fused_kernel<false>"), sorted(ctx.kernels())
+    assert _has(ctx.kernels(), "hole3d_fused_kernel<false"), sorted(ctx.kernels())
 
 
 @pytest.mark.timeout(900)
 def test_config4_hole_extent_m50_causal():
     ctx = _run("cfg:4:3", 101, 1, 10, 3)
     assert ctx.config.factors == [51, 51, 51]
-    assert _has(ctx.kernels(), "hole3d_fused_kernel<true>"), sorted(ctx.kernels())
+    assert _has(ctx.kernels(), "hole3d_fused_kernel<true"), sorted(ctx.kernels())
