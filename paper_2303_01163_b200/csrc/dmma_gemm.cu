@@ -215,10 +215,13 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
           jl = e / EP;
         }
         const int j = k0 + jl, jm = m - 1 - j;
+        // raw values only: the ci factors are applied in store(), so no arithmetic waits on
+        // these loads before the MMA loop of the current tile (the product here stalled every
+        // warp on its global loads: long_scoreboard 40 % of the forward kernel's samples)
         double g = 0.0, gm = 0.0;
         if (p0 + pl < L.nlines && j < mh) {
-          g = __ldg(in + s_ib[pl] + static_cast<i64>(j) * in_es) * __ldg(ci + j);
-          gm = jm == j ? 0.0 : __ldg(in + s_ib[pl] + static_cast<i64>(jm) * in_es) * __ldg(ci + jm);
+          g = __ldg(in + s_ib[pl] + static_cast<i64>(j) * in_es);
+          gm = jm == j ? 0.0 : __ldg(in + s_ib[pl] + static_cast<i64>(jm) * in_es);
         }
         ra[2 * r] = g;
         ra[2 * r + 1] = gm;
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
       rb[r] = v;
     }
   };
-  auto store = [&]() {
+  auto store = [&](int k0s) {
     if (kBack) {
 #pragma unroll
       for (int r = 0; r < PA; ++r) {
@@ -266,10 +269,13 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
           pl = e % EP;
           jl = e / EP;
         }
-        // h+ = g_j + g_{m-1-j}, h- = g_j - g_{m-1-j}; the middle row alone (its mirror loaded as
-        // 0: g + 0 and g - 0 are g); beyond the half (g = gm = 0) both are 0
-        AE[pl][jl] = ra[2 * r] + ra[2 * r + 1];
-        AO[pl][jl] = ra[2 * r] - ra[2 * r + 1];
+        // g_j = ci_j in(j); h+ = g_j + g_{m-1-j}, h- = g_j - g_{m-1-j}; the middle row alone (its
+        // mirror loaded as 0: g + 0 and g - 0 are g); beyond the half (raw values 0) both are 0
+        const int j = k0s + jl;
+        const double cj = j < mh ? __ldg(ci + j) : 0.0, cm = j < mh ? __ldg(ci + (m - 1 - j)) : 0.0;
+        const double g = ra[2 * r] * cj, gm = ra[2 * r + 1] * cm;
+        AE[pl][jl] = g + gm;
+        AO[pl][jl] = g - gm;
       }
     }
 #pragma unroll
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
   double(*Bs)[ELD2] = grp ? BO : BE;
   load(0);
   for (int k0 = 0; k0 < K; k0 += EK) {
-    store();
+    store(k0);
     __syncthreads();
     if (k0 + EK < K) load(k0 + EK);
 #pragma unroll
