@@ -398,11 +398,21 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
   const int ntile = P.tiles * P.nboxes;
   // the tile's modes, every k at once, by 8-byte cp.async: this warp's share is rows k = warp,
   // warp + nwarp, ... in chunks of 32 rows-of-j; item i = (row i / nch, chunk i % nch)
-  const int nch = (TR + 31) >> 5, nitem = ((m - warp + nwarp - 1) / nwarp) * nch;
-  auto issue_item = [&](const double* __restrict__ src, double* As, int i) {
-    const int k = warp + nwarp * (i / nch), j = 32 * (i % nch) + lane;
-    const int row = (k & 1) ? kh + (k >> 1) : (k >> 1);
-    if (j < TR) cp_async8(As + row * LDA + j, src + static_cast<i64>(k) * m1 + j);
+  // The issue state walks (k, chunk) incrementally -- a division and a modulo by nch per item were
+  // 29 % of the kernel's instructions in the ncu source page -- and the shared address is formed
+  // from a 32-bit base instead of a generic-to-shared conversion per copy.
+  const int nch = (TR + 31) >> 5;
+  int ik = warp, ic = 0;
+  auto issue_item = [&](const double* __restrict__ src, unsigned as_s) {
+    const int j = 32 * ic + lane;
+    const int row = (ik & 1) ? kh + (ik >> 1) : (ik >> 1);
+    if (j < TR)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(as_s + 8u * static_cast<unsigned>(row * LDA + j)),
+                   "l"(src + static_cast<i64>(ik) * m1 + j));
+    if (++ic == nch) {
+      ic = 0;
+      ik += nwarp;
+    }
   };
   auto tile_src = [&](int tile) {
     const int box = tile / P.tiles, t = tile - box * P.tiles;
@@ -427,7 +437,8 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
   int tile = blockIdx.x;
   if (tile < ntile) {
     const double* __restrict__ src = tile_src(tile);
-    for (int i = 0; i < nitem; ++i) issue_item(src, Ab, i);
+    const unsigned ab_s = static_cast<unsigned>(__cvta_generic_to_shared(Ab));
+    while (ik < m) issue_item(src, ab_s);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   const int r8 = lane >> 2, c4 = lane & 3, r0 = 16 * (warp >> 1), nb0 = (warp & 1) * NTW;
@@ -438,8 +449,9 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     const double* __restrict__ nsrc = next < ntile ? tile_src(next) : nullptr;
-    double* An = Ab + (buf ^ 1) * KA * LDA;
-    int ni = 0;
+    const unsigned an_s = static_cast<unsigned>(__cvta_generic_to_shared(Ab + (buf ^ 1) * KA * LDA));
+    ik = warp;
+    ic = 0;
     const double* As = Ab + buf * KA * LDA + r0 + r8;
     const double* Bw = Bs + (8 * nb0 + r8) * LDB + c4;
     double E[2][NTW][2], O[2][NTW][2];
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
 #pragma unroll 2
     for (int ks = 0; ks < kh; ks += 4) {
       const double a0 = As[(ks + c4) * LDA], a1 = As[(ks + c4) * LDA + 8];
-      if (nsrc && ni < nitem) issue_item(nsrc, An, ni++);
+      if (nsrc && ik < m) issue_item(nsrc, an_s);
 #pragma unroll
       for (int b = 0; b < NTW; ++b) {
         const double fb = Bw[8 * b * LDB + ks];
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
 #pragma unroll 2
     for (int ks = 0; ks < P.no4; ks += 4) {
       const double a0 = As[(kh + ks + c4) * LDA], a1 = As[(kh + ks + c4) * LDA + 8];
-      if (nsrc && ni < nitem) issue_item(nsrc, An, ni++);
+      if (nsrc && ik < m) issue_item(nsrc, an_s);
 #pragma unroll
       for (int b = 0; b < NTW; ++b) {
         const double fb = Bw[8 * b * LDB + kh + ks];
@@ -470,7 +482,7 @@ __global__ void __launch_bounds__(512) strip_back_kernel(const double* __restric
       }
     }
     if (nsrc)
-      for (; ni < nitem; ++ni) issue_item(nsrc, An, ni);
+      while (ik < m) issue_item(nsrc, an_s);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     // out(q) = sc_q (E + O), out(m-1-q) = sc_{m-1-q} (E - O) straight from the accumulators
     const int box = tile / P.tiles, t = tile - box * P.tiles;

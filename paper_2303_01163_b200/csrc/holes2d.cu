@@ -362,23 +362,41 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // element order so the requests spread over the L2 slices instead of queueing on one line.
 __device__ __forceinline__ void stage_table(double* dst, const double* __restrict__ src, int rows, int cols, int ld,
                                             int S, int tid) {
+  // (row, column) advance by the thread count without a division per element: the stride's
+  // quotient and remainder once, then a carry; the rotation wraps at rows
   if ((cols & 1) == 0 && (ld & 1) == 0) {
     const int hc = cols >> 1, n = rows * hc;
     const int rot = static_cast<int>((blockIdx.x * 977u) % static_cast<unsigned>(n));
+    const int dr = kFusedThreads / hc, dc = kFusedThreads - dr * hc;
+    int t = tid + rot;
+    if (t >= n) t -= n;
+    int r = t / hc, c = t - r * hc;
     for (int t0 = tid; t0 < n; t0 += kFusedThreads) {
-      int t = t0 + rot;
-      if (t >= n) t -= n;
-      const int r = t / hc, c = 2 * (t - r * hc);
-      cp_async16(dst + r * S + c, src + static_cast<i64>(r) * ld + c);
+      cp_async16(dst + r * S + 2 * c, src + static_cast<i64>(r) * ld + 2 * c);
+      r += dr;
+      c += dc;
+      if (c >= hc) {
+        c -= hc;
+        ++r;
+      }
+      if (r >= rows) r -= rows;
     }
   } else {
     const int n = rows * cols;
     const int rot = static_cast<int>((blockIdx.x * 977u) % static_cast<unsigned>(n));
+    const int dr = kFusedThreads / cols, dc = kFusedThreads - dr * cols;
+    int t = tid + rot;
+    if (t >= n) t -= n;
+    int r = t / cols, c = t - r * cols;
     for (int t0 = tid; t0 < n; t0 += kFusedThreads) {
-      int t = t0 + rot;
-      if (t >= n) t -= n;
-      const int r = t / cols, c = t - r * cols;
       cp_async8(dst + r * S + c, src + static_cast<i64>(r) * ld + c);
+      r += dr;
+      c += dc;
+      if (c >= cols) {
+        c -= cols;
+        ++r;
+      }
+      if (r >= rows) r -= rows;
     }
   }
 }
