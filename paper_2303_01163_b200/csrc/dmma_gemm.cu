@@ -20,14 +20,32 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 __device__ __forceinline__ void line_base(const GemmLines& L, i64 p, i64& ib, i64& ob) {
-  const i64 o0 = p % L.o_ext[0];
-  i64 t = p / L.o_ext[0];
-  const i64 o1 = t % L.o_ext[1];
-  t /= L.o_ext[1];
-  const i64 h0 = t % L.nbox[0];
-  t /= L.nbox[0];
-  const i64 h1 = t % L.nbox[1];
-  const i64 h2 = t / L.nbox[1];
+  i64 o0, o1, h0, h1, h2;
+  if (L.nlines < (i64{1} << 31)) {  // 32-bit divisions: five 64-bit ones open every tile otherwise
+    const unsigned e0 = static_cast<unsigned>(L.o_ext[0]), e1 = static_cast<unsigned>(L.o_ext[1]);
+    const unsigned b0 = static_cast<unsigned>(L.nbox[0]), b1 = static_cast<unsigned>(L.nbox[1]);
+    unsigned t = static_cast<unsigned>(p), q = t / e0;
+    o0 = t - q * e0;
+    t = q;
+    q = t / e1;
+    o1 = t - q * e1;
+    t = q;
+    q = t / b0;
+    h0 = t - q * b0;
+    t = q;
+    q = t / b1;
+    h1 = t - q * b1;
+    h2 = q;
+  } else {
+    o0 = p % L.o_ext[0];
+    i64 t = p / L.o_ext[0];
+    o1 = t % L.o_ext[1];
+    t /= L.o_ext[1];
+    h0 = t % L.nbox[0];
+    t /= L.nbox[0];
+    h1 = t % L.nbox[1];
+    h2 = t / L.nbox[1];
+  }
   ib = h0 * L.in_bs[0] + h1 * L.in_bs[1] + h2 * L.in_bs[2] + o0 * L.o_in[0] + o1 * L.o_in[1];
   ob = h0 * L.out_bs[0] + h1 * L.out_bs[1] + h2 * L.out_bs[2] + o0 * L.o_out[0] + o1 * L.o_out[1];
 }
