@@ -110,8 +110,7 @@ __global__ void __launch_bounds__(NTH, ASDSM_DENSE_MINB) dmma_transform_kernel(c
     store();
     __syncthreads();
     if (k0 + BK < m) load(k0 + BK);
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    auto kstep = [&](int kk) {
       double a[4], b[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = As[wp + i * 8 + (lane >> 2)][kk + (lane & 3)];
@@ -121,6 +120,12 @@ __global__ void __launch_bounds__(NTH, ASDSM_DENSE_MINB) dmma_transform_kernel(c
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    };
+    if (k0 + BK <= m) {
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) kstep(kk);
+    } else {  // last tile: only the k groups that hold modes (the rest of the tile is zeros)
+      for (int kk = 0; k0 + kk < m; kk += 4) kstep(kk);
     }
     __syncthreads();
   }
@@ -318,8 +323,7 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
     store(k0);
     __syncthreads();
     if (k0 + EK < K) load(k0 + EK);
-#pragma unroll
-    for (int kk = 0; kk < EK; kk += 4) {
+    auto kstep = [&](int kk) {
       double fa[4], fb[NB];
 #pragma unroll
       for (int a = 0; a < 4; ++a) fa[a] = As[wp + a * 8 + r8][kk + c4];
@@ -329,6 +333,12 @@ __global__ void __launch_bounds__(ENT2, 2) dmma_eo2_kernel(const double* __restr
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < NB; ++b) dmma(acc[a][b], fa[a], fb[b]);
+    };
+    if (k0 + EK <= K) {
+#pragma unroll
+      for (int kk = 0; kk < EK; kk += 4) kstep(kk);
+    } else {  // last tile: only the k groups below K (the rest of the tile is zeros)
+      for (int kk = 0; k0 + kk < K; kk += 4) kstep(kk);
     }
     __syncthreads();
   }
