@@ -766,7 +766,8 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
     // Among the chunk sizes that fit, the one with the least modelled time: per chunk the
     // step-A rounds (8-row blocks over 16 warps), the step-B rounds ((plane, j tile, n quad)
     // tasks over 16 warps) and a fixed per-chunk cost (ring transforms, barriers), in the
-    // proportions measured at config 4 (clock64 trace: 4.9 / 6.3 / 9.5 k cycles).
+    // proportions measured at config 4 (clock64 trace of the round-2 kernel: 5.0 / 6.4 k cycles
+    // per round, 4.9 k per chunk; the line steps cost per plane, not per chunk).
     const int nty = (A.ay.he + 7) / 8, nq = ((mx + 7) / 8 + 3) / 4;
     double best = 1e300;
     for (int c = std::min(mt, tc_max); c >= 1; --c) {
@@ -777,7 +778,7 @@ bool hole3d_fused_plan(Hole3DFusedArgs& A, bool causal) {
       xs = std::max(xs, 2 * static_cast<size_t>(mx) * my + 2 * static_cast<size_t>(std::max(mx, my)) * (A.ax.he + A.ay.he));
       if (o + xs > kMax) continue;
       const int ra = (c * L.rp + 7) / 8, rb = c * nty * nq;
-      const double t = ((mt + c - 1) / c) * (4.9 * ((ra + kH3Warps - 1) / kH3Warps) + 6.3 * ((rb + kH3Warps - 1) / kH3Warps) + 9.5);
+      const double t = ((mt + c - 1) / c) * (5.0 * ((ra + kH3Warps - 1) / kH3Warps) + 6.4 * ((rb + kH3Warps - 1) / kH3Warps) + 4.9);
       if (t < best) {
         best = t;
         tc = c;
