@@ -394,8 +394,10 @@ def measure_config(cid, args, world, rank, local, flush, steps, warmup):
         share = c["ms_per_launch"] * c["launches_per_solve"] / ms
         if c["flops_per_launch"] > 0 and c["flops_per_launch"] / max(c["bytes_per_launch"], 1) > FP64_PEAK_TFLOPS * 1e3 / hbm:
             ach = c["flops_per_launch"] / (c["ms_per_launch"] / 1e3) / 1e12
+            tr = ncu_traffic(cid, c["name"], kernels)
             return {"kernel": c["name"], "bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None, "share_of_step": share,
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": tr["bytes"] if tr else None,
+                    "traffic_source": tr, "share_of_step": share,
                     "peak_source": "fp64 DMMA/DFMA peak measured with scripts/probe_fp64.cu (MEASURED_PEAKS has no "
                                    "fp64); flops are dense-equivalent (the even/odd split executes half)"}
         if c["bytes_per_launch"] < 1e6:
