@@ -211,6 +211,21 @@ __global__ void gather_kernel(const double* src0, const double* src1, double* ds
     fstride[a] = s;
     s *= a < m.dim ? m.nf[a] : 1;
   }
+  if (count < (i64{1} << 31)) {  // 32-bit index arithmetic (three 64-bit divisions per point otherwise)
+    const unsigned n = static_cast<unsigned>(count), e0 = ext[0], e1 = ext[1];
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+      const unsigned q0 = t / e0, i0 = t - q0 * e0, q1 = q0 / e1, i1 = q0 - q1 * e1, i2 = q1;
+      const unsigned ia[3] = {i0, i1, i2};
+      i64 f = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const i64 fi = ((mask >> a) & 1u) ? static_cast<i64>(ia[a] + 1) * m.n[a] - 1 : ia[a];
+        if (a < m.dim) f += fi * fstride[a];
+      }
+      dst[t] = src[f];
+    }
+    return;
+  }
   for (i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
        t += static_cast<i64>(gridDim.x) * blockDim.x) {
     i64 rem = t, f = 0;
@@ -563,7 +578,8 @@ void launch_ae_dots(int dim, const double* e, const double* r0, const double* r1
 void launch_gather(const double* src0, const double* src1, double* dst, const MeshDev& m, unsigned mask, i64 count,
                    DevState* state, cudaStream_t s) {
   const int bs = 256;
-  const i64 nb = std::min<i64>((count + bs - 1) / bs, 4 * kNumSms);
+  const int per_sm = std::getenv("ASDSM_GATHER_CTAS") ? std::atoi(std::getenv("ASDSM_GATHER_CTAS")) : 4;  // 8 and 12 measured the same
+  const i64 nb = std::min<i64>((count + bs - 1) / bs, static_cast<i64>(per_sm) * kNumSms);
   gather_kernel<<<static_cast<unsigned>(nb), bs, 0, s>>>(src0, src1, dst, m, mask, count, state);
   ASDSM_CUDA_CHECK(cudaGetLastError());
   ++g_kernel_launches;
