@@ -4,7 +4,7 @@
 // The hole rhs 0 - A_ff*skeleton lives on the hole's faces, so its forward transform is
 // face-sparse (holes3d.cu explains the split into YA / XB / CH).  Per hole:
 //   faces : ring values f from the skeleton, YA_f[t][l] = (Wy A_f(.,t))[l],
-//           XB_f[t][k] = (Wx B_f(.,t))[k], CH_f = Wx C_f Wy^T               (scalar FMAs, smem)
+//           XB_f[t][k] = (Wx B_f(.,t))[k], CH_f = Wx C_f Wy^T     (pair sums, then DMMA dots)
 //   lines : per mode pair (k,l) the Thomas solve along t of
 //           fhat(t) = Wx[k][0] YA_0 + Wx[k][m-1] YA_1 + Wy[l][0] XB_0 + Wy[l][m-1] XB_1 (+ CH at t=0, m-1)
 //   back  : per plane t, out = Vx X_t Vy^T as two DMMA GEMMs from shared memory.
@@ -21,7 +21,9 @@
 //          back transform of every plane;
 //   CAUSAL (backward time stencil: line_right == 0 -- the bidiagonal line has one pivot and no
 //          back substitution): planes are produced in t order, TC planes at a time, the line
-//          values ride in registers -- any hole depth.
+//          values ride in registers (thread (k, l0) owns the lines (k, l0 + G u)) -- any hole
+//          depth; per chunk: dots -> line steps -> step A -> step B, the next chunk's pair sums
+//          right behind step B (4 CTA barriers per chunk).
 // Replaces the faces / Thomas / two transform-GEMM launches (a 1 GB mode buffer written and read
 // twice at config 4) by one pass that writes every hole value once.
 #include "holes3d.cuh"
