@@ -61,3 +61,35 @@ def test_config4_hole_extent_m50_causal():
     ctx = _run("cfg:4:3", 101, 1, 10, 3)
     assert ctx.config.factors == [51, 51, 51]
     assert _has(ctx.kernels(), "hole3d_fused_kernel<true"), sorted(ctx.kernels())
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("cid", [3, 4])
+def test_full_size_3d_properties(cid):
+    """Size-independent properties on the BASELINE meshes themselves (259^3 and 509^3: out of the
+    CPU reference's reach).  The fill solves the hole rows exactly, so A e vanishes there
+    (solver.cpp:463-465) and the residual on hole rows stays at rounding level through the
+    updates; the optimal step is clamped at zero and rejected steps revert, so the residual
+    history never increases (solver.cpp:447-484, 634-657); the recorded norm is the norm of the
+    residual the solve returns."""
+    mesh, _ = pb.baseline_mesh(cid)
+    ctx = pb.SolverContext(mesh, pb.baseline_problem(cid, 0))
+    st = ctx.iterate(pb.IterateOptions(tol=0.0, max_iter=3, stagnation_window=0, rng_seed=0))
+    res = np.array([h.res_l2 for h in st.history])
+    assert len(res) == 4 and np.all(np.isfinite(res))
+    assert np.all(np.diff(res) <= 1e-12 * res[:-1]), res
+    assert res[-1] < res[0]
+    assert abs(np.linalg.norm(st.r) - res[-1]) <= 1e-12 * res[-1]
+    assert abs(np.max(np.abs(st.r)) - st.history[-1].res_inf) <= 1e-12 * st.history[-1].res_inf
+    holes = pb.hole_positions(mesh, ctx)
+    assert holes.size == 1000 * (mesh.factors[0] - 1) ** 3
+    on_holes = np.max(np.abs(st.r[holes]))
+    print(f"cfg {cid} {mesh.fine_counts}: res {res[0]:.3e} -> {res[-1]:.3e}, max |r| on hole rows {on_holes:.2e} of {np.max(np.abs(st.r)):.2e}")
+    # relative to the residual while it is above rounding level, else to the rounding level of a
+    # row of b - A u itself (eps x the row's absolute sum, bounded by 2 diag max|u|)
+    spike = np.zeros(ctx.fine_size())
+    spike[ctx.fine_size() // 2] = 1.0  # an interior point: b - (b - A e_p) is column p of A
+    abs_col = np.sum(np.abs(ctx.bundle["fine"] - ctx.residual(spike)))
+    row_scale = abs_col * np.max(np.abs(st.u)) + np.max(np.abs(ctx.bundle["fine"]))
+    print(f"row scale {row_scale:.3e}")
+    assert on_holes <= max(1e-9 * np.max(np.abs(st.r)), 64 * np.finfo(float).eps * row_scale)
